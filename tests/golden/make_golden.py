@@ -1,0 +1,226 @@
+"""Generate golden fixtures by running the REFERENCE itself (build container only).
+
+Usage (from the repo root, in the build container where /root/reference exists):
+
+    PYTHONDONTWRITEBYTECODE=1 NUMBA_CACHE_DIR=/tmp/numba_cache \
+        python tests/golden/make_golden.py
+
+Imports ``patchbeam`` from /root/reference/pkg/src (read-only; the env vars keep
+Numba's cache out of the reference tree) and writes small .npz files next to
+this script.  The fixtures pin oracle/ (tests/test_oracle_golden.py) and the
+CUDA path's index/bit-exact behaviour (tests/test_gpu_*.py).  Nothing on the
+GPU box reads /root/reference; it only reads these committed fixtures.
+
+Recorded environment goes into ``meta.json`` (numpy/numba/python versions).
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import platform
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def _import_reference():
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+    sys.dont_write_bytecode = True
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    import patchbeam  # noqa: F401
+    return patchbeam
+
+
+def extraction_cases(pb):
+    from patchbeam.patches import PatchSpec, coverage_map, extract_patches, reconstitute
+
+    rng = np.random.default_rng(20260101)
+    cases = [
+        ((4, 4), (2, 2), (2, 2), 1.0, False),
+        ((9, 11), (3, 3), (1, 1), 0.5, True),
+        ((10, 11), (3, 4), (2, 3), 0.3, True),
+        ((17,), (4,), (3,), 0.6, False),
+        ((6, 7, 5), (2, 3, 5), (1, 2, 1), 0.4, False),
+        ((5, 4, 3, 4), (2, 2, 3, 2), (1, 2, 1, 1), 0.5, True),
+        ((32, 32), (8, 8), (1, 1), 0.25, True),
+        ((5, 5), (2, 2), (2, 2), 1.0, True),      # uncovered margin
+        ((12, 12), (4, 4), (1, 1), 0.0, True),    # empty mask
+    ]
+    out = {}
+    for ci, (shape, patch, stride, ratio, ms) in enumerate(cases):
+        t = rng.random(shape)
+        mask = rng.random(shape) < ratio
+        pm = extract_patches(t, mask, PatchSpec(patch, stride), mean_subtract=ms)
+        est = rng.standard_normal(pm.values.shape)
+        rec = reconstitute(pm, est)
+        pre = f"c{ci}_"
+        out[pre + "tensor"] = t
+        out[pre + "mask"] = mask
+        out[pre + "patch"] = np.asarray(patch)
+        out[pre + "stride"] = np.asarray(stride)
+        out[pre + "mean_subtract"] = np.asarray(ms)
+        out[pre + "values"] = pm.values
+        out[pre + "observed"] = pm.observed
+        out[pre + "origins"] = pm.origins
+        out[pre + "means"] = pm.means
+        out[pre + "coverage"] = coverage_map(pm)
+        out[pre + "est"] = est
+        out[pre + "recon"] = rec
+    out["num_cases"] = np.asarray(len(cases))
+    np.savez_compressed(os.path.join(OUT, "extract_cases.npz"), **out)
+
+
+def _traj(pb, name, img_shape, patch, ratio, kind, k, epochs, seed, mask_seed,
+          mean_subtract=True, freeze=False, init_mode="data", initial=False, average_last=1):
+    from patchbeam import bpfa
+    from patchbeam.patches import PatchSpec, extract_patches
+    from patchbeam.sampling import SamplerSpec, make_mask
+    from patchbeam.sources import synthetic_texture
+
+    img = synthetic_texture(img_shape, seed=mask_seed)
+    mask = make_mask(SamplerSpec(kind=kind, ratio=ratio, seed=mask_seed), img.shape)
+    pm = extract_patches(img, mask, PatchSpec(patch), mean_subtract=mean_subtract)
+    hp = bpfa.Hyperparams(num_atoms=k)
+    if initial:
+        r = np.random.default_rng(seed + 99)
+        atoms = r.standard_normal((k, pm.patch_size))
+        atoms /= np.linalg.norm(atoms, axis=1, keepdims=True)
+        init = bpfa.Dictionary(atoms, r.uniform(0.2, 0.8, k), tuple(patch))
+        state = bpfa.install_dictionary(seed, pm, hp, init)
+        out_init = {"init_atoms": atoms, "init_pi": init.pi}
+    else:
+        state = bpfa.init_state(pm, hp, seed, init_mode=init_mode)
+        out_init = {}
+    rec = {"img": img, "mask": mask, "patch": np.asarray(patch), "k": np.asarray(k),
+           "seed": np.asarray(seed), "epochs": np.asarray(epochs),
+           "mean_subtract": np.asarray(mean_subtract), "freeze": np.asarray(freeze),
+           "init_mode": np.asarray(init_mode), "average_last": np.asarray(average_last),
+           "e0_atoms": state.dictionary.atoms.copy(), **out_init}
+    tail = None
+    for e in range(1, epochs + 1):
+        bpfa.gibbs_epoch(state, pm, hp, freeze_dict=freeze)
+        rec[f"e{e}_atoms"] = state.dictionary.atoms.copy()
+        rec[f"e{e}_pi"] = state.dictionary.pi.copy()
+        rec[f"e{e}_usage"] = state.usage.copy()
+        rec[f"e{e}_weights"] = state.weights.copy()
+        rec[f"e{e}_gammas"] = np.array([state.weight_precision, state.noise_precision])
+        if e > epochs - average_last:
+            est = bpfa.compose_estimates(state)
+            tail = est if tail is None else tail + est
+    rec["est"] = tail / average_last
+    from patchbeam.patches import apply_data_consistency, reconstitute
+    rec["recon"] = reconstitute(pm, rec["est"])
+    rec["recon_dc"] = apply_data_consistency(rec["recon"], img, mask, True)
+    np.savez_compressed(os.path.join(OUT, f"traj_{name}.npz"), **rec)
+
+
+def trajectories(pb):
+    _traj(pb, "small", (24, 24), (4, 4), 0.4, "uniform-random", 6, 4, 3, 5)
+    _traj(pb, "linehop", (32, 40), (8, 8), 0.25, "line-hop", 8, 3, 7, 2)
+    _traj(pb, "frozen", (20, 20), (5, 5), 0.3, "uniform-random", 4, 3, 11, 4,
+          freeze=True, initial=True)
+    _traj(pb, "avg", (16, 20), (3, 3), 0.5, "uniform-random", 5, 4, 13, 6,
+          mean_subtract=False, average_last=2, init_mode="prior")
+    _traj(pb, "cfg1crop", (48, 48), (8, 8), 0.25, "uniform-random", 16, 3, 0, 0)
+
+
+def masks(pb):
+    from patchbeam.sampling import SamplerSpec, make_mask
+    from patchbeam.sources import synthetic_texture
+
+    out = {}
+    specs = [((64, 64), 0.25, "uniform-random", 0), ((37, 53), 0.1, "uniform-random", 5),
+             ((512, 512), 0.25, "line-hop", 0), ((30, 17), 0.33, "line-hop", 3),
+             ((12, 10, 3), 0.2, "uniform-random", 1)]
+    for i, (shape, ratio, kind, seed) in enumerate(specs):
+        out[f"m{i}"] = make_mask(SamplerSpec(kind=kind, ratio=ratio, seed=seed), shape)
+        out[f"m{i}_spec"] = np.array([str(shape), str(ratio), kind, str(seed)])
+    out["tex_64_s0"] = synthetic_texture((64, 64), seed=0)
+    out["tex_40x56_s3_ph"] = synthetic_texture((40, 56), seed=3, phase=0.45)
+    np.savez_compressed(os.path.join(OUT, "masks.npz"), **out)
+
+
+def live(pb):
+    """Pipeline.submit_frame over 3 synthetic frames (warm start, K=8)."""
+    from patchbeam import bpfa
+    from patchbeam.pipeline import Pipeline, ProblemConfig
+    from patchbeam.patches import PatchSpec
+    from patchbeam.sampling import SamplerSpec
+    from patchbeam.sources import SyntheticSource
+
+    pipe = Pipeline()
+    cfg = ProblemConfig(name="p", patch_spec=PatchSpec((6, 6)),
+                        hyperparams=bpfa.Hyperparams(num_atoms=8),
+                        sampler_spec=SamplerSpec(kind="line-hop", ratio=0.25, seed=0),
+                        epochs_per_frame=2, seed=0)
+    h = pipe.create_problem(cfg)
+    src = SyntheticSource((32, 32), num_frames=3, seed=0)
+    out = {}
+    for t, frame in enumerate(src.frames()):
+        res = pipe.submit_frame(h, frame, ground_truth=frame)
+        out[f"f{t}_frame"] = frame
+        out[f"f{t}_recon"] = res.reconstruction
+        out[f"f{t}_mask"] = res.mask
+        out[f"f{t}_atoms"] = res.dictionary.atoms
+        out[f"f{t}_psnr"] = np.asarray(res.metrics.psnr_db)
+    np.savez_compressed(os.path.join(OUT, "live.npz"), **out)
+
+
+def posterior(pb):
+    """Conditional parameters on random states (reference helpers bpfa.py:189-235)."""
+    from patchbeam import bpfa
+    from patchbeam.patches import PatchSpec, extract_patches
+
+    rng = np.random.default_rng(77)
+    img = rng.random((10, 9))
+    mask = rng.random(img.shape) < 0.6
+    pm = extract_patches(img, mask, PatchSpec((3, 3)), mean_subtract=True)
+    hp = bpfa.Hyperparams(num_atoms=5, concentration_a=1.3, concentration_b=0.7,
+                          weight_shape=1.1, weight_rate=0.9, noise_shape=1.5, noise_rate=0.6)
+    st = bpfa.init_state(pm, hp, seed=4, init_mode="prior")
+    n, k = st.usage.shape
+    st.usage[:] = rng.random((n, k)) < 0.5
+    st.weights[:] = rng.standard_normal((n, k))
+    st.dictionary.atoms[:] = rng.standard_normal(st.dictionary.atoms.shape)
+    st.dictionary.pi = rng.uniform(0.05, 0.95, size=k)
+    st.weight_precision = 1.7
+    st.noise_precision = 23.0
+    out = {"img": img, "mask": mask, "usage": st.usage, "weights": st.weights,
+           "atoms": st.dictionary.atoms, "pi": st.dictionary.pi,
+           "gammas": np.array([st.weight_precision, st.noise_precision])}
+    for kk in range(k):
+        lam, mu = bpfa.atom_posterior(pm, st, kk)
+        lr, al, me = bpfa.code_posterior(pm, st, kk)
+        out[f"k{kk}_lam"], out[f"k{kk}_mu"] = lam, mu
+        out[f"k{kk}_logrho"], out[f"k{kk}_alpha"], out[f"k{kk}_mean"] = lr, al, me
+    a, b = bpfa.pi_posterior(st, hp)
+    (ws, wr), (ns, nr) = bpfa.gamma_posteriors(pm, st, hp)
+    out["pi_a"], out["pi_b"] = a, b
+    out["gamma_post"] = np.array([ws, wr, ns, nr])
+    np.savez_compressed(os.path.join(OUT, "posterior.npz"), **out)
+
+
+def main():
+    pb = _import_reference()
+    import numba
+
+    extraction_cases(pb)
+    trajectories(pb)
+    masks(pb)
+    live(pb)
+    posterior(pb)
+    meta = {"python": platform.python_version(), "numpy": np.__version__,
+            "numba": numba.__version__, "reference": REF,
+            "note": "generated by running the reference patchbeam package itself"}
+    with open(os.path.join(OUT, "meta.json"), "w") as f:
+        json.dump(meta, f, indent=1)
+    print("golden fixtures written to", OUT)
+
+
+if __name__ == "__main__":
+    main()
