@@ -1,0 +1,182 @@
+/*
+ * pb200 — C ABI of the B200-native BPFA inpainting hot path.
+ *
+ * Drop-in boundary for reference pkg/src/patchbeam (arXiv 2311.15061 "SenseAI").
+ * The reference is Python; its own native seam is the Numba kernel module
+ * (_kernels.py) that bpfa.py calls through the module object (bpfa.py:30), plus
+ * the Python entry points patches.extract_patches / reconstitute and
+ * bpfa.gibbs_epoch / compose_estimates / infer.  Each entry point below names
+ * the reference function it replaces.  The ctypes binding that mirrors the
+ * reference API lives in paper_2311_15061_b200/ (see INTEGRATION.md).
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers unless a name ends in `_host`.
+ *  - Plane-major device layouts: values/observed/resid/estimates are (P, N)
+ *    ([p*N + i]); usage (uint8 0/1) and weights are (K, N); atoms are (K, P).
+ *    This is the transpose of the reference's row-major (N, P)/(N, K) arrays.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).
+ *  - Every function returns PB_OK (0) or a negative PB_E* code; the message of
+ *    the last failure on the calling thread is pb_last_error().
+ *  - Nothing here falls back to the CPU: without a CUDA device every compute
+ *    entry point fails with PB_ECUDA.
+ */
+#ifndef PB200_H_
+#define PB200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PB_OK 0
+#define PB_ESHAPE -1       /* patchbeam.patches.ShapeError          (patches.py:20-21) */
+#define PB_EVALUE -2       /* ValueError (bad hyperparameters etc.)  (bpfa.py:54-60)    */
+#define PB_ECOVERAGE -3    /* patchbeam.patches.CoverageError       (patches.py:24-25) */
+#define PB_EDIVERGED -4    /* patchbeam.bpfa.DivergenceError         (bpfa.py:38-39)    */
+#define PB_ECUDA -5        /* CUDA runtime failure / no device                           */
+#define PB_EUNSUPPORTED -6 /* shape outside the compiled kernel envelope                 */
+
+#define PB_RNG_REPLAY 0    /* draws supplied by the caller (reference numpy streams) */
+#define PB_RNG_PHILOX 1    /* device counter-based Philox4x32-10 draws               */
+
+const char* pb_last_error(void);
+int pb_version(void);
+int pb_device_count(void);
+
+/* Patch grid: rank 1..4, tensor shape M, patch shape B, stride s (patches.py:35-77). */
+typedef struct pb_grid_desc {
+  int32_t rank;
+  int64_t tensor_shape[4];
+  int32_t patch_shape[4];
+  int32_t stride[4];
+} pb_grid_desc;
+
+/* PatchSpec.grid_counts / num_patches / patch_size (patches.py:64-77).
+ * Validates like PatchSpec.validate_for (patches.py:54-62): PB_ESHAPE on error. */
+int pb_grid_counts(const pb_grid_desc* g, int64_t* counts_out, int64_t* num_patches, int32_t* patch_size);
+
+/* extract_patches (patches.py:125-164).  tensor: f32 (tensor_f64=0) or f64 device
+ * array of the tensor shape; mask: uint8.  Outputs (P,N) values, (P,N) observed,
+ * (N) means (0 unless mean_subtract), (N) observed counts. */
+int pb_extract_patches(const pb_grid_desc* g, const void* tensor, int32_t tensor_f64, const uint8_t* mask,
+                       int32_t mean_subtract, float* values, uint8_t* observed, float* means,
+                       int32_t* counts, void* stream);
+
+/* reconstitute + apply_data_consistency (patches.py:188-229).
+ * out[x] = sum_{i covers x} (est_scale*est[p,i] + means[i]) / coverage(x);
+ * if dc: out[x] = original[x] where mask[x].  out/original are f64 if io_f64 else f32.
+ * uncovered (device uint64, may be NULL) is incremented per uncovered element. */
+int pb_reconstitute(const pb_grid_desc* g, const float* est, float est_scale, const float* means,
+                    const void* original, const uint8_t* mask, int32_t dc, int32_t io_f64, void* out,
+                    unsigned long long* uncovered, void* stream);
+
+/* coverage_map (patches.py:181-185), int32 of the tensor shape. */
+int pb_coverage_map(const pb_grid_desc* g, int32_t* out, void* stream);
+
+/* ---- fine-grained seam: one entry per reference _kernels.* function ---- */
+
+/* _kernels.residual_full (_kernels.py:18-31) */
+int pb_residual_full(const float* values, const uint8_t* observed, const uint8_t* usage, const float* weights,
+                     const float* atoms, float* out, int64_t n, int32_t p, int32_t k, void* stream);
+/* _kernels.compose_estimates (_kernels.py:133-145); accumulate!=0 adds into out. */
+int pb_compose_estimates(const uint8_t* usage, const float* weights, const float* atoms, float* out, int64_t n,
+                         int32_t p, int32_t k, int32_t accumulate, void* stream);
+/* _kernels.atom_moments (_kernels.py:34-62): a_out, c_out are device f64[P];
+ * scratch: device f64[2 * P * 64]. */
+int pb_atom_moments(const float* resid, const uint8_t* observed, const float* w_col, int64_t n, int32_t p,
+                    double* a_out, double* c_out, double* scratch, void* stream);
+/* _kernels.shift_atom (_kernels.py:65-74) */
+int pb_shift_atom(float* resid, const uint8_t* observed, const float* w_col, const float* delta, int64_t n,
+                  int32_t p, void* stream);
+/* _kernels.code_moments (_kernels.py:77-97) */
+int pb_code_moments(const float* resid, const uint8_t* observed, const float* atom, int64_t n, int32_t p,
+                    float* u_out, float* v_out, void* stream);
+/* _kernels.shift_codes (_kernels.py:100-109) */
+int pb_shift_codes(float* resid, const uint8_t* observed, const float* atom, const float* dw, int64_t n,
+                   int32_t p, void* stream);
+/* _kernels.masked_sq_norm (_kernels.py:112-130): out = device f64 scalar; scratch f64[256]. */
+int pb_masked_sq_norm(const float* resid, int64_t total, double* out, double* scratch, void* stream);
+
+/* ---- the sweep: bpfa.gibbs_epoch (bpfa.py:278-345) ---- */
+
+/* Device-resident scalar block of a sampler state (layout fixed, 40 bytes). */
+typedef struct pb_scalars {
+  double gamma_s;    /* GibbsState.weight_precision */
+  double gamma_eps;  /* GibbsState.noise_precision  */
+  double sq_w;       /* sum of S^2 after the last code step  */
+  double sq_r;       /* sum of R^2 after the last code step  */
+  int32_t epoch;     /* GibbsState.epoch */
+  int32_t diverged;  /* set by the device pi/gamma draw on non-finite state */
+} pb_scalars;
+
+typedef struct pb_epoch_desc {
+  int64_t n;
+  int32_t p, k;
+  int32_t freeze_dict;      /* bpfa.gibbs_epoch(freeze_dict=...) */
+  int32_t rng_mode;         /* PB_RNG_REPLAY or PB_RNG_PHILOX */
+  uint64_t seed;            /* GibbsState.seed */
+  int64_t n_obs;            /* number of observed patch-matrix flags (bpfa.py:327) */
+  double hyper[6];          /* Hyperparams a, b, c, d, e, f (bpfa.py:46-52) */
+  /* problem */
+  const float* values;      /* (P,N) */
+  const uint8_t* observed;  /* (P,N) */
+  /* state (in/out) */
+  float* atoms;             /* (K,P) */
+  double* pi;               /* (K)   */
+  uint8_t* usage;           /* (K,N) */
+  float* weights;           /* (K,N) */
+  pb_scalars* scalars;
+  /* replay draws for this epoch (PB_RNG_REPLAY only; else NULL) */
+  const double* atom_draws; /* (K,P) standard normals, stream (seed,2,epoch,k) */
+  const double* code_u;     /* (K,N) uniforms, stream (seed,3,epoch,k) random(N) */
+  const double* code_g;     /* (K,N) normals,  stream (seed,3,epoch,k) standard_normal(N) */
+  /* workspace from pb_epoch_workspace_bytes() */
+  void* workspace;
+} pb_epoch_desc;
+
+size_t pb_epoch_workspace_bytes(int64_t n, int32_t p, int32_t k);
+
+/* One sweep through the dictionary and code steps.  After it returns (stream
+ * ordered), scalars->sq_w / sq_r hold the epoch sums and m_counts_out (device
+ * int32[K], may be NULL) the per-atom usage counts.  In PB_RNG_PHILOX mode the
+ * pi / gamma draws also run on the device (scalars->epoch advances, diverged
+ * flags non-finite state); in PB_RNG_REPLAY mode the caller draws pi/gamma from
+ * the reference streams and calls pb_epoch_commit. */
+int pb_gibbs_epoch(const pb_epoch_desc* d, int32_t* m_counts_out, void* stream);
+
+/* ---- stateful problem (C-ABI with HOST buffers; the live submit_frame slice,
+ *      pipeline.py:217-251).  Owns all device buffers. ---- */
+typedef struct pb_problem pb_problem;
+
+typedef struct pb_problem_desc {
+  pb_grid_desc grid;
+  int32_t num_atoms;
+  double hyper[6];
+  uint64_t seed;
+  int32_t mean_subtract;
+  int32_t epochs_per_frame;
+  int32_t freeze_dict;
+  int32_t data_consistency;
+  int32_t warm_start;
+  int32_t average_last;
+} pb_problem_desc;
+
+int pb_problem_create(const pb_problem_desc* desc, pb_problem** out);
+int pb_problem_destroy(pb_problem* pr);
+/* One live frame: H2D frame (f64) + mask (uint8, cached when unchanged),
+ * extract, epochs_per_frame warm-started sweeps (device RNG), compose, overlap-add,
+ * data consistency, D2H reconstruction (f64).  Mirrors Pipeline.submit_frame's
+ * hot slice (pipeline.py:224-251). */
+int pb_problem_submit_frame(pb_problem* pr, const double* frame_host, const uint8_t* mask_host,
+                            double* recon_host);
+/* Device-side timing of the last submit_frame's GPU work (ms). */
+float pb_problem_last_gpu_ms(pb_problem* pr);
+/* Current dictionary (K,P) f32 and scalars, copied to host. */
+int pb_problem_get_dictionary(pb_problem* pr, float* atoms_host, double* pi_host, pb_scalars* scalars_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PB200_H_ */

@@ -1,0 +1,397 @@
+// pb200 — C ABI (include/pb200.h) over the sm_100a kernels, plus the native
+// stateful "problem" used for the host-buffer live-frame path.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <vector>
+
+#include "../../include/pb200.h"
+#include "pb_sweep.cuh"
+
+namespace pb {
+
+// ---- error state ----------------------------------------------------------
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+const char* last_error() { return g_err; }
+
+static int make_grid(const pb_grid_desc* d, Grid& g) {
+  if (!d) { set_error("null grid"); return PB_EVALUE; }
+  if (d->rank < 1 || d->rank > kMaxRank) { set_error("tensor rank must be 1..4, got %d", d->rank); return PB_ESHAPE; }
+  g.rank = d->rank;
+  g.n = 1; g.p = 1; g.m = 1;
+  for (int i = 0; i < d->rank; ++i) {
+    const int64_t m = d->tensor_shape[i];
+    const int b = d->patch_shape[i], s = d->stride[i];
+    if (m < 1) { set_error("tensor dims must be >= 1"); return PB_ESHAPE; }
+    if (b < 1) { set_error("patch dims must be >= 1"); return PB_ESHAPE; }
+    if (s < 1) { set_error("strides must be >= 1"); return PB_ESHAPE; }
+    if (b > m) { set_error("patch shape exceeds tensor in dim %d (%d > %lld)", i, b, (long long)m); return PB_ESHAPE; }
+    g.tshape[i] = m; g.bshape[i] = b; g.step[i] = s;
+    g.gcount[i] = (m - b) / s + 1;
+    g.n *= g.gcount[i]; g.p *= b; g.m *= m;
+  }
+  int64_t acc = 1;
+  for (int i = d->rank - 1; i >= 0; --i) { g.tstride[i] = acc; acc *= g.tshape[i]; }
+  return PB_OK;
+}
+
+// Epoch workspace carve-up
+struct EpochWs {
+  float* resid;
+  double* partials;
+  float* delta;
+  unsigned int* sync;
+  double* block_sums;
+  int32_t* m_count;
+};
+static const int kMaxDictBlocks = 148 * 4;
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+static size_t code_blocks_upper(int64_t n, int p) {
+  int g = 1;
+  while ((p + g - 1) / g > 64 && g < 32) g *= 2;
+  return (size_t)ceil_div(n * g, 256);
+}
+static size_t ws_bytes(int64_t n, int p, int k, EpochWs* ws, char* base) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return base ? base + o : nullptr; };
+  char* r = take((size_t)n * p * 4);
+  char* pa = take((size_t)kMaxDictBlocks * 2 * p * 8);
+  char* dl = take((size_t)p * 4);
+  char* sy = take(16);
+  char* bs = take(code_blocks_upper(n, p) * 2 * 8);
+  char* mc = take((size_t)k * 4);
+  if (ws) {
+    ws->resid = (float*)r; ws->partials = (double*)pa; ws->delta = (float*)dl;
+    ws->sync = (unsigned int*)sy; ws->block_sums = (double*)bs; ws->m_count = (int32_t*)mc;
+  }
+  return off;
+}
+
+static void device_key(uint64_t seed, uint32_t& k0, uint32_t& k1) {
+  // splitmix64 of the seed; the Python side uses the same derivation only as a
+  // label — device draws are keyed solely by this pair.
+  uint64_t z = seed + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  k0 = (uint32_t)z;
+  k1 = (uint32_t)(z >> 32);
+}
+
+static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
+  if (d->n < 1 || d->p < 1 || d->k < 1) { set_error("empty problem"); return PB_ESHAPE; }
+  if (d->rng_mode == PB_RNG_REPLAY && (!d->code_u || !d->code_g || (!d->freeze_dict && !d->atom_draws))) {
+    set_error("replay mode needs atom_draws, code_u and code_g");
+    return PB_EVALUE;
+  }
+  EpochWs ws;
+  ws_bytes(d->n, d->p, d->k, &ws, (char*)d->workspace);
+  if (m_out) ws.m_count = m_out;
+  uint32_t k0, k1;
+  device_key(d->seed, k0, k1);
+  SweepScalars* sc = (SweepScalars*)d->scalars;
+  int rc = launch_accumulate_atoms(true, d->values, d->observed, d->usage, d->weights, d->atoms, ws.resid, d->n, d->p,
+                                   d->k, 0, st);
+  if (rc) return rc;
+  if (!d->freeze_dict) {
+    int blocks, threads, tile;
+    size_t smem;
+    if ((rc = dict_step_grid(d->p, blocks, threads, smem, tile))) return rc;
+    if (blocks > kMaxDictBlocks) blocks = kMaxDictBlocks;
+    DictArgs a{ws.resid, d->observed, d->usage, d->weights, d->atoms,
+               d->rng_mode == PB_RNG_REPLAY ? d->atom_draws : nullptr,
+               sc, ws.partials, ws.delta, ws.sync, d->n, d->p, d->k, tile, k0, k1};
+    if ((rc = launch_dict_step(a, blocks, threads, smem, st))) return rc;
+  }
+  CodeArgs c{ws.resid, d->observed, d->usage, d->weights, d->atoms, d->pi,
+             d->rng_mode == PB_RNG_REPLAY ? d->code_u : nullptr,
+             d->rng_mode == PB_RNG_REPLAY ? d->code_g : nullptr,
+             sc, ws.block_sums, ws.m_count, d->n, d->p, d->k, 0, k0, k1};
+  int nblocks = 0;
+  if ((rc = launch_code_step(c, d->rng_mode, nblocks, st))) return rc;
+  if ((rc = launch_finish_stats(ws.block_sums, nblocks, sc, st))) return rc;
+  if (d->rng_mode == PB_RNG_PHILOX)
+    rc = launch_draw_pi_gamma(d->pi, ws.m_count, sc, d->k, d->n, d->n_obs, d->hyper, k0, k1, st);
+  return rc;
+}
+
+}  // namespace pb
+
+using namespace pb;
+
+extern "C" {
+
+const char* pb_last_error(void) { return last_error(); }
+int pb_version(void) { return 1; }
+int pb_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+  return c;
+}
+
+int pb_grid_counts(const pb_grid_desc* d, int64_t* counts_out, int64_t* num_patches, int32_t* patch_size) {
+  Grid g;
+  int rc = make_grid(d, g);
+  if (rc) return rc;
+  for (int i = 0; i < g.rank; ++i)
+    if (counts_out) counts_out[i] = g.gcount[i];
+  if (num_patches) *num_patches = g.n;
+  if (patch_size) *patch_size = g.p;
+  return PB_OK;
+}
+
+int pb_extract_patches(const pb_grid_desc* d, const void* tensor, int32_t tensor_f64, const uint8_t* mask,
+                       int32_t mean_subtract, float* values, uint8_t* observed, float* means, int32_t* counts,
+                       void* stream) {
+  Grid g;
+  int rc = make_grid(d, g);
+  if (rc) return rc;
+  return launch_extract(g, tensor, tensor_f64, mask, mean_subtract, values, observed, means, counts,
+                        (cudaStream_t)stream);
+}
+
+int pb_reconstitute(const pb_grid_desc* d, const float* est, float est_scale, const float* means,
+                    const void* original, const uint8_t* mask, int32_t dc, int32_t io_f64, void* out,
+                    unsigned long long* uncovered, void* stream) {
+  Grid g;
+  int rc = make_grid(d, g);
+  if (rc) return rc;
+  return launch_reconstitute(g, est, est_scale, means, original, mask, dc, io_f64, out, uncovered,
+                             (cudaStream_t)stream);
+}
+
+int pb_coverage_map(const pb_grid_desc* d, int32_t* out, void* stream) {
+  Grid g;
+  int rc = make_grid(d, g);
+  if (rc) return rc;
+  return launch_coverage(g, out, (cudaStream_t)stream);
+}
+
+int pb_residual_full(const float* values, const uint8_t* observed, const uint8_t* usage, const float* weights,
+                     const float* atoms, float* out, int64_t n, int32_t p, int32_t k, void* stream) {
+  return launch_accumulate_atoms(true, values, observed, usage, weights, atoms, out, n, p, k, 0, (cudaStream_t)stream);
+}
+
+int pb_compose_estimates(const uint8_t* usage, const float* weights, const float* atoms, float* out, int64_t n,
+                         int32_t p, int32_t k, int32_t accumulate, void* stream) {
+  return launch_accumulate_atoms(false, nullptr, nullptr, usage, weights, atoms, out, n, p, k, accumulate,
+                                 (cudaStream_t)stream);
+}
+
+int pb_atom_moments(const float* resid, const uint8_t* observed, const float* w_col, int64_t n, int32_t p,
+                    double* a_out, double* c_out, double* scratch, void* stream) {
+  return launch_atom_moments(resid, observed, w_col, n, p, scratch, 64, a_out, c_out, (cudaStream_t)stream);
+}
+
+int pb_shift_atom(float* resid, const uint8_t* observed, const float* w_col, const float* delta, int64_t n,
+                  int32_t p, void* stream) {
+  return launch_shift_atom(resid, observed, w_col, delta, n, p, (cudaStream_t)stream);
+}
+
+int pb_code_moments(const float* resid, const uint8_t* observed, const float* atom, int64_t n, int32_t p,
+                    float* u_out, float* v_out, void* stream) {
+  return launch_code_moments(resid, observed, atom, n, p, u_out, v_out, (cudaStream_t)stream);
+}
+
+int pb_shift_codes(float* resid, const uint8_t* observed, const float* atom, const float* dw, int64_t n, int32_t p,
+                   void* stream) {
+  return launch_shift_codes(resid, observed, atom, dw, n, p, (cudaStream_t)stream);
+}
+
+int pb_masked_sq_norm(const float* resid, int64_t total, double* out, double* scratch, void* stream) {
+  return launch_sq_norm(resid, total, scratch, 256, out, (cudaStream_t)stream);
+}
+
+size_t pb_epoch_workspace_bytes(int64_t n, int32_t p, int32_t k) { return ws_bytes(n, p, k, nullptr, nullptr); }
+
+int pb_gibbs_epoch(const pb_epoch_desc* d, int32_t* m_counts_out, void* stream) {
+  if (!d) { set_error("null epoch desc"); return PB_EVALUE; }
+  return run_epoch(d, m_counts_out, (cudaStream_t)stream);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Native stateful problem: the live submit_frame hot slice with host buffers
+// (pipeline.py:224-251), device RNG, warm start (codes re-burn each frame;
+// dictionary, pi and precisions carry over, pipeline.py:230-238).
+
+struct pb_problem {
+  pb_problem_desc desc;
+  pb::Grid grid;
+  int64_t n = 0;
+  int p = 0, k = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double* frame = nullptr;
+  uint8_t* mask = nullptr;
+  float *values = nullptr, *means = nullptr, *atoms = nullptr, *weights = nullptr, *est = nullptr;
+  uint8_t *obs = nullptr, *usage = nullptr;
+  int32_t *counts = nullptr, *m_count = nullptr;
+  double *pi = nullptr, *recon = nullptr;
+  pb_scalars* scalars = nullptr;
+  unsigned long long* nobs_dev = nullptr;
+  void* ws = nullptr;
+  std::vector<uint8_t> mask_cache;
+  int64_t n_obs = 0;
+  bool have_state = false;
+  float last_ms = 0.f;
+};
+
+namespace {
+template <typename T>
+int dalloc(T** p, size_t count) {
+  PB_CUDA_TRY(cudaMalloc((void**)p, count * sizeof(T) + 16));
+  return PB_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int pb_problem_destroy(pb_problem* pr) {
+  if (!pr) return PB_OK;
+  void* bufs[] = {pr->frame, pr->mask, pr->values, pr->means, pr->atoms, pr->weights, pr->est, pr->obs, pr->usage,
+                  pr->counts, pr->m_count, pr->pi, pr->recon, pr->scalars, pr->nobs_dev, pr->ws};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (pr->ev0) cudaEventDestroy(pr->ev0);
+  if (pr->ev1) cudaEventDestroy(pr->ev1);
+  if (pr->stream) cudaStreamDestroy(pr->stream);
+  delete pr;
+  return PB_OK;
+}
+
+int pb_problem_create(const pb_problem_desc* desc, pb_problem** out) {
+  if (!desc || !out) { set_error("null argument"); return PB_EVALUE; }
+  if (desc->num_atoms < 1) { set_error("num_atoms must be >= 1"); return PB_EVALUE; }
+  if (desc->epochs_per_frame < 1) { set_error("epochs_per_frame must be >= 1"); return PB_EVALUE; }
+  for (int j = 0; j < 6; ++j)
+    if (!(desc->hyper[j] > 0)) { set_error("hyperparameters must be > 0"); return PB_EVALUE; }
+  pb_problem* pr = new pb_problem();
+  pr->desc = *desc;
+  int rc = make_grid(&desc->grid, pr->grid);
+  if (rc) { delete pr; return rc; }
+  pr->n = pr->grid.n; pr->p = pr->grid.p; pr->k = desc->num_atoms;
+  const int64_t m = pr->grid.m, n = pr->n, p = pr->p, k = pr->k;
+#define PB_A(ptr, cnt) if ((rc = dalloc(&pr->ptr, (size_t)(cnt)))) { pb_problem_destroy(pr); return rc; }
+  PB_A(frame, m) PB_A(mask, m) PB_A(values, p * n) PB_A(obs, p * n) PB_A(means, n) PB_A(counts, n)
+  PB_A(atoms, k * p) PB_A(pi, k) PB_A(usage, k * n) PB_A(weights, k * n) PB_A(est, p * n) PB_A(recon, m)
+  PB_A(m_count, k) PB_A(scalars, 1) PB_A(nobs_dev, 1)
+  char* wsp = nullptr;
+  if ((rc = dalloc(&wsp, pb_epoch_workspace_bytes(n, (int)p, (int)k)))) { pb_problem_destroy(pr); return rc; }
+  pr->ws = wsp;
+#undef PB_A
+  if (cudaStreamCreateWithFlags(&pr->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&pr->ev0) != cudaSuccess || cudaEventCreate(&pr->ev1) != cudaSuccess) {
+    set_error("stream/event creation failed");
+    pb_problem_destroy(pr);
+    return PB_ECUDA;
+  }
+  *out = pr;
+  return PB_OK;
+}
+
+static int problem_cold_init(pb_problem* pr) {
+  // init_state(prior) on device (bpfa.py:121-149): prior atoms, pi = a/(a+b),
+  // gammas at their prior means, Z = S = 0, epoch 0.  (Data-mode seeding only
+  // matters with freeze_dict; see infer() in bpfa.py of this package.)
+  uint32_t k0, k1;
+  device_key(pr->desc.seed, k0, k1);
+  int rc = launch_prior_atoms(pr->atoms, pr->k, pr->p, k0, k1, pr->stream);
+  if (rc) return rc;
+  std::vector<double> pi(pr->k, pr->desc.hyper[0] / (pr->desc.hyper[0] + pr->desc.hyper[1]));
+  PB_CUDA_TRY(cudaMemcpyAsync(pr->pi, pi.data(), pr->k * sizeof(double), cudaMemcpyHostToDevice, pr->stream));
+  pb_scalars s{};
+  s.gamma_s = fmax(pr->desc.hyper[2] / pr->desc.hyper[3], 1e-12);
+  s.gamma_eps = fmax(pr->desc.hyper[4] / pr->desc.hyper[5], 1e-12);
+  PB_CUDA_TRY(cudaMemcpyAsync(pr->scalars, &s, sizeof(s), cudaMemcpyHostToDevice, pr->stream));
+  PB_CUDA_TRY(cudaStreamSynchronize(pr->stream));  // s/pi live on this stack frame
+  pr->have_state = true;
+  return PB_OK;
+}
+
+int pb_problem_submit_frame(pb_problem* pr, const double* frame_host, const uint8_t* mask_host,
+                            double* recon_host) {
+  if (!pr || !frame_host || !mask_host || !recon_host) { set_error("null argument"); return PB_EVALUE; }
+  const int64_t m = pr->grid.m, n = pr->n;
+  cudaStream_t st = pr->stream;
+  PB_CUDA_TRY(cudaEventRecord(pr->ev0, st));
+  PB_CUDA_TRY(cudaMemcpyAsync(pr->frame, frame_host, m * sizeof(double), cudaMemcpyHostToDevice, st));
+  const bool new_mask = pr->mask_cache.size() != (size_t)m || memcmp(pr->mask_cache.data(), mask_host, m) != 0;
+  if (new_mask) {
+    pr->mask_cache.assign(mask_host, mask_host + m);
+    PB_CUDA_TRY(cudaMemcpyAsync(pr->mask, pr->mask_cache.data(), m, cudaMemcpyHostToDevice, st));
+  }
+  int rc = launch_extract(pr->grid, pr->frame, 1, pr->mask, pr->desc.mean_subtract, pr->values, pr->obs, pr->means,
+                          pr->counts, st);
+  if (rc) return rc;
+  if (new_mask) {
+    if ((rc = launch_sum_counts(pr->counts, n, pr->nobs_dev, st))) return rc;
+    unsigned long long nobs = 0;
+    PB_CUDA_TRY(cudaMemcpyAsync(&nobs, pr->nobs_dev, sizeof(nobs), cudaMemcpyDeviceToHost, st));
+    PB_CUDA_TRY(cudaStreamSynchronize(st));
+    pr->n_obs = (int64_t)nobs;
+  }
+  if (!pr->have_state || !pr->desc.warm_start) {
+    if ((rc = problem_cold_init(pr))) return rc;
+  }
+  PB_CUDA_TRY(cudaMemsetAsync(pr->usage, 0, (size_t)pr->k * n, st));
+  PB_CUDA_TRY(cudaMemsetAsync(pr->weights, 0, (size_t)pr->k * n * sizeof(float), st));
+  pb_epoch_desc d{};
+  d.n = n; d.p = pr->p; d.k = pr->k;
+  d.freeze_dict = pr->desc.freeze_dict;
+  d.rng_mode = PB_RNG_PHILOX;
+  d.seed = pr->desc.seed;
+  d.n_obs = pr->n_obs;
+  for (int j = 0; j < 6; ++j) d.hyper[j] = pr->desc.hyper[j];
+  d.values = pr->values; d.observed = pr->obs; d.atoms = pr->atoms; d.pi = pr->pi;
+  d.usage = pr->usage; d.weights = pr->weights; d.scalars = pr->scalars; d.workspace = pr->ws;
+  const int epochs = pr->desc.epochs_per_frame;
+  int tail = pr->desc.average_last < 1 ? 1 : (pr->desc.average_last > epochs ? epochs : pr->desc.average_last);
+  for (int e = 0; e < epochs; ++e) {
+    if ((rc = run_epoch(&d, pr->m_count, st))) return rc;
+    if (e >= epochs - tail) {
+      rc = launch_accumulate_atoms(false, nullptr, nullptr, pr->usage, pr->weights, pr->atoms, pr->est, n, pr->p,
+                                   pr->k, e > epochs - tail ? 1 : 0, st);
+      if (rc) return rc;
+    }
+  }
+  rc = launch_reconstitute(pr->grid, pr->est, 1.0f / (float)tail, pr->means, pr->frame, pr->mask,
+                           pr->desc.data_consistency, 1, pr->recon, nullptr, st);
+  if (rc) return rc;
+  PB_CUDA_TRY(cudaMemcpyAsync(recon_host, pr->recon, m * sizeof(double), cudaMemcpyDeviceToHost, st));
+  pb_scalars s;
+  PB_CUDA_TRY(cudaMemcpyAsync(&s, pr->scalars, sizeof(s), cudaMemcpyDeviceToHost, st));
+  PB_CUDA_TRY(cudaEventRecord(pr->ev1, st));
+  PB_CUDA_TRY(cudaStreamSynchronize(st));
+  cudaEventElapsedTime(&pr->last_ms, pr->ev0, pr->ev1);
+  if (s.diverged) {
+    set_error("non-finite state at epoch %d: gamma_s=%g, gamma_eps=%g, masked residual norm=%g", s.epoch, s.gamma_s,
+              s.gamma_eps, s.sq_r);
+    return PB_EDIVERGED;
+  }
+  return PB_OK;
+}
+
+float pb_problem_last_gpu_ms(pb_problem* pr) { return pr ? pr->last_ms : 0.f; }
+
+int pb_problem_get_dictionary(pb_problem* pr, float* atoms_host, double* pi_host, pb_scalars* scalars_host) {
+  if (!pr) { set_error("null problem"); return PB_EVALUE; }
+  if (atoms_host)
+    PB_CUDA_TRY(cudaMemcpyAsync(atoms_host, pr->atoms, (size_t)pr->k * pr->p * 4, cudaMemcpyDeviceToHost, pr->stream));
+  if (pi_host) PB_CUDA_TRY(cudaMemcpyAsync(pi_host, pr->pi, (size_t)pr->k * 8, cudaMemcpyDeviceToHost, pr->stream));
+  if (scalars_host)
+    PB_CUDA_TRY(cudaMemcpyAsync(scalars_host, pr->scalars, sizeof(pb_scalars), cudaMemcpyDeviceToHost, pr->stream));
+  PB_CUDA_TRY(cudaStreamSynchronize(pr->stream));
+  return PB_OK;
+}
+
+}  // extern "C"

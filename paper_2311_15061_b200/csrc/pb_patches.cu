@@ -1,0 +1,200 @@
+// pb200 — N-D strided patch extraction and gather-form overlap-add.
+//
+// Reference behaviour (pkg/src/patchbeam/patches.py):
+//   grid / origins          : 64-70, 107-113 (row-major grid, origins g_d * s_d)
+//   extract_patches         : 125-164 (values = x*o; observed-only mean; (x-mean)*o)
+//   reconstitute            : 188-215 (sum of (est + mean) over covering patches in
+//                             ascending patch order, / coverage; uncovered -> 0)
+//   apply_data_consistency  : 218-229 (fused here as the OLA epilogue)
+//
+// B200 design: extraction is one thread per patch writing the plane-major (P, N)
+// matrix, so every store instruction of a warp is a contiguous 128 B line and the
+// tensor reads along the fastest dim are contiguous for stride 1.  Overlap-add
+// is a gather (one thread per output element, coverage computed analytically),
+// so it is deterministic and atomic-free; neighbouring output elements read
+// neighbouring patches at the same offset -> coalesced.  Both are HBM-bound.
+#include "pb_sweep.cuh"
+
+namespace pb {
+
+// Padded-to-rank-4 geometry in constant-friendly POD form.
+struct Geo4 {
+  int64_t tstride[4];
+  int64_t tshape[4];
+  int64_t gcount[4];
+  int64_t gstride[4];  // row-major strides over the patch grid
+  int bshape[4];
+  int bstride[4];      // row-major strides within a patch
+  int step[4];
+  int64_t n, m;
+  int p;
+};
+
+static Geo4 make_geo4(const Grid& g) {
+  Geo4 o;
+  const int pad = kMaxRank - g.rank;
+  for (int d = 0; d < 4; ++d) {
+    if (d < pad) {
+      o.tshape[d] = 1; o.bshape[d] = 1; o.step[d] = 1; o.gcount[d] = 1;
+    } else {
+      o.tshape[d] = g.tshape[d - pad]; o.bshape[d] = g.bshape[d - pad];
+      o.step[d] = g.step[d - pad]; o.gcount[d] = g.gcount[d - pad];
+    }
+  }
+  int64_t acc = 1, gacc = 1;
+  int bacc = 1;
+  for (int d = 3; d >= 0; --d) {
+    o.tstride[d] = acc; acc *= o.tshape[d];
+    o.gstride[d] = gacc; gacc *= o.gcount[d];
+    o.bstride[d] = bacc; bacc *= o.bshape[d];
+  }
+  o.m = acc; o.n = gacc; o.p = bacc;
+  return o;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_extract(Geo4 g, const T* __restrict__ tensor,
+                                                 const uint8_t* __restrict__ mask, int mean_subtract,
+                                                 float* __restrict__ values, uint8_t* __restrict__ obs,
+                                                 float* __restrict__ means, int32_t* __restrict__ counts) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t base = 0, rem = i;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const int64_t gd = rem / g.gstride[d];
+      rem -= gd * g.gstride[d];
+      base += gd * g.step[d] * g.tstride[d];
+    }
+    // pass 1: observed count and observed-only sum (f64 accumulation)
+    double sum = 0.0;
+    int cnt = 0;
+    {
+      int q0 = 0, q1 = 0, q2 = 0, q3 = 0;
+      for (int p = 0; p < g.p; ++p) {
+        const int64_t off = base + q0 * g.tstride[0] + q1 * g.tstride[1] + q2 * g.tstride[2] + q3 * g.tstride[3];
+        if (mask[off]) { sum += (double)tensor[off]; ++cnt; }
+        if (++q3 == g.bshape[3]) { q3 = 0; if (++q2 == g.bshape[2]) { q2 = 0; if (++q1 == g.bshape[1]) { q1 = 0; ++q0; } } }
+      }
+    }
+    const double mean = (mean_subtract && cnt > 0) ? sum / (double)cnt : 0.0;
+    means[i] = (float)mean;
+    counts[i] = cnt;
+    // pass 2: plane-major write
+    int q0 = 0, q1 = 0, q2 = 0, q3 = 0;
+    for (int p = 0; p < g.p; ++p) {
+      const int64_t off = base + q0 * g.tstride[0] + q1 * g.tstride[1] + q2 * g.tstride[2] + q3 * g.tstride[3];
+      const uint8_t o = mask[off] ? 1 : 0;
+      values[(int64_t)p * g.n + i] = o ? (float)((double)tensor[off] - mean) : 0.0f;
+      obs[(int64_t)p * g.n + i] = o;
+      if (++q3 == g.bshape[3]) { q3 = 0; if (++q2 == g.bshape[2]) { q2 = 0; if (++q1 == g.bshape[1]) { q1 = 0; ++q0; } } }
+    }
+  }
+}
+
+__device__ __forceinline__ void cover_range(int64_t c, int b, int s, int64_t gc, int64_t& lo, int64_t& hi) {
+  const int64_t t = c - b + 1;
+  lo = t <= 0 ? 0 : (t + s - 1) / s;
+  hi = c / s;
+  if (hi > gc - 1) hi = gc - 1;
+}
+
+// out[x] = sum_{i covers x} (est_scale*est[p,i] + mean_i) / cov(x); DC epilogue.
+template <typename T>
+__global__ void __launch_bounds__(256) k_reconstitute(Geo4 g, const float* __restrict__ est, float est_scale,
+                                                      const float* __restrict__ means, const T* __restrict__ original,
+                                                      const uint8_t* __restrict__ mask, int dc, T* __restrict__ out,
+                                                      unsigned long long* __restrict__ uncovered) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < g.m;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c[4], lo[4], hi[4], rem = x;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      c[d] = rem / g.tstride[d];
+      rem -= c[d] * g.tstride[d];
+      cover_range(c[d], g.bshape[d], g.step[d], g.gcount[d], lo[d], hi[d]);
+    }
+    int64_t cov = 1;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) cov *= (hi[d] >= lo[d]) ? (hi[d] - lo[d] + 1) : 0;
+    double acc = 0.0;
+    if (cov > 0) {
+      for (int64_t a0 = lo[0]; a0 <= hi[0]; ++a0)
+        for (int64_t a1 = lo[1]; a1 <= hi[1]; ++a1)
+          for (int64_t a2 = lo[2]; a2 <= hi[2]; ++a2)
+            for (int64_t a3 = lo[3]; a3 <= hi[3]; ++a3) {
+              const int64_t i = a0 * g.gstride[0] + a1 * g.gstride[1] + a2 * g.gstride[2] + a3 * g.gstride[3];
+              const int64_t p = (c[0] - a0 * g.step[0]) * g.bstride[0] + (c[1] - a1 * g.step[1]) * g.bstride[1] +
+                                (c[2] - a2 * g.step[2]) * g.bstride[2] + (c[3] - a3 * g.step[3]) * g.bstride[3];
+              acc += (double)est[p * g.n + i] * (double)est_scale + (double)means[i];
+            }
+    }
+    double v = cov > 0 ? acc / (double)cov : 0.0;
+    if (cov == 0 && uncovered) atomicAdd(uncovered, 1ull);
+    if (dc && mask[x]) v = (double)original[x];
+    out[x] = (T)v;
+  }
+}
+
+__global__ void k_coverage(Geo4 g, int32_t* __restrict__ out) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < g.m;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    int64_t rem = x, cov = 1;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const int64_t c = rem / g.tstride[d];
+      rem -= c * g.tstride[d];
+      int64_t lo, hi;
+      cover_range(c, g.bshape[d], g.step[d], g.gcount[d], lo, hi);
+      cov *= hi >= lo ? hi - lo + 1 : 0;
+    }
+    out[x] = (int32_t)cov;
+  }
+}
+
+static int grid_blocks(int64_t work, int threads) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t b = ceil_div(work, threads);
+  const int64_t cap = (int64_t)sms * 16;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+int launch_extract(const Grid& grid, const void* tensor, int f64, const uint8_t* mask, int mean_subtract,
+                   float* values, uint8_t* obs, float* means, int32_t* counts, cudaStream_t st) {
+  const Geo4 g = make_geo4(grid);
+  const int th = 256;
+  const int nb = grid_blocks(g.n, th);
+  if (f64)
+    k_extract<double><<<nb, th, 0, st>>>(g, (const double*)tensor, mask, mean_subtract, values, obs, means, counts);
+  else
+    k_extract<float><<<nb, th, 0, st>>>(g, (const float*)tensor, mask, mean_subtract, values, obs, means, counts);
+  PB_LAUNCH_CHECK();
+  return PB_OK;
+}
+
+int launch_reconstitute(const Grid& grid, const float* est, float est_scale, const float* means, const void* original,
+                        const uint8_t* mask, int dc, int f64, void* out, unsigned long long* uncovered,
+                        cudaStream_t st) {
+  const Geo4 g = make_geo4(grid);
+  const int th = 256;
+  const int nb = grid_blocks(g.m, th);
+  if (f64)
+    k_reconstitute<double><<<nb, th, 0, st>>>(g, est, est_scale, means, (const double*)original, mask, dc,
+                                              (double*)out, uncovered);
+  else
+    k_reconstitute<float><<<nb, th, 0, st>>>(g, est, est_scale, means, (const float*)original, mask, dc,
+                                             (float*)out, uncovered);
+  PB_LAUNCH_CHECK();
+  return PB_OK;
+}
+
+int launch_coverage(const Grid& grid, int32_t* out, cudaStream_t st) {
+  const Geo4 g = make_geo4(grid);
+  k_coverage<<<grid_blocks(g.m, 256), 256, 0, st>>>(g, out);
+  PB_LAUNCH_CHECK();
+  return PB_OK;
+}
+
+}  // namespace pb

@@ -1,0 +1,128 @@
+"""GPU parity: N-D extraction, coverage and overlap-add vs the oracle and the
+reference-generated fixtures (tests/golden/extract_cases.npz).
+
+Bars: patch order, observed flags, origins, coverage and uncovered handling are
+BIT-EXACT; values/means/reconstructions (f32 on device vs f64 reference) within
+abs 1e-6 (values in [0,1]-scaled units) — stated tolerance.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import patches as op
+from paper_2311_15061_b200 import patches as pp
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-6
+
+
+def test_golden_cases(golden, cuda_device):
+    g = golden("extract_cases.npz")
+    for ci in range(int(g["num_cases"])):
+        p = f"c{ci}_"
+        spec = pp.PatchSpec(tuple(g[p + "patch"]), tuple(g[p + "stride"]))
+        pm = pp.extract_patches(g[p + "tensor"], g[p + "mask"], spec, bool(g[p + "mean_subtract"]))
+        vals, obs, means = pm.to_host()
+        assert np.array_equal(obs, g[p + "observed"]), ci
+        assert np.array_equal(pm.origins, g[p + "origins"]), ci
+        assert np.abs(vals - g[p + "values"]).max(initial=0) <= TOL, ci
+        assert np.abs(means - g[p + "means"]).max(initial=0) <= TOL, ci
+        assert np.array_equal(vals[~obs], np.zeros((~obs).sum())), "unobserved must be exactly 0"
+        assert np.array_equal(pp.coverage_map(pm), g[p + "coverage"]), ci
+        assert pm.n_obs == int(g[p + "observed"].sum())
+        rec = pp.reconstitute(pm, g[p + "est"])
+        assert rec.dtype == np.float64 and rec.shape == g[p + "recon"].shape
+        assert np.abs(rec - g[p + "recon"]).max() <= 1e-5, ci
+
+
+def test_extract_2x2_stride_2_exact(cuda_device):
+    t = np.arange(16, dtype=float).reshape(4, 4)
+    pm = pp.extract_patches(t, np.ones((4, 4), bool), pp.PatchSpec((2, 2), (2, 2)))
+    v, _, m = pm.to_host()
+    assert v[0].tolist() == [0, 1, 4, 5] and v[3].tolist() == [10, 11, 14, 15]
+    assert np.all(m == 0)
+
+
+def test_mean_subtraction_uses_observed_only(cuda_device):
+    t = np.array([[1.0, 3.0], [100.0, 5.0]])
+    mask = np.array([[True, True], [False, True]])
+    pm = pp.extract_patches(t, mask, pp.PatchSpec((2, 2)), mean_subtract=True)
+    v, _, m = pm.to_host()
+    assert m[0] == pytest.approx(3.0)
+    assert v[0].tolist() == [-2.0, 0.0, 0.0, 2.0]
+
+
+def test_unobserved_values_never_leak(cuda_device):
+    rng = np.random.default_rng(1)
+    t = rng.random((6, 6))
+    mask = rng.random((6, 6)) < 0.5
+    garbage = t.copy()
+    garbage[~mask] = rng.random((~mask).sum()) * 1e6
+    for ms in (False, True):
+        a = pp.extract_patches(t, mask, pp.PatchSpec((3, 3)), ms)
+        b = pp.extract_patches(garbage, mask, pp.PatchSpec((3, 3)), ms)
+        assert torch.equal(a.values_pn, b.values_pn) and torch.equal(a.means_dev, b.means_dev)
+
+
+@pytest.mark.parametrize("shape,patch,stride", [((7, 9), (3, 3), (1, 1)), ((8, 8), (4, 2), (2, 2)),
+                                                ((5, 5, 3), (2, 2, 3), (1, 1, 1)), ((16,), (4,), (2,)),
+                                                ((5, 4, 3, 4), (2, 2, 3, 2), (1, 2, 1, 1))])
+def test_roundtrip_identity_bitwise_on_integers(cuda_device, shape, patch, stride):
+    rng = np.random.default_rng(2)
+    t = rng.integers(0, 256, size=shape).astype(np.float64)
+    pm = pp.extract_patches(t, np.ones(shape, bool), pp.PatchSpec(patch, stride))
+    rec = pp.reconstitute(pm, pm.values)
+    cov = pp.coverage_map(pm) > 0
+    assert np.array_equal(rec[cov], t[cov])
+
+
+def test_reconstitute_matches_oracle_random(cuda_device):
+    rng = np.random.default_rng(5)
+    for shape, patch, stride, ms in [((37, 41), (8, 8), (1, 1), True), ((12, 10, 6), (4, 3, 6), (2, 1, 1), False),
+                                     ((64, 64), (10, 10), (3, 2), True)]:
+        t = rng.random(shape)
+        mask = rng.random(shape) < 0.3
+        pm = pp.extract_patches(t, mask, pp.PatchSpec(patch, stride), ms)
+        opm = op.extract_patches(t, mask, patch, stride, ms)
+        est = rng.standard_normal(opm.values.shape)
+        got = pp.reconstitute(pm, est)
+        want = op.reconstitute(opm, est)
+        assert np.abs(got - want).max() <= 1e-5
+        # fused data consistency
+        got_dc = pp.reconstitute(pm, est, dc_original=t, dc_mask=mask)
+        assert np.array_equal(got_dc[mask], t[mask])
+        assert np.abs(got_dc[~mask] - want[~mask]).max() <= 1e-5
+
+
+def test_strict_coverage_error(cuda_device):
+    pm = pp.extract_patches(np.zeros((5, 5)), np.ones((5, 5), bool), pp.PatchSpec((2, 2), (2, 2)))
+    with pytest.raises(pp.CoverageError):
+        pp.reconstitute(pm, pm.values, strict=True)
+    out = pp.reconstitute(pm, pm.values)
+    assert np.all(out[4, :] == 0) and np.all(out[:, 4] == 0)
+
+
+def test_shape_errors(cuda_device):
+    t = np.zeros((4, 4))
+    with pytest.raises(pp.ShapeError):
+        pp.extract_patches(t, np.ones((3, 4), bool), pp.PatchSpec((2, 2)))
+    with pytest.raises(pp.ShapeError):
+        pp.extract_patches(t, np.ones((4, 4), bool), pp.PatchSpec((5, 2)))
+    pm = pp.extract_patches(t, np.ones((4, 4), bool), pp.PatchSpec((2, 2)))
+    with pytest.raises(pp.ShapeError):
+        pp.reconstitute(pm, np.zeros((3, 4)))
+
+
+def test_large_frame_indices_exact(cuda_device):
+    """cfg-3-sized frame (512^2, 8x8, line-hop): observed flags and coverage exact."""
+    from paper_2311_15061_b200 import inputs
+
+    img = inputs.synthetic_texture((512, 512), seed=0)
+    mask = inputs.make_mask((512, 512), 0.25, "line-hop", 0)
+    pm = pp.extract_patches(img, mask, pp.PatchSpec((8, 8)), True)
+    opm = op.extract_patches(img, mask, (8, 8), (), True)
+    _, obs, means = pm.to_host()
+    assert np.array_equal(obs, opm.observed)
+    assert np.abs(means - opm.means).max() <= TOL
+    assert np.array_equal(pp.coverage_map(pm), op.coverage((512, 512), (8, 8), (1, 1)))

@@ -1,0 +1,37 @@
+"""Scratch timing of the device path on the BASELINE configs (not the bench)."""
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2311_15061_b200 import bpfa as gb  # noqa: E402
+from paper_2311_15061_b200 import inputs  # noqa: E402
+from paper_2311_15061_b200 import patches as pp  # noqa: E402
+
+CFGS = {
+    1: dict(shape=(256, 256), ratio=0.25, kind="uniform-random", patch=(8, 8), k=64, epochs=10),
+    3: dict(shape=(512, 512), ratio=0.25, kind="line-hop", patch=(8, 8), k=256, epochs=2),
+    2: dict(shape=(1024, 1024), ratio=0.10, kind="uniform-random", patch=(10, 10), k=256, epochs=3),
+}
+
+for cid in [int(a) for a in sys.argv[1:]] or [1, 3, 2]:
+    c = CFGS[cid]
+    img = inputs.synthetic_texture(c["shape"], seed=0)
+    mask = inputs.make_mask(c["shape"], c["ratio"], c["kind"], 0)
+    pm = pp.extract_patches(img, mask, pp.PatchSpec(c["patch"]), True)
+    hp = gb.Hyperparams(num_atoms=c["k"])
+    st, est = gb.infer(pm, hp, 1, 0, rng="philox")  # warm-up
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    st, est = gb.infer(pm, hp, c["epochs"], 0, rng="philox")
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    rec = pp.reconstitute(pm, est, dc_original=img, dc_mask=mask)
+    from paper_2311_15061_b200.metrics import psnr
+    upd = pm.num_patches * c["k"] * c["epochs"]
+    print(f"cfg{cid}: N={pm.num_patches} K={c['k']} epochs={c['epochs']} {ms:.2f} ms "
+          f"({ms / c['epochs']:.3f} ms/epoch) {upd / ms * 1e3:.3e} upd/s psnr={psnr(rec, img):.2f}", flush=True)
