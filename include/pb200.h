@@ -143,8 +143,15 @@ size_t pb_epoch_workspace_bytes(int64_t n, int32_t p, int32_t k);
  * int32[K], may be NULL) the per-atom usage counts.  In PB_RNG_PHILOX mode the
  * pi / gamma draws also run on the device (scalars->epoch advances, diverged
  * flags non-finite state); in PB_RNG_REPLAY mode the caller draws pi/gamma from
- * the reference streams and calls pb_epoch_commit. */
+ * the reference streams and writes pi / scalars itself. */
 int pb_gibbs_epoch(const pb_epoch_desc* d, int32_t* m_counts_out, void* stream);
+
+/* Phase timing for profiling/bench: when enabled, every pb_gibbs_epoch brackets
+ * its phases with CUDA events on its stream; pb_phase_read returns the summed
+ * milliseconds of [residual, dictionary step, code step, stats+pi/gamma] over
+ * the epochs since enabling (single host thread use). */
+int pb_phase_timing(int32_t enable);
+int pb_phase_read(double* ms_out /* [4] */, int64_t* epochs_out);
 
 /* ---- stateful problem (C-ABI with HOST buffers; the live submit_frame slice,
  *      pipeline.py:217-251).  Owns all device buffers. ---- */

@@ -72,6 +72,8 @@ SIGNATURES = {
     "pb_masked_sq_norm": (c_i32, [c_vp, c_i64, c_vp, c_vp, c_vp]),
     "pb_epoch_workspace_bytes": (ctypes.c_size_t, [c_i64, c_i32, c_i32]),
     "pb_gibbs_epoch": (c_i32, [ctypes.POINTER(EpochDesc), c_vp, c_vp]),
+    "pb_phase_timing": (c_i32, [c_i32]),
+    "pb_phase_read": (c_i32, [c_vp, c_vp]),
     "pb_problem_create": (c_i32, [ctypes.POINTER(ProblemDesc), ctypes.POINTER(c_vp)]),
     "pb_problem_destroy": (c_i32, [c_vp]),
     "pb_problem_submit_frame": (c_i32, [c_vp, c_vp, c_vp, c_vp]),

@@ -86,7 +86,32 @@ static void device_key(uint64_t seed, uint32_t& k0, uint32_t& k1) {
   k1 = (uint32_t)(z >> 32);
 }
 
+// Optional phase timing (bench / profiling): events bracketing the epoch's
+// kernels, accumulated per phase on the launching stream.
+enum { kPhResid = 0, kPhDict, kPhCode, kPhStats, kPhEnd, kNumPh };
+static bool g_phase_on = false;
+static cudaEvent_t g_ev[kNumPh];
+static double g_phase_ms[kNumPh - 1];
+static long g_phase_n = 0;
+static bool g_phase_pending = false;
+
+static void phase_mark(int ph, cudaStream_t st) {
+  if (g_phase_on) cudaEventRecord(g_ev[ph], st);
+}
+static void phase_collect() {
+  if (!g_phase_on || !g_phase_pending) return;
+  cudaEventSynchronize(g_ev[kPhEnd]);
+  for (int i = 0; i < kNumPh - 1; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, g_ev[i], g_ev[i + 1]);
+    g_phase_ms[i] += ms;
+  }
+  ++g_phase_n;
+  g_phase_pending = false;
+}
+
 static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
+  phase_collect();
   if (d->n < 1 || d->p < 1 || d->k < 1) { set_error("empty problem"); return PB_ESHAPE; }
   if (d->rng_mode == PB_RNG_REPLAY && (!d->code_u || !d->code_g || (!d->freeze_dict && !d->atom_draws))) {
     set_error("replay mode needs atom_draws, code_u and code_g");
@@ -98,9 +123,11 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
   uint32_t k0, k1;
   device_key(d->seed, k0, k1);
   SweepScalars* sc = (SweepScalars*)d->scalars;
+  phase_mark(kPhResid, st);
   int rc = launch_accumulate_atoms(true, d->values, d->observed, d->usage, d->weights, d->atoms, ws.resid, d->n, d->p,
                                    d->k, 0, st);
   if (rc) return rc;
+  phase_mark(kPhDict, st);
   if (!d->freeze_dict) {
     int blocks, threads, tile;
     size_t smem;
@@ -116,10 +143,14 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
              d->rng_mode == PB_RNG_REPLAY ? d->code_g : nullptr,
              sc, ws.block_sums, ws.m_count, d->n, d->p, d->k, 0, k0, k1};
   int nblocks = 0;
+  phase_mark(kPhCode, st);
   if ((rc = launch_code_step(c, d->rng_mode, nblocks, st))) return rc;
+  phase_mark(kPhStats, st);
   if ((rc = launch_finish_stats(ws.block_sums, nblocks, sc, st))) return rc;
   if (d->rng_mode == PB_RNG_PHILOX)
     rc = launch_draw_pi_gamma(d->pi, ws.m_count, sc, d->k, d->n, d->n_obs, d->hyper, k0, k1, st);
+  phase_mark(kPhEnd, st);
+  g_phase_pending = g_phase_on;
   return rc;
 }
 
@@ -211,6 +242,27 @@ int pb_masked_sq_norm(const float* resid, int64_t total, double* out, double* sc
 }
 
 size_t pb_epoch_workspace_bytes(int64_t n, int32_t p, int32_t k) { return ws_bytes(n, p, k, nullptr, nullptr); }
+
+int pb_phase_timing(int32_t enable) {
+  if (enable && !g_phase_on) {
+    for (int i = 0; i < kNumPh; ++i) PB_CUDA_TRY(cudaEventCreate(&g_ev[i]));
+  }
+  if (!enable && g_phase_on) {
+    for (int i = 0; i < kNumPh; ++i) cudaEventDestroy(g_ev[i]);
+  }
+  g_phase_on = enable != 0;
+  g_phase_pending = false;
+  for (int i = 0; i < kNumPh - 1; ++i) g_phase_ms[i] = 0.0;
+  g_phase_n = 0;
+  return PB_OK;
+}
+
+int pb_phase_read(double* ms_out, int64_t* epochs_out) {
+  phase_collect();
+  for (int i = 0; i < kNumPh - 1; ++i) ms_out[i] = g_phase_ms[i];
+  if (epochs_out) *epochs_out = g_phase_n;
+  return PB_OK;
+}
 
 int pb_gibbs_epoch(const pb_epoch_desc* d, int32_t* m_counts_out, void* stream) {
   if (!d) { set_error("null epoch desc"); return PB_EVALUE; }
