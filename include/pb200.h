@@ -99,6 +99,27 @@ int pb_shift_codes(float* resid, const uint8_t* observed, const float* atom, con
 /* _kernels.masked_sq_norm (_kernels.py:112-130): out = device f64 scalar; scratch f64[256]. */
 int pb_masked_sq_norm(const float* resid, int64_t total, double* out, double* scratch, void* stream);
 
+/* ---- observed-element index (built once per mask) ----
+ * Every conditional of the reference sampler sums over observed elements only
+ * (bpfa.py:1-21), so the sweep stores the residual for the nnz observed
+ * elements in a tiled column-major order plus a per-patch slot list.  The
+ * index depends on the mask only; pb_index_refresh_values updates the observed
+ * values for a new frame under the same mask (the live path). */
+typedef struct pb_patch_index {
+  int64_t n;        /* patches */
+  int32_t p;        /* patch size */
+  int32_t ntiles;   /* set by pb_build_index */
+  int64_t nnz;      /* observed elements = sum of counts (caller supplies) */
+  int32_t cmax;     /* max observed per patch (set by pb_build_index) */
+  void* buffer;     /* device buffer of pb_index_bytes(n, p, nnz) bytes */
+} pb_patch_index;
+
+size_t pb_index_bytes(int64_t n, int32_t p, int64_t nnz);
+/* Builds the index from the extract_patches outputs; synchronizes `stream` once. */
+int pb_build_index(pb_patch_index* index, const uint8_t* observed, const float* values, const int32_t* counts,
+                   void* stream);
+int pb_index_refresh_values(const pb_patch_index* index, const float* values, const int32_t* counts, void* stream);
+
 /* ---- the sweep: bpfa.gibbs_epoch (bpfa.py:278-345) ---- */
 
 /* Device-resident scalar block of a sampler state (layout fixed, 40 bytes). */
@@ -122,6 +143,8 @@ typedef struct pb_epoch_desc {
   /* problem */
   const float* values;      /* (P,N) */
   const uint8_t* observed;  /* (P,N) */
+  const int32_t* counts;    /* (N) observed per patch */
+  const pb_patch_index* index;
   /* state (in/out) */
   float* atoms;             /* (K,P) */
   double* pi;               /* (K)   */
@@ -136,7 +159,7 @@ typedef struct pb_epoch_desc {
   void* workspace;
 } pb_epoch_desc;
 
-size_t pb_epoch_workspace_bytes(int64_t n, int32_t p, int32_t k);
+size_t pb_epoch_workspace_bytes(int64_t n, int32_t p, int32_t k, int64_t nnz);
 
 /* One sweep through the dictionary and code steps.  After it returns (stream
  * ordered), scalars->sq_w / sq_r hold the epoch sums and m_counts_out (device

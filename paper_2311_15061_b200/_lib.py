@@ -38,10 +38,16 @@ class Scalars(ctypes.Structure):
                 ("epoch", c_i32), ("diverged", c_i32)]
 
 
+class PatchIndex(ctypes.Structure):
+    _fields_ = [("n", c_i64), ("p", c_i32), ("ntiles", c_i32), ("nnz", c_i64), ("cmax", c_i32),
+                ("buffer", c_vp)]
+
+
 class EpochDesc(ctypes.Structure):
     _fields_ = [("n", c_i64), ("p", c_i32), ("k", c_i32), ("freeze_dict", c_i32), ("rng_mode", c_i32),
                 ("seed", c_u64), ("n_obs", c_i64), ("hyper", c_f64 * 6),
-                ("values", c_vp), ("observed", c_vp), ("atoms", c_vp), ("pi", c_vp), ("usage", c_vp),
+                ("values", c_vp), ("observed", c_vp), ("counts", c_vp), ("index", ctypes.POINTER(PatchIndex)),
+                ("atoms", c_vp), ("pi", c_vp), ("usage", c_vp),
                 ("weights", c_vp), ("scalars", c_vp), ("atom_draws", c_vp), ("code_u", c_vp),
                 ("code_g", c_vp), ("workspace", c_vp)]
 
@@ -70,7 +76,10 @@ SIGNATURES = {
     "pb_code_moments": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
     "pb_shift_codes": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp]),
     "pb_masked_sq_norm": (c_i32, [c_vp, c_i64, c_vp, c_vp, c_vp]),
-    "pb_epoch_workspace_bytes": (ctypes.c_size_t, [c_i64, c_i32, c_i32]),
+    "pb_index_bytes": (ctypes.c_size_t, [c_i64, c_i32, c_i64]),
+    "pb_build_index": (c_i32, [ctypes.POINTER(PatchIndex), c_vp, c_vp, c_vp, c_vp]),
+    "pb_index_refresh_values": (c_i32, [ctypes.POINTER(PatchIndex), c_vp, c_vp, c_vp]),
+    "pb_epoch_workspace_bytes": (ctypes.c_size_t, [c_i64, c_i32, c_i32, c_i64]),
     "pb_gibbs_epoch": (c_i32, [ctypes.POINTER(EpochDesc), c_vp, c_vp]),
     "pb_phase_timing": (c_i32, [c_i32]),
     "pb_phase_read": (c_i32, [c_vp, c_vp]),

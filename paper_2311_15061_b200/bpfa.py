@@ -162,10 +162,10 @@ class GibbsState:
         sc = _make_scalars(weight_precision, noise_precision, epoch, device)
         return cls(Dictionary(atoms_t, pi_t, tuple(patch_shape)), u, w, sc, seed)
 
-    def workspace(self, n, p, k):
-        key = (n, p, k)
+    def workspace(self, n, p, k, nnz):
+        key = (n, p, k, nnz)
         if self._workspace is None or self._workspace[0] != key:
-            nb = int(_lib.load().pb_epoch_workspace_bytes(n, p, k))
+            nb = int(_lib.load().pb_epoch_workspace_bytes(n, p, k, nnz))
             self._workspace = (key, torch.empty((nb,), dtype=torch.uint8, device=self.usage_kn.device),
                                torch.empty((k,), dtype=torch.int32, device=self.usage_kn.device))
         return self._workspace[1], self._workspace[2]
@@ -231,8 +231,11 @@ def install_dictionary(state_seed: int, pm: PatchMatrix, hp: Hyperparams, dictio
 
 def _epoch_desc(state: GibbsState, pm: PatchMatrix, hp: Hyperparams, freeze: bool, mode: int):
     n, p, k = pm.num_patches, pm.patch_size, state.num_atoms
-    ws, m = state.workspace(n, p, k)
+    ix = pm.index()
+    ws, m = state.workspace(n, p, k, pm.n_obs)
     d = _lib.EpochDesc()
+    d.index = ctypes.pointer(ix)
+    d.counts = pm.counts.data_ptr()
     d.n, d.p, d.k = n, p, k
     d.freeze_dict = int(bool(freeze))
     d.rng_mode = mode

@@ -7,7 +7,7 @@
 #include <vector>
 
 #include "../../include/pb200.h"
-#include "pb_sweep.cuh"
+#include "pb_compact.cuh"
 
 namespace pb {
 
@@ -45,34 +45,33 @@ static int make_grid(const pb_grid_desc* d, Grid& g) {
 
 // Epoch workspace carve-up
 struct EpochWs {
-  float* resid;
-  double* partials;
-  float* delta;
-  unsigned int* sync;
+  float* r_csc;
+  float* partials;
+  double* reduced;
+  unsigned* bar;
   double* block_sums;
   int32_t* m_count;
 };
-static const int kMaxDictBlocks = 148 * 4;
+static const int kMaxDictBlocks = 148 * 8;
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
-static size_t code_blocks_upper(int64_t n, int p) {
-  int g = 1;
-  while ((p + g - 1) / g > 64 && g < 32) g *= 2;
-  return (size_t)ceil_div(n * g, 256);
-}
-static size_t ws_bytes(int64_t n, int p, int k, EpochWs* ws, char* base) {
+static size_t ws_bytes(int64_t n, int p, int k, int64_t nnz, EpochWs* ws, char* base) {
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return base ? base + o : nullptr; };
-  char* r = take((size_t)n * p * 4);
-  char* pa = take((size_t)kMaxDictBlocks * 2 * p * 8);
-  char* dl = take((size_t)p * 4);
-  char* sy = take(16);
-  char* bs = take(code_blocks_upper(n, p) * 2 * 8);
+  char* r = take((size_t)nnz * 4);
+  char* pa = take(dict_gram_partials_bytes(p, kMaxDictBlocks));
+  char* rd = take(dict_gram_reduced_bytes(p));
+  char* bar = take(16);
+  char* bs = take((size_t)ceil_div(n * 32, 256) * 2 * 8);  // upper bound of code-step blocks
   char* mc = take((size_t)k * 4);
   if (ws) {
-    ws->resid = (float*)r; ws->partials = (double*)pa; ws->delta = (float*)dl;
-    ws->sync = (unsigned int*)sy; ws->block_sums = (double*)bs; ws->m_count = (int32_t*)mc;
+    ws->r_csc = (float*)r; ws->partials = (float*)pa; ws->reduced = (double*)rd;
+    ws->bar = (unsigned*)bar; ws->block_sums = (double*)bs; ws->m_count = (int32_t*)mc;
   }
   return off;
+}
+
+static void index_view(const pb_patch_index* pi, PatchIndex& ix) {
+  carve_index(ix, (char*)pi->buffer, pi->n, pi->p, pi->nnz);
 }
 
 static void device_key(uint64_t seed, uint32_t& k0, uint32_t& k1) {
@@ -113,38 +112,46 @@ static void phase_collect() {
 static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
   phase_collect();
   if (d->n < 1 || d->p < 1 || d->k < 1) { set_error("empty problem"); return PB_ESHAPE; }
+  if (!d->index || !d->index->buffer || d->index->n != d->n || d->index->p != d->p) {
+    set_error("pb_gibbs_epoch needs the patch index of this patch matrix (pb_build_index)");
+    return PB_EVALUE;
+  }
   if (d->rng_mode == PB_RNG_REPLAY && (!d->code_u || !d->code_g || (!d->freeze_dict && !d->atom_draws))) {
     set_error("replay mode needs atom_draws, code_u and code_g");
     return PB_EVALUE;
   }
+  PatchIndex ix;
+  index_view(d->index, ix);
   EpochWs ws;
-  ws_bytes(d->n, d->p, d->k, &ws, (char*)d->workspace);
+  ws_bytes(d->n, d->p, d->k, d->index->nnz, &ws, (char*)d->workspace);
   if (m_out) ws.m_count = m_out;
   uint32_t k0, k1;
   device_key(d->seed, k0, k1);
   SweepScalars* sc = (SweepScalars*)d->scalars;
+  CompactArgs c{};
+  c.counts = d->counts; c.rowptr = ix.rowptr; c.csr_p = ix.csr_p; c.csr_pos = ix.csr_pos;
+  c.x_csc = ix.x_csc; c.r_csc = ws.r_csc; c.cmax = d->index->cmax;
+  c.usage = d->usage; c.weights = d->weights; c.atoms = d->atoms; c.pi = d->pi; c.sc = sc;
+  c.u_draw = d->rng_mode == PB_RNG_REPLAY ? d->code_u : nullptr;
+  c.g_draw = d->rng_mode == PB_RNG_REPLAY ? d->code_g : nullptr;
+  c.block_sums = ws.block_sums; c.m_count = ws.m_count;
+  c.n = d->n; c.p = d->p; c.k = d->k; c.key0 = k0; c.key1 = k1;
   phase_mark(kPhResid, st);
-  int rc = launch_accumulate_atoms(true, d->values, d->observed, d->usage, d->weights, d->atoms, ws.resid, d->n, d->p,
-                                   d->k, 0, st);
+  int rc = launch_resid_compact(c, st);
   if (rc) return rc;
   phase_mark(kPhDict, st);
   if (!d->freeze_dict) {
-    int blocks, threads, tile;
-    size_t smem;
-    if ((rc = dict_step_grid(d->p, blocks, threads, smem, tile))) return rc;
-    if (blocks > kMaxDictBlocks) blocks = kMaxDictBlocks;
-    DictArgs a{ws.resid, d->observed, d->usage, d->weights, d->atoms,
-               d->rng_mode == PB_RNG_REPLAY ? d->atom_draws : nullptr,
-               sc, ws.partials, ws.delta, ws.sync, d->n, d->p, d->k, tile, k0, k1};
-    if ((rc = launch_dict_step(a, blocks, threads, smem, st))) return rc;
+    DictGramArgs g{};
+    g.tile_base = ix.tile_base; g.colptr = ix.colptr; g.e_loc = ix.e_loc; g.ntiles = ix.ntiles;
+    g.r_csc = ws.r_csc; g.usage = d->usage; g.weights = d->weights; g.atoms = d->atoms;
+    g.draws = d->rng_mode == PB_RNG_REPLAY ? d->atom_draws : nullptr;
+    g.sc = sc; g.partials = ws.partials; g.reduced = ws.reduced; g.bar = ws.bar; g.max_blocks = kMaxDictBlocks;
+    g.n = d->n; g.p = d->p; g.k = d->k; g.key0 = k0; g.key1 = k1;
+    if ((rc = launch_dict_gram(g, st))) return rc;
   }
-  CodeArgs c{ws.resid, d->observed, d->usage, d->weights, d->atoms, d->pi,
-             d->rng_mode == PB_RNG_REPLAY ? d->code_u : nullptr,
-             d->rng_mode == PB_RNG_REPLAY ? d->code_g : nullptr,
-             sc, ws.block_sums, ws.m_count, d->n, d->p, d->k, 0, k0, k1};
   int nblocks = 0;
   phase_mark(kPhCode, st);
-  if ((rc = launch_code_step(c, d->rng_mode, nblocks, st))) return rc;
+  if ((rc = launch_code_compact(c, d->rng_mode, nblocks, st))) return rc;
   phase_mark(kPhStats, st);
   if ((rc = launch_finish_stats(ws.block_sums, nblocks, sc, st))) return rc;
   if (d->rng_mode == PB_RNG_PHILOX)
@@ -241,7 +248,39 @@ int pb_masked_sq_norm(const float* resid, int64_t total, double* out, double* sc
   return launch_sq_norm(resid, total, scratch, 256, out, (cudaStream_t)stream);
 }
 
-size_t pb_epoch_workspace_bytes(int64_t n, int32_t p, int32_t k) { return ws_bytes(n, p, k, nullptr, nullptr); }
+size_t pb_epoch_workspace_bytes(int64_t n, int32_t p, int32_t k, int64_t nnz) {
+  return ws_bytes(n, p, k, nnz, nullptr, nullptr);
+}
+
+size_t pb_index_bytes(int64_t n, int32_t p, int64_t nnz) {
+  size_t b = 0;
+  index_bytes(n, p, nnz, &b);
+  return b;
+}
+
+int pb_build_index(pb_patch_index* pi, const uint8_t* observed, const float* values, const int32_t* counts,
+                   void* stream) {
+  if (!pi || !pi->buffer) { set_error("null index"); return PB_EVALUE; }
+  if (pi->nnz >= (int64_t)1 << 31) { set_error("too many observed elements for 32-bit positions"); return PB_EUNSUPPORTED; }
+  PatchIndex ix;
+  index_view(pi, ix);
+  pi->ntiles = ix.ntiles;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = launch_build_index(ix, observed, values, counts, st);
+  if (rc) return rc;
+  int32_t cmax = 0;
+  PB_CUDA_TRY(cudaMemcpyAsync(&cmax, ix.cmax_dev, 4, cudaMemcpyDeviceToHost, st));
+  PB_CUDA_TRY(cudaStreamSynchronize(st));
+  pi->cmax = cmax;
+  return PB_OK;
+}
+
+int pb_index_refresh_values(const pb_patch_index* pi, const float* values, const int32_t* counts, void* stream) {
+  if (!pi || !pi->buffer) { set_error("null index"); return PB_EVALUE; }
+  PatchIndex ix;
+  index_view(pi, ix);
+  return launch_scatter_x(ix, values, counts, (cudaStream_t)stream);
+}
 
 int pb_phase_timing(int32_t enable) {
   if (enable && !g_phase_on) {
@@ -292,6 +331,9 @@ struct pb_problem {
   pb_scalars* scalars = nullptr;
   unsigned long long* nobs_dev = nullptr;
   void* ws = nullptr;
+  size_t ws_cap = 0;
+  pb_patch_index index{};
+  size_t ix_cap = 0;
   std::vector<uint8_t> mask_cache;
   int64_t n_obs = 0;
   bool have_state = false;
@@ -311,7 +353,7 @@ extern "C" {
 int pb_problem_destroy(pb_problem* pr) {
   if (!pr) return PB_OK;
   void* bufs[] = {pr->frame, pr->mask, pr->values, pr->means, pr->atoms, pr->weights, pr->est, pr->obs, pr->usage,
-                  pr->counts, pr->m_count, pr->pi, pr->recon, pr->scalars, pr->nobs_dev, pr->ws};
+                  pr->counts, pr->m_count, pr->pi, pr->recon, pr->scalars, pr->nobs_dev, pr->ws, pr->index.buffer};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (pr->ev0) cudaEventDestroy(pr->ev0);
@@ -337,9 +379,6 @@ int pb_problem_create(const pb_problem_desc* desc, pb_problem** out) {
   PB_A(frame, m) PB_A(mask, m) PB_A(values, p * n) PB_A(obs, p * n) PB_A(means, n) PB_A(counts, n)
   PB_A(atoms, k * p) PB_A(pi, k) PB_A(usage, k * n) PB_A(weights, k * n) PB_A(est, p * n) PB_A(recon, m)
   PB_A(m_count, k) PB_A(scalars, 1) PB_A(nobs_dev, 1)
-  char* wsp = nullptr;
-  if ((rc = dalloc(&wsp, pb_epoch_workspace_bytes(n, (int)p, (int)k)))) { pb_problem_destroy(pr); return rc; }
-  pr->ws = wsp;
 #undef PB_A
   if (cudaStreamCreateWithFlags(&pr->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&pr->ev0) != cudaSuccess || cudaEventCreate(&pr->ev1) != cudaSuccess) {
@@ -391,6 +430,25 @@ int pb_problem_submit_frame(pb_problem* pr, const double* frame_host, const uint
     PB_CUDA_TRY(cudaMemcpyAsync(&nobs, pr->nobs_dev, sizeof(nobs), cudaMemcpyDeviceToHost, st));
     PB_CUDA_TRY(cudaStreamSynchronize(st));
     pr->n_obs = (int64_t)nobs;
+    // (re)size the observed-element index and the epoch workspace for this mask
+    const size_t ixb = pb_index_bytes(n, pr->p, pr->n_obs);
+    if (ixb > pr->ix_cap) {
+      if (pr->index.buffer) cudaFree(pr->index.buffer);
+      pr->index.buffer = nullptr;
+      PB_CUDA_TRY(cudaMalloc(&pr->index.buffer, ixb));
+      pr->ix_cap = ixb;
+    }
+    const size_t wsb = pb_epoch_workspace_bytes(n, pr->p, pr->k, pr->n_obs);
+    if (wsb > pr->ws_cap) {
+      if (pr->ws) cudaFree(pr->ws);
+      pr->ws = nullptr;
+      PB_CUDA_TRY(cudaMalloc(&pr->ws, wsb));
+      pr->ws_cap = wsb;
+    }
+    pr->index.n = n; pr->index.p = pr->p; pr->index.nnz = pr->n_obs;
+    if ((rc = pb_build_index(&pr->index, pr->obs, pr->values, pr->counts, st))) return rc;
+  } else {
+    if ((rc = pb_index_refresh_values(&pr->index, pr->values, pr->counts, st))) return rc;
   }
   if (!pr->have_state || !pr->desc.warm_start) {
     if ((rc = problem_cold_init(pr))) return rc;
@@ -406,6 +464,7 @@ int pb_problem_submit_frame(pb_problem* pr, const double* frame_host, const uint
   for (int j = 0; j < 6; ++j) d.hyper[j] = pr->desc.hyper[j];
   d.values = pr->values; d.observed = pr->obs; d.atoms = pr->atoms; d.pi = pr->pi;
   d.usage = pr->usage; d.weights = pr->weights; d.scalars = pr->scalars; d.workspace = pr->ws;
+  d.index = &pr->index; d.counts = pr->counts;
   const int epochs = pr->desc.epochs_per_frame;
   int tail = pr->desc.average_last < 1 ? 1 : (pr->desc.average_last > epochs ? epochs : pr->desc.average_last);
   for (int e = 0; e < epochs; ++e) {

@@ -1,0 +1,66 @@
+// pb200 — compact (observed-element) sweep kernels: argument blocks and launchers.
+#pragma once
+#include <algorithm>
+
+#include "pb_index.cuh"
+#include "pb_sweep.cuh"
+
+namespace pb {
+
+struct CompactArgs {
+  // index (CSR view) + residual in CSC order
+  const int32_t* counts;
+  const int64_t* rowptr;
+  const uint16_t* csr_p;
+  const uint32_t* csr_pos;
+  const float* x_csc;
+  float* r_csc;
+  int cmax;
+  // state
+  uint8_t* usage;
+  float* weights;
+  const float* atoms;
+  const double* pi;
+  const SweepScalars* sc;
+  // replay draws (code step)
+  const double* u_draw;
+  const double* g_draw;
+  // outputs
+  double* block_sums;
+  int32_t* m_count;
+  int64_t n;
+  int p, k, kc;
+  uint32_t key0, key1;
+};
+
+struct DictGramArgs {
+  // index (CSC view)
+  const int64_t* tile_base;
+  const int32_t* colptr;
+  const uint16_t* e_loc;
+  int ntiles;
+  float* r_csc;
+  // state
+  const uint8_t* usage;
+  const float* weights;
+  float* atoms;
+  const double* draws;  // replay atom normals (K,P) or null
+  const SweepScalars* sc;
+  // workspace
+  float* partials;      // max_blocks * P * NACC
+  double* reduced;      // P * NACC
+  unsigned* bar;        // 2
+  int max_blocks;
+  int wbytes;
+  int64_t n;
+  int p, k;
+  uint32_t key0, key1;
+};
+
+int launch_resid_compact(const CompactArgs& a, cudaStream_t st);
+int launch_code_compact(const CompactArgs& a, int mode, int& nblocks, cudaStream_t st);
+int launch_dict_gram(const DictGramArgs& a, cudaStream_t st);
+size_t dict_gram_partials_bytes(int p, int max_blocks);
+size_t dict_gram_reduced_bytes(int p);
+
+}  // namespace pb

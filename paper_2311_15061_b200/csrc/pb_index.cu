@@ -1,0 +1,214 @@
+// pb200 — observed-element index of a patch matrix (built once per mask).
+//
+// The sweep never touches unobserved elements: every conditional of the
+// reference sampler sums over Omega_i only (bpfa.py:1-21, _kernels.py:18-109),
+// and with 10-25 % sampling the dense (P, N) layout wastes 4-10x of every
+// pass.  This kernel set turns the plane-major observed mask into two views of
+// the same nnz observed elements:
+//
+//   CSC-tile order  (the dictionary step's order): patches are cut into tiles
+//     of kTile consecutive patches; inside a tile, elements are grouped by
+//     patch offset p (column) and sorted by patch.  Per element: e_loc (u16,
+//     patch index inside the tile), x_csc (the observed value), and the
+//     residual lives in this order.  colptr[t][p] = first element of column p.
+//   CSR order (the code step's order): per patch, its observed offsets in
+//     ascending p: csr_p (u16) and csr_pos (u32, the element's CSC position),
+//     slots [rowptr[i], rowptr[i] + count[i]).
+//
+// Both are deterministic (ascending patch, ascending p), built with block-wide
+// ballot scans; no atomics except the max count.
+#include "pb_index.cuh"
+
+namespace pb {
+
+__global__ void k_tile_totals(const int32_t* __restrict__ counts, int64_t n, int32_t* __restrict__ tile_tot,
+                              int32_t* __restrict__ cmax) {
+  __shared__ int red[32];
+  __shared__ int mx[32];
+  const int64_t base = (int64_t)blockIdx.x * kTile;
+  int s = 0, m = 0;
+  for (int li = threadIdx.x; li < kTile; li += blockDim.x) {
+    const int64_t i = base + li;
+    if (i < n) {
+      const int c = counts[i];
+      s += c;
+      m = max(m, c);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  }
+  if ((threadIdx.x & 31) == 0) { red[threadIdx.x >> 5] = s; mx[threadIdx.x >> 5] = m; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0, mm = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { t += red[w]; mm = max(mm, mx[w]); }
+    tile_tot[blockIdx.x] = t;
+    atomicMax(cmax, mm);
+  }
+}
+
+// Exclusive scan of the tile totals (one block; ntiles is N/1024).
+__global__ void k_tile_scan(const int32_t* __restrict__ tile_tot, int ntiles, int64_t* __restrict__ tile_base) {
+  __shared__ int64_t wsum[32];
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < ntiles; c0 += blockDim.x) {
+    const int t = c0 + threadIdx.x;
+    int64_t v = t < ntiles ? tile_tot[t] : 0, x = v;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int64_t s = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0, z = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, z, o);
+        if (lane >= o) z += y;
+      }
+      wsum[lane] = z - s;
+    }
+    __syncthreads();
+    if (t < ntiles) tile_base[t] = carry + wsum[w] + x - v;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry += wsum[w] + x;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tile_base[ntiles] = carry;
+}
+
+// Block-wide exclusive scan of small ints (blockDim.x == kTile == 1024).
+__device__ __forceinline__ int block_excl_scan(int v, int* wsum, int& total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    const int s = wsum[lane];
+    int z = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
+    }
+    wsum[lane] = z - s;
+    if (lane == 31) wsum[32] = z;
+  }
+  __syncthreads();
+  total = wsum[32];
+  return wsum[w] + x - v;
+}
+
+__global__ void __launch_bounds__(kTile) k_tile_fill(const uint8_t* __restrict__ obs, const float* __restrict__ values,
+                                                      const int32_t* __restrict__ counts, int64_t n, int p,
+                                                      const int64_t* __restrict__ tile_base,
+                                                      int32_t* __restrict__ colptr, uint16_t* __restrict__ e_loc,
+                                                      float* __restrict__ x_csc, int64_t* __restrict__ rowptr,
+                                                      uint16_t* __restrict__ csr_p, uint32_t* __restrict__ csr_pos) {
+  __shared__ int wsum[33];
+  const int t = blockIdx.x;
+  const int li = threadIdx.x;
+  const int64_t gi = (int64_t)t * kTile + li;
+  const bool live = gi < n;
+  const int64_t tb = tile_base[t];
+  int tot;
+  const int my_cnt = live ? counts[gi] : 0;
+  const int64_t my_row = tb + block_excl_scan(my_cnt, wsum, tot);
+  if (live) rowptr[gi] = my_row;
+  if (gi == n - 1) rowptr[n] = my_row + my_cnt;
+  int64_t col = tb;
+  int j = 0;
+  for (int pe = 0; pe < p; ++pe) {
+    const int o = (live && obs[(int64_t)pe * n + gi]) ? 1 : 0;
+    const int rank = block_excl_scan(o, wsum, tot);
+    if (li == 0) colptr[(int64_t)t * (p + 1) + pe] = (int32_t)col;
+    if (o) {
+      const int64_t pos = col + rank;
+      e_loc[pos] = (uint16_t)li;
+      x_csc[pos] = values[(int64_t)pe * n + gi];
+      csr_p[my_row + j] = (uint16_t)pe;
+      csr_pos[my_row + j] = (uint32_t)pos;
+      ++j;
+    }
+    col += tot;
+  }
+  if (li == 0) colptr[(int64_t)t * (p + 1) + p] = (int32_t)col;
+}
+
+// Refresh the CSC values for a new frame under a cached mask (live path).
+__global__ void k_scatter_x(const float* __restrict__ values, const int32_t* __restrict__ counts,
+                            const int64_t* __restrict__ rowptr, const uint16_t* __restrict__ csr_p,
+                            const uint32_t* __restrict__ csr_pos, int64_t n, float* __restrict__ x_csc) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = rowptr[i];
+    const int c = counts[i];
+    for (int j = 0; j < c; ++j) x_csc[csr_pos[r + j]] = values[(int64_t)csr_p[r + j] * n + i];
+  }
+}
+
+int index_bytes(int64_t n, int p, int64_t nnz_upper, size_t* out) {
+  const int64_t ntiles = ceil_div(n, kTile);
+  size_t b = 0;
+  auto a = [&](size_t x) { b += (x + 255) & ~size_t(255); };
+  a((size_t)ntiles * 4);              // tile_tot
+  a((size_t)(ntiles + 1) * 8);        // tile_base
+  a((size_t)ntiles * (p + 1) * 4);    // colptr
+  a((size_t)(n + 1) * 8);             // rowptr
+  a((size_t)nnz_upper * 2);           // e_loc
+  a((size_t)nnz_upper * 4);           // x_csc
+  a((size_t)nnz_upper * 2);           // csr_p
+  a((size_t)nnz_upper * 4);           // csr_pos
+  a(64);                              // cmax + misc
+  *out = b;
+  return PB_OK;
+}
+
+void carve_index(PatchIndex& ix, char* base, int64_t n, int p, int64_t nnz_upper) {
+  const int64_t ntiles = ceil_div(n, kTile);
+  size_t off = 0;
+  auto take = [&](size_t x) { char* r = base + off; off += (x + 255) & ~size_t(255); return r; };
+  ix.n = n; ix.p = p; ix.ntiles = (int)ntiles;
+  ix.tile_tot = (int32_t*)take((size_t)ntiles * 4);
+  ix.tile_base = (int64_t*)take((size_t)(ntiles + 1) * 8);
+  ix.colptr = (int32_t*)take((size_t)ntiles * (p + 1) * 4);
+  ix.rowptr = (int64_t*)take((size_t)(n + 1) * 8);
+  ix.e_loc = (uint16_t*)take((size_t)nnz_upper * 2);
+  ix.x_csc = (float*)take((size_t)nnz_upper * 4);
+  ix.csr_p = (uint16_t*)take((size_t)nnz_upper * 2);
+  ix.csr_pos = (uint32_t*)take((size_t)nnz_upper * 4);
+  ix.cmax_dev = (int32_t*)take(64);
+}
+
+int launch_build_index(PatchIndex& ix, const uint8_t* obs, const float* values, const int32_t* counts,
+                       cudaStream_t st) {
+  PB_CUDA_TRY(cudaMemsetAsync(ix.cmax_dev, 0, 4, st));
+  k_tile_totals<<<ix.ntiles, 256, 0, st>>>(counts, ix.n, ix.tile_tot, ix.cmax_dev);
+  k_tile_scan<<<1, 1024, 0, st>>>(ix.tile_tot, ix.ntiles, ix.tile_base);
+  k_tile_fill<<<ix.ntiles, kTile, 0, st>>>(obs, values, counts, ix.n, ix.p, ix.tile_base, ix.colptr, ix.e_loc,
+                                           ix.x_csc, ix.rowptr, ix.csr_p, ix.csr_pos);
+  PB_LAUNCH_CHECK();
+  return PB_OK;
+}
+
+int launch_scatter_x(const PatchIndex& ix, const float* values, const int32_t* counts, cudaStream_t st) {
+  k_scatter_x<<<(unsigned)ceil_div(ix.n, 256), 256, 0, st>>>(values, counts, ix.rowptr, ix.csr_p, ix.csr_pos, ix.n,
+                                                             ix.x_csc);
+  PB_LAUNCH_CHECK();
+  return PB_OK;
+}
+
+}  // namespace pb

@@ -1,0 +1,30 @@
+// pb200 — observed-element index (pb_index.cu) shared by the compact sweep kernels.
+#pragma once
+#include "pb_common.cuh"
+
+namespace pb {
+
+constexpr int kTile = 1024;  // patches per CSC tile (one build block, one dict-step work unit)
+
+struct PatchIndex {
+  int64_t n;
+  int p;
+  int ntiles;
+  int32_t* tile_tot;    // [ntiles]
+  int64_t* tile_base;   // [ntiles + 1] first element of each tile; tile_base[ntiles] = nnz
+  int32_t* colptr;      // [ntiles][p + 1] global element offset of each column
+  int64_t* rowptr;      // [n + 1] first CSR slot of each patch
+  uint16_t* e_loc;      // [nnz] CSC: patch index inside its tile
+  float* x_csc;         // [nnz] CSC: observed (mean-subtracted) value
+  uint16_t* csr_p;      // [nnz] CSR: patch offset p of each slot
+  uint32_t* csr_pos;    // [nnz] CSR: CSC position of each slot
+  int32_t* cmax_dev;    // max observed count over patches
+};
+
+int index_bytes(int64_t n, int p, int64_t nnz, size_t* out);
+void carve_index(PatchIndex& ix, char* base, int64_t n, int p, int64_t nnz);
+int launch_build_index(PatchIndex& ix, const uint8_t* obs, const float* values, const int32_t* counts,
+                       cudaStream_t st);
+int launch_scatter_x(const PatchIndex& ix, const float* values, const int32_t* counts, cudaStream_t st);
+
+}  // namespace pb

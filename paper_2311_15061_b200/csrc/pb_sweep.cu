@@ -1,26 +1,11 @@
-// pb200 — the BPFA Gibbs sweep on sm_100a.
+// pb200 — dense helper kernels of the Gibbs sweep on sm_100a.
 //
-// Reference: pkg/src/patchbeam/bpfa.py:278-345 (gibbs_epoch) and the seven Numba
-// kernels of pkg/src/patchbeam/_kernels.py.  One epoch here is:
-//
-//   k_residual        R = o * (X - (Z*S) D)                       (_kernels.py:18-31)
-//   k_dict_step       persistent cooperative kernel, atoms k = 0..K-1 in order:
-//                     A_k, C_k block partials -> last-arriving CTA reduces them in
-//                     fixed CTA order, draws d_k = mu + g/sqrt(lambda), publishes
-//                     delta_k; every CTA shifts its resident tile of R and, in the
-//                     same pass, accumulates the next atom's moments
-//                     (bpfa.py:299-307, _kernels.py:34-74)
-//   k_code_step       one thread group per patch, the patch's residual in registers,
-//                     the dictionary in shared memory, atoms k = 0..K-1 in order:
-//                     u, v dot products, the z/s conditional draw, register shift
-//                     (bpfa.py:240-275, _kernels.py:77-109); epilogue block sums of
-//                     sum S^2, sum R^2 and per-atom usage counts m_k (bpfa.py:313-328)
-//   k_finish_stats    fixed-order reduction of the block partials
-//   k_draw_pi_gamma   (philox mode) pi ~ Beta, gamma_s, gamma_eps ~ Gamma on device
-//
-// Compute precision: f32 state and FMAs; cross-patch sums accumulate in f64 at
-// block/grid level; the z/s conditional algebra is f32 (numpy mode compares the
-// reference's exact logistic draw in f64).
+// The epoch itself runs on the observed-element ("compact") kernels of
+// pb_compact.cu.  This file holds the dense (P,N) kernels behind the fine-grained
+// seam of the C ABI (one per reference _kernels.* function, _kernels.py:18-145),
+// the dense compose used for overlap-add (every p, not only observed), the
+// epoch statistics finish, and the device pi/gamma draws of philox mode
+// (bpfa.py:313-342).
 #include <math.h>
 
 #include "pb_sweep.cuh"
@@ -86,251 +71,6 @@ __global__ void __launch_bounds__(256) k_accumulate_atoms(
     const int pe = j * G + g;
     if (pe < p) *o = (RESID && !((ob >> j) & 1ull)) ? 0.0f : acc[j];
   }
-}
-
-// ---------------------------------------------------------------------------
-// Dictionary step: persistent cooperative kernel (all CTAs co-resident).
-
-
-__device__ __forceinline__ float active_w(const uint8_t* usage, const float* weights, int64_t idx) {
-  return usage[idx] ? weights[idx] : 0.0f;
-}
-
-__global__ void __launch_bounds__(512) k_dict_step(DictArgs a) {
-  extern __shared__ float sm[];
-  const int tile = a.tile;
-  float* wprev = sm;                 // tile
-  float* wcur = wprev + tile;        // tile
-  float* acc = wcur + tile;          // 2P  (A then C)
-  float* dprev = acc + 2 * a.p;      // P
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int64_t per = ceil_div(a.n, gridDim.x);
-  const int64_t lo = min((int64_t)blockIdx.x * per, a.n), hi = min(lo + per, a.n);
-  const int epoch = a.sc->epoch + 1;
-  const double geps = a.sc->gamma_eps;
-
-  for (int k = 0; k <= a.k_len; ++k) {
-    for (int t = threadIdx.x; t < 2 * a.p; t += blockDim.x) acc[t] = 0.0f;
-    for (int64_t t0 = lo; t0 < hi; t0 += tile) {
-      const int tn = (int)min((int64_t)tile, hi - t0);
-      __syncthreads();
-      for (int t = threadIdx.x; t < tn; t += blockDim.x) {
-        wprev[t] = k > 0 ? active_w(a.usage, a.weights, (int64_t)(k - 1) * a.n + t0 + t) : 0.0f;
-        wcur[t] = k < a.k_len ? active_w(a.usage, a.weights, (int64_t)k * a.n + t0 + t) : 0.0f;
-      }
-      __syncthreads();
-      for (int pr = wid; pr < a.p; pr += nw) {
-        const float dl = k > 0 ? dprev[pr] : 0.0f;
-        float sa = 0.0f, sc = 0.0f;
-        float* rrow = a.resid + (int64_t)pr * a.n + t0;
-        const uint8_t* orow = a.obs + (int64_t)pr * a.n + t0;
-        for (int t = lane; t < tn; t += 32) {
-          if (!orow[t]) continue;
-          const float wp = wprev[t], wc = wcur[t];
-          if (wp == 0.0f && wc == 0.0f) continue;
-          float r = rrow[t];
-          if (wp != 0.0f) {
-            r = fmaf(wp, dl, r);
-            rrow[t] = r;
-          }
-          sa = fmaf(wc, wc, sa);
-          sc = fmaf(wc, r, sc);
-        }
-        if (k < a.k_len) {
-          sa = warp_sum(sa);
-          sc = warp_sum(sc);
-          if (lane == 0) {
-            acc[pr] += sa;
-            acc[a.p + pr] += sc;
-          }
-        }
-      }
-    }
-    if (k == a.k_len) break;
-    __syncthreads();
-    // publish this CTA's partial moments for atom k
-    double* mine = a.partials + (size_t)blockIdx.x * 2 * a.p;
-    for (int t = threadIdx.x; t < 2 * a.p; t += blockDim.x) mine[t] = (double)acc[t];
-    __shared__ unsigned int s_last;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      const unsigned int ticket = atomicAdd(&a.sync[0], 1u);
-      s_last = (ticket == (unsigned int)(k + 1) * gridDim.x - 1u) ? 1u : 0u;
-    }
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      // fixed-order cross-CTA reduction, then the atom draw (bpfa.py:161-166, 303-307)
-      for (int pe = threadIdx.x; pe < a.p; pe += blockDim.x) {
-        double sa = 0.0, sc = 0.0;
-        for (int b = 0; b < (int)gridDim.x; ++b) {
-          sa += __ldcg(a.partials + (size_t)b * 2 * a.p + pe);
-          sc += __ldcg(a.partials + (size_t)b * 2 * a.p + a.p + pe);
-        }
-        const double dold = (double)a.atoms[(int64_t)k * a.p + pe];
-        const double lam = (double)a.p + geps * sa;
-        const double mu = geps * (sc + dold * sa) / lam;
-        double gdraw;
-        if (a.draws) {
-          gdraw = a.draws[(int64_t)k * a.p + pe];
-        } else {
-          const u32x4 r = philox4x32_10(u32x4{(uint32_t)(pe >> 1), (uint32_t)k, (uint32_t)epoch, kDomAtom << 24},
-                                        a.key0, a.key1);
-          float n0, n1;
-          box_muller(r.x, r.y, n0, n1);
-          gdraw = (pe & 1) ? n1 : n0;
-        }
-        const float dnew = (float)(mu + gdraw / sqrt(lam));
-        a.atoms[(int64_t)k * a.p + pe] = dnew;
-        a.delta[pe] = (float)dold - dnew;
-      }
-      __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0) atomicExch(&a.sync[1], (unsigned int)(k + 1));
-    }
-    if (threadIdx.x == 0) {
-      while (atomicAdd(&a.sync[1], 0u) < (unsigned int)(k + 1)) __nanosleep(32);
-      __threadfence();
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < a.p; t += blockDim.x) dprev[t] = __ldcg(a.delta + t);
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Code step.
-
-
-template <int G>
-__device__ __forceinline__ float group_sum(float v) {
-#pragma unroll
-  for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-template <int VPT, int G, int MODE>
-__global__ void __launch_bounds__(256) k_code_step(CodeArgs a) {
-  extern __shared__ float sm[];
-  float* logit = sm;                       // K
-  int* mcnt = (int*)(logit + a.k_len);     // K
-  float* ds = (float*)(mcnt + a.k_len);    // kc * P
-  __shared__ double red[32];
-  const int g = threadIdx.x % G;
-  const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
-  const bool live = i < a.n;
-  const int lane = threadIdx.x & 31;
-  const int epoch = a.sc->epoch + 1;
-  const float geps = (float)a.sc->gamma_eps, gs = (float)a.sc->gamma_s;
-  const float inv_sqrt_gs = (float)(1.0 / sqrt(a.sc->gamma_s));
-
-  for (int k = threadIdx.x; k < a.k_len; k += blockDim.x) {
-    double pk = a.pi[k];
-    pk = fmin(fmax(pk, 1e-15), 1.0 - 1e-15);  // bpfa.py:173
-    logit[k] = (float)(log(pk) - log1p(-pk));
-    mcnt[k] = 0;
-  }
-  float r[VPT];
-  uint64_t ob = 0;
-#pragma unroll
-  for (int j = 0; j < VPT; ++j) {
-    const int pe = j * G + g;
-    r[j] = 0.0f;
-    if (live && pe < a.p) {
-      r[j] = a.resid[(int64_t)pe * a.n + i];
-      if (a.obs[(int64_t)pe * a.n + i]) ob |= 1ull << j;
-    }
-  }
-  double sq_w = 0.0;
-  u32x4 rnd{0, 0, 0, 0};
-  float nrm0 = 0.f, nrm1 = 0.f;
-  constexpr int PP = VPT * G;  // shared-memory row pitch, zero padded past p
-  for (int k0 = 0; k0 < a.k_len; k0 += a.kc) {
-    const int kn = min(a.kc, a.k_len - k0);
-    __syncthreads();
-    for (int t = threadIdx.x; t < kn * PP; t += blockDim.x) {
-      const int kk = t / PP, pe = t - kk * PP;
-      ds[t] = pe < a.p ? a.atoms[(int64_t)(k0 + kk) * a.p + pe] : 0.0f;
-    }
-    __syncthreads();
-    for (int kk = 0; kk < kn; ++kk) {
-      const int k = k0 + kk;
-      const float* d = ds + kk * PP + g;
-      float u = 0.0f, v = 0.0f;
-#pragma unroll
-      for (int j = 0; j < VPT; ++j) {
-        const float dj = d[j * G];
-        const float dm = ((ob >> j) & 1ull) ? dj : 0.0f;
-        u = fmaf(dm, dm, u);
-        v = fmaf(dj, r[j], v);
-      }
-      if (G > 1) {
-        u = group_sum<G>(u);
-        v = group_sum<G>(v);
-      }
-      // Re-read d from shared memory for the shift instead of holding VPT more
-      // registers across the draw (keeps the residual itself register-resident).
-      asm volatile("" ::: "memory");
-      bool z = false;
-      if (live) {
-        const int64_t zi = (int64_t)k * a.n + i;
-        const bool z_old = a.usage[zi] != 0;
-        const float s_old = a.weights[zi];
-        const float w_old = z_old ? s_old : 0.0f;
-        // _code_params (bpfa.py:169-178)
-        const float proj = fmaf(w_old, u, v);
-        const float log_rho = logit[k] - 0.5f * geps * (s_old * s_old * u - 2.0f * s_old * proj);
-        const float alpha = fmaf(geps, u, gs);
-        const float mean = geps * proj / alpha;
-        float gn;
-        if (MODE == kRngReplay) {
-          const double ud = a.u_draw[zi];
-          gn = (float)a.g_draw[zi];
-          z = (log(ud) - log1p(-ud)) < (double)log_rho;  // bpfa.py:262-263
-        } else {
-          if ((k & 1) == 0) {
-            rnd = philox4x32_10(u32x4{(uint32_t)i, (uint32_t)(i >> 32), (uint32_t)(k >> 1),
-                                      ((uint32_t)epoch & 0xFFFFFFu) | (kDomCode << 24)},
-                                a.key0, a.key1);
-            box_muller(rnd.z, rnd.w, nrm0, nrm1);
-          }
-          const float uu = u01_24((k & 1) ? rnd.y : rnd.x);
-          gn = (k & 1) ? nrm1 : nrm0;
-          // z = 1 w.p. sigmoid(log_rho): U < 1/(1+exp(-log_rho))
-          z = uu * (1.0f + __expf(-log_rho)) < 1.0f;
-        }
-        const float s_new = z ? mean + gn * rsqrtf(alpha) : gn * inv_sqrt_gs;  // bpfa.py:265-269
-        const float dw = w_old - (z ? s_new : 0.0f);
-        if (dw != 0.0f) {
-#pragma unroll
-          for (int j = 0; j < VPT; ++j)
-            if ((ob >> j) & 1ull) r[j] = fmaf(dw, d[j * G], r[j]);
-        }
-        if (g == 0) {
-          a.usage[zi] = z ? 1 : 0;
-          a.weights[zi] = s_new;
-          sq_w += (double)s_new * (double)s_new;
-        }
-      }
-      // usage count for pi (bpfa.py:217-222): one ballot per warp
-      const unsigned bal = __ballot_sync(0xffffffffu, z && g == 0);
-      if (lane == 0 && bal) atomicAdd(&mcnt[k], __popc(bal));
-    }
-  }
-  double sq_r = 0.0;
-#pragma unroll
-  for (int j = 0; j < VPT; ++j) sq_r += (double)r[j] * (double)r[j];
-  const double bw = block_sum_d(sq_w, red);
-  __syncthreads();
-  const double br = block_sum_d(sq_r, red);
-  if (threadIdx.x == 0) {
-    a.block_sums[2 * blockIdx.x] = bw;
-    a.block_sums[2 * blockIdx.x + 1] = br;
-  }
-  __syncthreads();
-  for (int k = threadIdx.x; k < a.k_len; k += blockDim.x)
-    if (mcnt[k]) atomicAdd(&a.m_count[k], mcnt[k]);
 }
 
 __global__ void k_finish_stats(const double* __restrict__ block_sums, int nblocks, SweepScalars* sc) {
@@ -589,51 +329,6 @@ int launch_accumulate_atoms(bool resid, const float* values, const uint8_t* obs,
   }
   PB_DISPATCH_VG(vpt, g, PB_ACC)
 #undef PB_ACC
-  PB_LAUNCH_CHECK();
-  return PB_OK;
-}
-
-int dict_step_grid(int p, int& blocks, int& threads, size_t& smem, int& tile) {
-  threads = 512;
-  tile = 2048;
-  smem = (size_t)(2 * tile + 3 * p) * sizeof(float);
-  if (smem > 200 * 1024) { set_error("patch size too large for dict step"); return PB_EUNSUPPORTED; }
-  PB_CUDA_TRY(cudaFuncSetAttribute(k_dict_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  PB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dict_step, threads, smem));
-  if (per_sm < 1) { set_error("dict step cannot be resident"); return PB_EUNSUPPORTED; }
-  blocks = sm_count() * (per_sm > 2 ? 2 : per_sm);
-  return PB_OK;
-}
-
-int launch_dict_step(const DictArgs& a_in, int blocks, int threads, size_t smem, cudaStream_t st) {
-  DictArgs a = a_in;
-  PB_CUDA_TRY(cudaMemsetAsync(a.sync, 0, 2 * sizeof(unsigned int), st));
-  void* args[] = {&a};
-  PB_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_dict_step, dim3(blocks), dim3(threads), args, smem, st));
-  return PB_OK;
-}
-
-int launch_code_step(const CodeArgs& a_in, int mode, int& nblocks, cudaStream_t st) {
-  CodeArgs a = a_in;
-  int vpt, g;
-  if (!pick_layout(a.p, vpt, g)) { set_error("patch size %d exceeds 2048", a.p); return PB_EUNSUPPORTED; }
-  const int th = 256;
-  a.kc = pick_kc(a.k_len, vpt * g, 100 * 1024);
-  const size_t smem = (size_t)a.kc * vpt * g * 4 + (size_t)a.k_len * 8;
-  if (smem > 220 * 1024) { set_error("too many atoms for the code step (K=%d)", a.k_len); return PB_EUNSUPPORTED; }
-  const int64_t nb = ceil_div(a.n * g, th);
-  nblocks = (int)nb;
-  PB_CUDA_TRY(cudaMemsetAsync(a.m_count, 0, (size_t)a.k_len * sizeof(int32_t), st));
-#define PB_CODE(V, GG)                                                                                   \
-  case V * 100 + GG: {                                                                                   \
-    auto kern = mode == kRngReplay ? k_code_step<V, GG, kRngReplay> : k_code_step<V, GG, kRngPhilox>;    \
-    PB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));     \
-    kern<<<(unsigned)nb, th, smem, st>>>(a);                                                             \
-    break;                                                                                               \
-  }
-  PB_DISPATCH_VG(vpt, g, PB_CODE)
-#undef PB_CODE
   PB_LAUNCH_CHECK();
   return PB_OK;
 }

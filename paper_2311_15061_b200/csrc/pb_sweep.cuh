@@ -16,39 +16,6 @@ struct SweepScalars {   // device-resident per-problem scalars
 };
 static_assert(sizeof(SweepScalars) == 40, "SweepScalars must match pb_scalars");
 
-struct DictArgs {
-  float* resid;             // (P,N) in/out
-  const uint8_t* obs;       // (P,N)
-  const uint8_t* usage;     // (K,N)
-  const float* weights;     // (K,N)
-  float* atoms;             // (K,P) in/out
-  const double* draws;      // (K,P) replay normals, or null (philox)
-  const SweepScalars* sc;
-  double* partials;         // gridDim * 2P
-  float* delta;             // P
-  unsigned int* sync;       // [0] arrival counter, [1] published atom count
-  int64_t n;
-  int p, k_len, tile;
-  uint32_t key0, key1;
-};
-
-struct CodeArgs {
-  const float* resid;       // (P,N) residual after the dictionary step
-  const uint8_t* obs;       // (P,N)
-  uint8_t* usage;           // (K,N) in/out
-  float* weights;           // (K,N) in/out
-  const float* atoms;       // (K,P)
-  const double* pi;         // (K)
-  const double* u_draw;     // (K,N) replay uniforms or null
-  const double* g_draw;     // (K,N) replay normals or null
-  const SweepScalars* sc;
-  double* block_sums;       // gridDim * 2  (sum S^2, sum R^2)
-  int32_t* m_count;         // (K) usage counts (atomic, integer => deterministic)
-  int64_t n;
-  int p, k_len, kc;
-  uint32_t key0, key1;
-};
-
 // pb_patches.cu
 int launch_extract(const Grid&, const void*, int, const uint8_t*, int, float*, uint8_t*, float*, int32_t*,
                    cudaStream_t);
@@ -59,9 +26,6 @@ int launch_coverage(const Grid&, int32_t*, cudaStream_t);
 int launch_accumulate_atoms(bool resid, const float* values, const uint8_t* obs, const uint8_t* usage,
                             const float* weights, const float* atoms, float* out, int64_t n, int p, int k_len,
                             int accumulate, cudaStream_t st);
-int dict_step_grid(int p, int& blocks, int& threads, size_t& smem, int& tile);
-int launch_dict_step(const DictArgs&, int blocks, int threads, size_t smem, cudaStream_t);
-int launch_code_step(const CodeArgs&, int mode, int& nblocks, cudaStream_t);
 int launch_finish_stats(const double*, int, SweepScalars*, cudaStream_t);
 int launch_draw_pi_gamma(double*, const int32_t*, SweepScalars*, int, int64_t, int64_t, const double*, uint32_t,
                          uint32_t, cudaStream_t);

@@ -157,6 +157,46 @@ class PatchMatrix:
             self._cache["origins"] = np.stack([m.ravel() for m in mesh], axis=1)
         return self._cache["origins"]
 
+    def index(self) -> "_lib.PatchIndex":
+        """Observed-element index used by the sweep (pb_build_index), built once
+        per mask and refreshed if ``values``/``observed`` were edited in place
+        (tracked through the tensors' version counters)."""
+        c = self._cache
+        ov, vv = self.observed_pn._version, self.values_pn._version
+        if c.get("ix_obs_version") != ov:
+            self.counts = self.observed_pn.sum(dim=0, dtype=torch.int32)
+            self.n_obs = int(self.counts.sum(dtype=torch.int64).item())
+            n, p = self.num_patches, self.patch_size
+            nb = int(_lib.load().pb_index_bytes(n, p, self.n_obs))
+            ix = _lib.PatchIndex(n, p, 0, self.n_obs, 0, None)
+            buf = torch.empty((max(nb, 1),), dtype=torch.uint8, device=self.values_pn.device)
+            ix.buffer = buf.data_ptr()
+            _lib.call("pb_build_index", ctypes.byref(ix), _ptr(self.observed_pn), _ptr(self.values_pn),
+                      _ptr(self.counts), _stream())
+            c.update(ix=ix, ix_buf=buf, ix_obs_version=ov, ix_val_version=vv)
+        elif c.get("ix_val_version") != vv:
+            _lib.call("pb_index_refresh_values", ctypes.byref(c["ix"]), _ptr(self.values_pn), _ptr(self.counts),
+                      _stream())
+            c["ix_val_version"] = vv
+        return c["ix"]
+
+    @classmethod
+    def from_arrays(cls, values, observed, means=None, tensor_shape=None, spec=None):
+        """Build a device PatchMatrix from reference-layout (N,P) arrays (tests /
+        callers that assemble patch matrices themselves, cf. test_bpfa.py:264-293)."""
+        v = np.asarray(values, dtype=np.float64)
+        o = np.asarray(observed, dtype=bool)
+        n, p = v.shape
+        dev = torch.device("cuda")
+        values_pn = torch.as_tensor(np.ascontiguousarray(np.where(o, v, 0.0).T), dtype=torch.float32, device=dev)
+        obs_pn = torch.as_tensor(np.ascontiguousarray(o.T).astype(np.uint8), device=dev)
+        means_t = torch.as_tensor(np.zeros(n) if means is None else np.asarray(means), dtype=torch.float32,
+                                  device=dev)
+        counts = obs_pn.sum(dim=0, dtype=torch.int32)
+        spec = spec or PatchSpec((p,))
+        return cls(values_pn, obs_pn, means_t, counts, tuple(tensor_shape or (p,)), spec, False,
+                   int(o.sum()))
+
     def to_host(self):
         """Reference-typed numpy copy: values (N,P) f64, observed (N,P) bool, means (N,) f64."""
         return (self.values_pn.T.double().cpu().numpy(), self.observed_pn.T.bool().cpu().numpy(),

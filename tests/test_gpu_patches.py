@@ -126,3 +126,52 @@ def test_large_frame_indices_exact(cuda_device):
     assert np.array_equal(obs, opm.observed)
     assert np.abs(means - opm.means).max() <= TOL
     assert np.array_equal(pp.coverage_map(pm), op.coverage((512, 512), (8, 8), (1, 1)))
+
+
+def _carve(buf, n, p, nnz):
+    """Mirror of carve_index (pb_index.cu) to read the index back for checking."""
+    kt = 1024
+    nt = -(-n // kt)
+    out, off = {}, 0
+    for name, cnt, dt in [("tile_tot", nt, np.int32), ("tile_base", nt + 1, np.int64),
+                          ("colptr", nt * (p + 1), np.int32), ("rowptr", n + 1, np.int64),
+                          ("e_loc", nnz, np.uint16), ("x_csc", nnz, np.float32), ("csr_p", nnz, np.uint16),
+                          ("csr_pos", nnz, np.uint32)]:
+        nb = cnt * np.dtype(dt).itemsize
+        out[name] = buf[off:off + nb].view(dt)
+        off += (nb + 255) & ~255
+    return out
+
+
+@pytest.mark.parametrize("shape,patch,ratio,kind", [((40, 45), (8, 8), 0.25, "uniform-random"),
+                                                     ((70, 64), (8, 8), 0.25, "line-hop"),
+                                                     ((50, 41), (10, 10), 0.1, "uniform-random"),
+                                                     ((12, 10, 6), (4, 3, 6), 0.3, "uniform-random")])
+def test_observed_element_index_exact(cuda_device, shape, patch, ratio, kind):
+    from paper_2311_15061_b200 import inputs
+
+    rng = np.random.default_rng(0)
+    img = rng.random(shape)
+    mask = inputs.make_mask(shape, ratio, kind, 3)
+    pm = pp.extract_patches(img, mask, pp.PatchSpec(patch), True)
+    ix = pm.index()
+    vals, obs, _ = pm.to_host()
+    n, p = obs.shape
+    assert ix.nnz == obs.sum() and ix.cmax == obs.sum(1).max()
+    b = _carve(pm._cache["ix_buf"].cpu().numpy(), n, p, int(ix.nnz))
+    # CSR: per patch, ascending observed offsets; positions point at the same element in CSC
+    rows, cols = np.nonzero(obs)          # row-major => ascending (i, p)
+    assert np.array_equal(b["csr_p"].astype(np.int64), cols)
+    assert np.array_equal(b["rowptr"][:n], np.concatenate([[0], np.cumsum(obs.sum(1))[:-1]]))
+    pos = b["csr_pos"].astype(np.int64)
+    assert np.array_equal(np.sort(pos), np.arange(ix.nnz))
+    tile = rows // 1024
+    assert np.array_equal(b["e_loc"][pos].astype(np.int64), rows - tile * 1024)
+    assert np.array_equal(b["x_csc"][pos], vals[rows, cols].astype(np.float32))
+    cp = b["colptr"].reshape(-1, p + 1)
+    assert np.all((pos >= cp[tile, cols]) & (pos < cp[tile, cols + 1]))
+    # CSC order inside a column: ascending patch
+    for t in range(cp.shape[0]):
+        for pe in range(p):
+            seg = b["e_loc"][cp[t, pe]:cp[t, pe + 1]]
+            assert np.all(np.diff(seg.astype(np.int64)) > 0)
