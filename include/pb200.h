@@ -38,6 +38,11 @@ extern "C" {
 #define PB_ECUDA -5        /* CUDA runtime failure / no device                           */
 #define PB_EUNSUPPORTED -6 /* shape outside the compiled kernel envelope                 */
 
+#define PB_RESID_RECOMPUTE 0   /* residual_full from (X, Z, S, D) — the reference's behaviour */
+#define PB_RESID_FROM_VALUES 1 /* caller asserts Z*S == 0 (fresh / warm-reset codes): R = X */
+#define PB_RESID_CARRY 2       /* workspace holds the end residual of the previous epoch of this
+                                  exact state (same patch matrix, state untouched since)  */
+
 #define PB_RNG_REPLAY 0    /* draws supplied by the caller (reference numpy streams) */
 #define PB_RNG_PHILOX 1    /* device counter-based Philox4x32-10 draws               */
 
@@ -77,12 +82,12 @@ int pb_coverage_map(const pb_grid_desc* g, int32_t* out, void* stream);
 
 /* ---- fine-grained seam: one entry per reference _kernels.* function ---- */
 
-/* _kernels.residual_full (_kernels.py:18-31) */
+/* _kernels.residual_full (_kernels.py:18-31).  usage/weights rows have pitch ld >= n. */
 int pb_residual_full(const float* values, const uint8_t* observed, const uint8_t* usage, const float* weights,
-                     const float* atoms, float* out, int64_t n, int32_t p, int32_t k, void* stream);
+                     const float* atoms, float* out, int64_t n, int32_t p, int32_t k, int64_t ld, void* stream);
 /* _kernels.compose_estimates (_kernels.py:133-145); accumulate!=0 adds into out. */
 int pb_compose_estimates(const uint8_t* usage, const float* weights, const float* atoms, float* out, int64_t n,
-                         int32_t p, int32_t k, int32_t accumulate, void* stream);
+                         int32_t p, int32_t k, int64_t ld, int32_t accumulate, void* stream);
 /* _kernels.atom_moments (_kernels.py:34-62): a_out, c_out are device f64[P];
  * scratch: device f64[2 * P * 64]. */
 int pb_atom_moments(const float* resid, const uint8_t* observed, const float* w_col, int64_t n, int32_t p,
@@ -134,9 +139,11 @@ typedef struct pb_scalars {
 
 typedef struct pb_epoch_desc {
   int64_t n;
+  int64_t ld;               /* row pitch of usage/weights (K, ld); 0 => n */
   int32_t p, k;
   int32_t freeze_dict;      /* bpfa.gibbs_epoch(freeze_dict=...) */
   int32_t rng_mode;         /* PB_RNG_REPLAY or PB_RNG_PHILOX */
+  int32_t resid_mode;       /* PB_RESID_* */
   uint64_t seed;            /* GibbsState.seed */
   int64_t n_obs;            /* number of observed patch-matrix flags (bpfa.py:327) */
   double hyper[6];          /* Hyperparams a, b, c, d, e, f (bpfa.py:46-52) */
@@ -160,6 +167,9 @@ typedef struct pb_epoch_desc {
 } pb_epoch_desc;
 
 size_t pb_epoch_workspace_bytes(int64_t n, int32_t p, int32_t k, int64_t nnz);
+/* Recommended row pitch for (K, ld) usage/weights: n rounded up to 64 (aligned
+ * vector loads in the dictionary step).  Any ld >= n is accepted. */
+int64_t pb_code_pitch(int64_t n);
 
 /* One sweep through the dictionary and code steps.  After it returns (stream
  * ordered), scalars->sq_w / sq_r hold the epoch sums and m_counts_out (device
@@ -175,6 +185,10 @@ int pb_gibbs_epoch(const pb_epoch_desc* d, int32_t* m_counts_out, void* stream);
  * the epochs since enabling (single host thread use). */
 int pb_phase_timing(int32_t enable);
 int pb_phase_read(double* ms_out /* [4] */, int64_t* epochs_out);
+/* Profiling only: in-kernel globaltimer phases of the dictionary step, max over
+ * CTAs, accumulated since enabling: [staging, last-tile elements, pass-end
+ * reduce, grid sync 1, cross-CTA reduce, grid sync 2, atom update, elements]. */
+int pb_dict_profile(int32_t enable, double* slots_ns_out /* [8] or NULL */);
 
 /* ---- stateful problem (C-ABI with HOST buffers; the live submit_frame slice,
  *      pipeline.py:217-251).  Owns all device buffers. ---- */

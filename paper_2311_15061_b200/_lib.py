@@ -21,6 +21,10 @@ PB_EDIVERGED = -4
 PB_ECUDA = -5
 PB_EUNSUPPORTED = -6
 
+PB_RESID_RECOMPUTE = 0
+PB_RESID_FROM_VALUES = 1
+PB_RESID_CARRY = 2
+
 PB_RNG_REPLAY = 0
 PB_RNG_PHILOX = 1
 
@@ -44,8 +48,8 @@ class PatchIndex(ctypes.Structure):
 
 
 class EpochDesc(ctypes.Structure):
-    _fields_ = [("n", c_i64), ("p", c_i32), ("k", c_i32), ("freeze_dict", c_i32), ("rng_mode", c_i32),
-                ("seed", c_u64), ("n_obs", c_i64), ("hyper", c_f64 * 6),
+    _fields_ = [("n", c_i64), ("ld", c_i64), ("p", c_i32), ("k", c_i32), ("freeze_dict", c_i32), ("rng_mode", c_i32),
+                ("resid_mode", c_i32), ("seed", c_u64), ("n_obs", c_i64), ("hyper", c_f64 * 6),
                 ("values", c_vp), ("observed", c_vp), ("counts", c_vp), ("index", ctypes.POINTER(PatchIndex)),
                 ("atoms", c_vp), ("pi", c_vp), ("usage", c_vp),
                 ("weights", c_vp), ("scalars", c_vp), ("atom_draws", c_vp), ("code_u", c_vp),
@@ -69,8 +73,8 @@ SIGNATURES = {
     "pb_reconstitute": (c_i32, [ctypes.POINTER(GridDesc), c_vp, c_f32, c_vp, c_vp, c_vp, c_i32, c_i32,
                                 c_vp, c_vp, c_vp]),
     "pb_coverage_map": (c_i32, [ctypes.POINTER(GridDesc), c_vp, c_vp]),
-    "pb_residual_full": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_vp]),
-    "pb_compose_estimates": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp]),
+    "pb_residual_full": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_i64, c_vp]),
+    "pb_compose_estimates": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_i64, c_i32, c_vp]),
     "pb_atom_moments": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "pb_shift_atom": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp]),
     "pb_code_moments": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
@@ -80,9 +84,11 @@ SIGNATURES = {
     "pb_build_index": (c_i32, [ctypes.POINTER(PatchIndex), c_vp, c_vp, c_vp, c_vp]),
     "pb_index_refresh_values": (c_i32, [ctypes.POINTER(PatchIndex), c_vp, c_vp, c_vp]),
     "pb_epoch_workspace_bytes": (ctypes.c_size_t, [c_i64, c_i32, c_i32, c_i64]),
+    "pb_code_pitch": (c_i64, [c_i64]),
     "pb_gibbs_epoch": (c_i32, [ctypes.POINTER(EpochDesc), c_vp, c_vp]),
     "pb_phase_timing": (c_i32, [c_i32]),
     "pb_phase_read": (c_i32, [c_vp, c_vp]),
+    "pb_dict_profile": (c_i32, [c_i32, c_vp]),
     "pb_problem_create": (c_i32, [ctypes.POINTER(ProblemDesc), ctypes.POINTER(c_vp)]),
     "pb_problem_destroy": (c_i32, [c_vp]),
     "pb_problem_submit_frame": (c_i32, [c_vp, c_vp, c_vp, c_vp]),

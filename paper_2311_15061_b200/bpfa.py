@@ -101,13 +101,26 @@ class GibbsState:
     """Device-resident latent state of one problem (bpfa.py:83-101)."""
 
     def __init__(self, dictionary: Dictionary, usage_kn: torch.Tensor, weights_kn: torch.Tensor,
-                 scalars: torch.Tensor, seed: int):
+                 scalars: torch.Tensor, seed: int, codes_zero: bool = False):
         self.dictionary = dictionary
         self.usage_kn = usage_kn        # (K,N) uint8
         self.weights_kn = weights_kn    # (K,N) f32
         self.scalars = scalars          # 40-byte pb_scalars block (uint8 tensor)
         self.seed = int(seed)
         self._workspace = None
+        self._resid_key = None          # residual in the workspace belongs to this key
+        # codes known to be all zero at these tensor versions (fresh init / reset_codes)
+        self._zero_key = self._codes_key() if codes_zero else None
+
+    def _codes_key(self):
+        return (self.usage_kn._version, self.weights_kn._version, id(self.usage_kn), id(self.weights_kn))
+
+    def reset_codes(self):
+        """Zero Z and S in place (the live warm start, pipeline.py:232-233) and
+        remember that the next sweep may start from R = X."""
+        self.usage_kn.zero_()
+        self.weights_kn.zero_()
+        self._zero_key = self._codes_key()
 
     # -- reference-shaped views -------------------------------------------
     @property
@@ -117,6 +130,11 @@ class GibbsState:
     @property
     def weights(self):
         return self.weights_kn.T
+
+    @property
+    def ld(self):
+        """Row pitch of the (K, ld) code buffers."""
+        return self.usage_kn.stride(0)
 
     @property
     def num_patches(self):
@@ -157,8 +175,10 @@ class GibbsState:
         """Upload a reference-typed state ((N,K) usage/weights, (K,P) atoms)."""
         atoms_t = torch.as_tensor(np.asarray(atoms, dtype=np.float32), device=device).contiguous()
         pi_t = torch.as_tensor(np.asarray(pi, dtype=np.float64), device=device).contiguous()
-        u = torch.as_tensor(np.ascontiguousarray(np.asarray(usage, dtype=np.uint8).T), device=device)
-        w = torch.as_tensor(np.ascontiguousarray(np.asarray(weights, dtype=np.float32).T), device=device)
+        k, n = np.asarray(atoms).shape[0], np.asarray(usage).shape[0]
+        u, w = _alloc_codes(k, n, torch.device(device))
+        u.copy_(torch.as_tensor(np.ascontiguousarray(np.asarray(usage, dtype=np.uint8).T)))
+        w.copy_(torch.as_tensor(np.ascontiguousarray(np.asarray(weights, dtype=np.float32).T)))
         sc = _make_scalars(weight_precision, noise_precision, epoch, device)
         return cls(Dictionary(atoms_t, pi_t, tuple(patch_shape)), u, w, sc, seed)
 
@@ -169,6 +189,15 @@ class GibbsState:
             self._workspace = (key, torch.empty((nb,), dtype=torch.uint8, device=self.usage_kn.device),
                                torch.empty((k,), dtype=torch.int32, device=self.usage_kn.device))
         return self._workspace[1], self._workspace[2]
+
+
+def _alloc_codes(k, n, device):
+    """Zeroed (K, N) usage/weights views of row-pitched (K, ld) buffers
+    (ld = pb_code_pitch(N): aligned vector loads in the dictionary step)."""
+    ld = int(_lib.load().pb_code_pitch(n))
+    u = torch.zeros((k, ld), dtype=torch.uint8, device=device)
+    w = torch.zeros((k, ld), dtype=torch.float32, device=device)
+    return u[:, :n], w[:, :n]
 
 
 def _make_scalars(gs, ge, epoch, device):
@@ -205,10 +234,10 @@ def init_state(pm: PatchMatrix, hp: Hyperparams, seed: int, init_mode: str = "da
     pi0 = hp.concentration_a / (hp.concentration_a + hp.concentration_b)
     d = Dictionary(torch.as_tensor(atoms, dtype=torch.float32, device=dev).contiguous(),
                    torch.full((k,), pi0, dtype=torch.float64, device=dev), tuple(pm.spec.patch_shape))
-    return GibbsState(d, torch.zeros((k, n), dtype=torch.uint8, device=dev),
-                      torch.zeros((k, n), dtype=torch.float32, device=dev),
+    return GibbsState(d, *_alloc_codes(k, n, dev),
                       _make_scalars(max(hp.weight_shape / hp.weight_rate, PRECISION_FLOOR),
-                                    max(hp.noise_shape / hp.noise_rate, PRECISION_FLOOR), 0, dev), seed)
+                                    max(hp.noise_shape / hp.noise_rate, PRECISION_FLOOR), 0, dev), seed,
+                      codes_zero=True)
 
 
 def install_dictionary(state_seed: int, pm: PatchMatrix, hp: Hyperparams, dictionary: Dictionary) -> GibbsState:
@@ -221,22 +250,37 @@ def install_dictionary(state_seed: int, pm: PatchMatrix, hp: Hyperparams, dictio
     pi = torch.as_tensor(np.asarray(dictionary.pi.cpu() if isinstance(dictionary.pi, torch.Tensor)
                                     else dictionary.pi), dtype=torch.float64, device=dev).contiguous()
     return GibbsState(Dictionary(atoms, pi, tuple(dictionary.patch_shape)),
-                      torch.zeros((k, n), dtype=torch.uint8, device=dev),
-                      torch.zeros((k, n), dtype=torch.float32, device=dev),
+                      *_alloc_codes(k, n, dev),
                       _make_scalars(max(hp.weight_shape / hp.weight_rate, PRECISION_FLOOR),
-                                    max(hp.noise_shape / hp.noise_rate, PRECISION_FLOOR), 0, dev), state_seed)
+                                    max(hp.noise_shape / hp.noise_rate, PRECISION_FLOOR), 0, dev), state_seed,
+                      codes_zero=True)
 
 
 # --- the sweep ---------------------------------------------------------------
+
+def _resid_key(state: GibbsState, pm: PatchMatrix, ws):
+    a = state.dictionary.atoms
+    return (id(pm), pm.values_pn._version, pm.observed_pn._version, id(pm._cache.get("ix_buf")),
+            state._codes_key(), id(a), a._version, ws.data_ptr())
+
 
 def _epoch_desc(state: GibbsState, pm: PatchMatrix, hp: Hyperparams, freeze: bool, mode: int):
     n, p, k = pm.num_patches, pm.patch_size, state.num_atoms
     ix = pm.index()
     ws, m = state.workspace(n, p, k, pm.n_obs)
     d = _lib.EpochDesc()
+    key = _resid_key(state, pm, ws)
+    if state._resid_key == key:
+        d.resid_mode = _lib.PB_RESID_CARRY            # residual of this exact state is resident
+    elif state._zero_key == state._codes_key():
+        d.resid_mode = _lib.PB_RESID_FROM_VALUES      # Z*S == 0  =>  R = X
+    else:
+        d.resid_mode = _lib.PB_RESID_RECOMPUTE        # residual_full (bpfa.py:297)
+    state._resid_key = key
     d.index = ctypes.pointer(ix)
     d.counts = pm.counts.data_ptr()
     d.n, d.p, d.k = n, p, k
+    d.ld = state.ld
     d.freeze_dict = int(bool(freeze))
     d.rng_mode = mode
     d.seed = state.seed & 0xFFFFFFFFFFFFFFFF
@@ -331,7 +375,7 @@ def compose_estimates(state: GibbsState, out: torch.Tensor | None = None, accumu
     if out is None:
         out = torch.empty((p, n), dtype=torch.float32, device=state.usage_kn.device)
     _lib.call("pb_compose_estimates", _ptr(state.usage_kn), _ptr(state.weights_kn),
-              _ptr(state.dictionary.atoms), _ptr(out), n, p, k, int(accumulate), _stream())
+              _ptr(state.dictionary.atoms), _ptr(out), n, p, k, state.ld, int(accumulate), _stream())
     return out.T
 
 
@@ -400,7 +444,7 @@ def _residual(pm: PatchMatrix, state: GibbsState) -> torch.Tensor:
     out = torch.empty_like(pm.values_pn)
     _lib.call("pb_residual_full", _ptr(pm.values_pn), _ptr(pm.observed_pn), _ptr(state.usage_kn),
               _ptr(state.weights_kn), _ptr(state.dictionary.atoms), _ptr(out), pm.num_patches, pm.patch_size,
-              state.num_atoms, _stream())
+              state.num_atoms, state.ld, _stream())
     return out
 
 
@@ -458,7 +502,7 @@ def gamma_posteriors(pm: PatchMatrix, state: GibbsState, hp: Hyperparams):
     dev = pm.values_pn.device
     scratch = torch.empty((256,), dtype=torch.float64, device=dev)
     out = torch.empty((1,), dtype=torch.float64, device=dev)
-    _lib.call("pb_masked_sq_norm", _ptr(state.weights_kn), n * k, _ptr(out), _ptr(scratch), _stream())
+    _lib.call("pb_masked_sq_norm", _ptr(state.weights_kn), state.ld * k, _ptr(out), _ptr(scratch), _stream())
     sq_w = float(out.item())
     r = _residual(pm, state)
     _lib.call("pb_masked_sq_norm", _ptr(r), n * pm.patch_size, _ptr(out), _ptr(scratch), _stream())

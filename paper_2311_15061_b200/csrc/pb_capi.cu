@@ -46,6 +46,8 @@ static int make_grid(const pb_grid_desc* d, Grid& g) {
 // Epoch workspace carve-up
 struct EpochWs {
   float* r_csc;
+  float* wt;        // tile-blocked code copy [tile][k/8][patch][8]
+  size_t wt_bytes;
   float* partials;
   double* reduced;
   unsigned* bar;
@@ -58,13 +60,16 @@ static size_t ws_bytes(int64_t n, int p, int k, int64_t nnz, EpochWs* ws, char* 
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return base ? base + o : nullptr; };
   char* r = take((size_t)nnz * 4);
+  const size_t wtb = (size_t)ceil_div(n, kTile) * ceil_div(k, kWB) * kTile * kWB * 4;
+  char* wt = take(wtb);
   char* pa = take(dict_gram_partials_bytes(p, kMaxDictBlocks));
   char* rd = take(dict_gram_reduced_bytes(p));
   char* bar = take(16);
   char* bs = take((size_t)ceil_div(n * 32, 256) * 2 * 8);  // upper bound of code-step blocks
   char* mc = take((size_t)k * 4);
   if (ws) {
-    ws->r_csc = (float*)r; ws->partials = (float*)pa; ws->reduced = (double*)rd;
+    ws->r_csc = (float*)r; ws->wt = (float*)wt; ws->wt_bytes = wtb;
+    ws->partials = (float*)pa; ws->reduced = (double*)rd;
     ws->bar = (unsigned*)bar; ws->block_sums = (double*)bs; ws->m_count = (int32_t*)mc;
   }
   return off;
@@ -86,31 +91,34 @@ static void device_key(uint64_t seed, uint32_t& k0, uint32_t& k1) {
 }
 
 // Optional phase timing (bench / profiling): events bracketing the epoch's
-// kernels, accumulated per phase on the launching stream.
+// kernels on the launching stream, one fresh event set per epoch (no host
+// synchronization until pb_phase_read).
 enum { kPhResid = 0, kPhDict, kPhCode, kPhStats, kPhEnd, kNumPh };
+struct PhaseSet { cudaEvent_t ev[kNumPh]; };
 static bool g_phase_on = false;
-static cudaEvent_t g_ev[kNumPh];
-static double g_phase_ms[kNumPh - 1];
-static long g_phase_n = 0;
-static bool g_phase_pending = false;
+static std::vector<PhaseSet> g_phase_sets;
+static size_t g_phase_used = 0;
+static PhaseSet* g_phase_cur = nullptr;
 
-static void phase_mark(int ph, cudaStream_t st) {
-  if (g_phase_on) cudaEventRecord(g_ev[ph], st);
-}
-static void phase_collect() {
-  if (!g_phase_on || !g_phase_pending) return;
-  cudaEventSynchronize(g_ev[kPhEnd]);
-  for (int i = 0; i < kNumPh - 1; ++i) {
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, g_ev[i], g_ev[i + 1]);
-    g_phase_ms[i] += ms;
+static void phase_begin() {
+  g_phase_cur = nullptr;
+  if (!g_phase_on) return;
+  if (g_phase_used == g_phase_sets.size()) {
+    PhaseSet ps;
+    for (int i = 0; i < kNumPh; ++i) cudaEventCreate(&ps.ev[i]);
+    g_phase_sets.push_back(ps);
   }
-  ++g_phase_n;
-  g_phase_pending = false;
+  g_phase_cur = &g_phase_sets[g_phase_used++];
 }
+static void phase_mark(int ph, cudaStream_t st) {
+  if (g_phase_cur) cudaEventRecord(g_phase_cur->ev[ph], st);
+}
+
+// Optional in-kernel phase profile of the dictionary step (globaltimer, CTA 0..n thread 0).
+static unsigned long long* g_dict_prof = nullptr;
 
 static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
-  phase_collect();
+  phase_begin();
   if (d->n < 1 || d->p < 1 || d->k < 1) { set_error("empty problem"); return PB_ESHAPE; }
   if (!d->index || !d->index->buffer || d->index->n != d->n || d->index->p != d->p) {
     set_error("pb_gibbs_epoch needs the patch index of this patch matrix (pb_build_index)");
@@ -131,22 +139,39 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
   CompactArgs c{};
   c.counts = d->counts; c.rowptr = ix.rowptr; c.csr_p = ix.csr_p; c.csr_pos = ix.csr_pos;
   c.x_csc = ix.x_csc; c.r_csc = ws.r_csc; c.cmax = d->index->cmax;
+  c.wt = ws.wt; c.nblk8 = (int)ceil_div(d->k, kWB);
   c.usage = d->usage; c.weights = d->weights; c.atoms = d->atoms; c.pi = d->pi; c.sc = sc;
   c.u_draw = d->rng_mode == PB_RNG_REPLAY ? d->code_u : nullptr;
   c.g_draw = d->rng_mode == PB_RNG_REPLAY ? d->code_g : nullptr;
   c.block_sums = ws.block_sums; c.m_count = ws.m_count;
   c.n = d->n; c.p = d->p; c.k = d->k; c.key0 = k0; c.key1 = k1;
+  c.ld = d->ld > d->n ? d->ld : d->n;
   phase_mark(kPhResid, st);
-  int rc = launch_resid_compact(c, st);
+  int rc = PB_OK;
+  if (d->resid_mode == PB_RESID_RECOMPUTE) {
+    rc = launch_resid_compact(c, st);                    // residual_full (bpfa.py:297)
+  } else if (d->resid_mode == PB_RESID_FROM_VALUES) {    // Z*S == 0  =>  R = X
+    if (cudaMemcpyAsync(ws.r_csc, ix.x_csc, (size_t)d->index->nnz * 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+        cudaMemsetAsync(ws.wt, 0, ws.wt_bytes, st) != cudaSuccess) {
+      set_error("residual copy failed");
+      rc = PB_ECUDA;
+    }
+  } else if (d->resid_mode != PB_RESID_CARRY) {
+    set_error("bad resid_mode %d", d->resid_mode);
+    rc = PB_EVALUE;
+  }
   if (rc) return rc;
   phase_mark(kPhDict, st);
   if (!d->freeze_dict) {
     DictGramArgs g{};
     g.tile_base = ix.tile_base; g.colptr = ix.colptr; g.e_loc = ix.e_loc; g.ntiles = ix.ntiles;
+    g.wt = ws.wt; g.nblk8 = c.nblk8;
     g.r_csc = ws.r_csc; g.usage = d->usage; g.weights = d->weights; g.atoms = d->atoms;
     g.draws = d->rng_mode == PB_RNG_REPLAY ? d->atom_draws : nullptr;
     g.sc = sc; g.partials = ws.partials; g.reduced = ws.reduced; g.bar = ws.bar; g.max_blocks = kMaxDictBlocks;
+    g.prof = g_dict_prof;
     g.n = d->n; g.p = d->p; g.k = d->k; g.key0 = k0; g.key1 = k1;
+    g.ld = c.ld;
     if ((rc = launch_dict_gram(g, st))) return rc;
   }
   int nblocks = 0;
@@ -157,7 +182,6 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
   if (d->rng_mode == PB_RNG_PHILOX)
     rc = launch_draw_pi_gamma(d->pi, ws.m_count, sc, d->k, d->n, d->n_obs, d->hyper, k0, k1, st);
   phase_mark(kPhEnd, st);
-  g_phase_pending = g_phase_on;
   return rc;
 }
 
@@ -214,13 +238,14 @@ int pb_coverage_map(const pb_grid_desc* d, int32_t* out, void* stream) {
 }
 
 int pb_residual_full(const float* values, const uint8_t* observed, const uint8_t* usage, const float* weights,
-                     const float* atoms, float* out, int64_t n, int32_t p, int32_t k, void* stream) {
-  return launch_accumulate_atoms(true, values, observed, usage, weights, atoms, out, n, p, k, 0, (cudaStream_t)stream);
+                     const float* atoms, float* out, int64_t n, int32_t p, int32_t k, int64_t ld, void* stream) {
+  return launch_accumulate_atoms(true, values, observed, usage, weights, atoms, out, n, p, k, 0, ld,
+                                 (cudaStream_t)stream);
 }
 
 int pb_compose_estimates(const uint8_t* usage, const float* weights, const float* atoms, float* out, int64_t n,
-                         int32_t p, int32_t k, int32_t accumulate, void* stream) {
-  return launch_accumulate_atoms(false, nullptr, nullptr, usage, weights, atoms, out, n, p, k, accumulate,
+                         int32_t p, int32_t k, int64_t ld, int32_t accumulate, void* stream) {
+  return launch_accumulate_atoms(false, nullptr, nullptr, usage, weights, atoms, out, n, p, k, accumulate, ld,
                                  (cudaStream_t)stream);
 }
 
@@ -252,6 +277,8 @@ size_t pb_epoch_workspace_bytes(int64_t n, int32_t p, int32_t k, int64_t nnz) {
   return ws_bytes(n, p, k, nnz, nullptr, nullptr);
 }
 
+int64_t pb_code_pitch(int64_t n) { return (n + 63) / 64 * 64; }
+
 size_t pb_index_bytes(int64_t n, int32_t p, int64_t nnz) {
   size_t b = 0;
   index_bytes(n, p, nnz, &b);
@@ -282,24 +309,41 @@ int pb_index_refresh_values(const pb_patch_index* pi, const float* values, const
   return launch_scatter_x(ix, values, counts, (cudaStream_t)stream);
 }
 
+int pb_dict_profile(int32_t enable, double* slots_ns_out) {
+  const size_t bytes = (size_t)kMaxDictBlocks * 8 * sizeof(unsigned long long);
+  if (slots_ns_out) {
+    for (int i = 0; i < 8; ++i) slots_ns_out[i] = 0.0;
+    if (g_dict_prof) {
+      std::vector<unsigned long long> h(kMaxDictBlocks * 8);
+      PB_CUDA_TRY(cudaDeviceSynchronize());
+      PB_CUDA_TRY(cudaMemcpy(h.data(), g_dict_prof, bytes, cudaMemcpyDeviceToHost));
+      for (int b = 0; b < kMaxDictBlocks; ++b)
+        for (int i = 0; i < 8; ++i) slots_ns_out[i] = std::max(slots_ns_out[i], (double)h[b * 8 + i]);
+    }
+  }
+  if (enable && !g_dict_prof) PB_CUDA_TRY(cudaMalloc(&g_dict_prof, bytes));
+  if (enable) PB_CUDA_TRY(cudaMemset(g_dict_prof, 0, bytes));
+  if (!enable && g_dict_prof) { cudaFree(g_dict_prof); g_dict_prof = nullptr; }
+  return PB_OK;
+}
+
 int pb_phase_timing(int32_t enable) {
-  if (enable && !g_phase_on) {
-    for (int i = 0; i < kNumPh; ++i) PB_CUDA_TRY(cudaEventCreate(&g_ev[i]));
-  }
-  if (!enable && g_phase_on) {
-    for (int i = 0; i < kNumPh; ++i) cudaEventDestroy(g_ev[i]);
-  }
   g_phase_on = enable != 0;
-  g_phase_pending = false;
-  for (int i = 0; i < kNumPh - 1; ++i) g_phase_ms[i] = 0.0;
-  g_phase_n = 0;
+  g_phase_used = 0;
   return PB_OK;
 }
 
 int pb_phase_read(double* ms_out, int64_t* epochs_out) {
-  phase_collect();
-  for (int i = 0; i < kNumPh - 1; ++i) ms_out[i] = g_phase_ms[i];
-  if (epochs_out) *epochs_out = g_phase_n;
+  for (int i = 0; i < kNumPh - 1; ++i) ms_out[i] = 0.0;
+  for (size_t e = 0; e < g_phase_used; ++e) {
+    PhaseSet& ps = g_phase_sets[e];
+    PB_CUDA_TRY(cudaEventSynchronize(ps.ev[kPhEnd]));
+    for (int i = 0; i < kNumPh - 1; ++i) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, ps.ev[i], ps.ev[i + 1]) == cudaSuccess) ms_out[i] += ms;
+    }
+  }
+  if (epochs_out) *epochs_out = (int64_t)g_phase_used;
   return PB_OK;
 }
 
@@ -319,6 +363,7 @@ struct pb_problem {
   pb_problem_desc desc;
   pb::Grid grid;
   int64_t n = 0;
+  int64_t ld = 0;  // row pitch of usage/weights
   int p = 0, k = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -374,10 +419,11 @@ int pb_problem_create(const pb_problem_desc* desc, pb_problem** out) {
   int rc = make_grid(&desc->grid, pr->grid);
   if (rc) { delete pr; return rc; }
   pr->n = pr->grid.n; pr->p = pr->grid.p; pr->k = desc->num_atoms;
-  const int64_t m = pr->grid.m, n = pr->n, p = pr->p, k = pr->k;
+  pr->ld = pb_code_pitch(pr->n);
+  const int64_t m = pr->grid.m, n = pr->n, p = pr->p, k = pr->k, ld = pr->ld;
 #define PB_A(ptr, cnt) if ((rc = dalloc(&pr->ptr, (size_t)(cnt)))) { pb_problem_destroy(pr); return rc; }
   PB_A(frame, m) PB_A(mask, m) PB_A(values, p * n) PB_A(obs, p * n) PB_A(means, n) PB_A(counts, n)
-  PB_A(atoms, k * p) PB_A(pi, k) PB_A(usage, k * n) PB_A(weights, k * n) PB_A(est, p * n) PB_A(recon, m)
+  PB_A(atoms, k * p) PB_A(pi, k) PB_A(usage, k * ld) PB_A(weights, k * ld) PB_A(est, p * n) PB_A(recon, m)
   PB_A(m_count, k) PB_A(scalars, 1) PB_A(nobs_dev, 1)
 #undef PB_A
   if (cudaStreamCreateWithFlags(&pr->stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -453,10 +499,10 @@ int pb_problem_submit_frame(pb_problem* pr, const double* frame_host, const uint
   if (!pr->have_state || !pr->desc.warm_start) {
     if ((rc = problem_cold_init(pr))) return rc;
   }
-  PB_CUDA_TRY(cudaMemsetAsync(pr->usage, 0, (size_t)pr->k * n, st));
-  PB_CUDA_TRY(cudaMemsetAsync(pr->weights, 0, (size_t)pr->k * n * sizeof(float), st));
+  PB_CUDA_TRY(cudaMemsetAsync(pr->usage, 0, (size_t)pr->k * pr->ld, st));
+  PB_CUDA_TRY(cudaMemsetAsync(pr->weights, 0, (size_t)pr->k * pr->ld * sizeof(float), st));
   pb_epoch_desc d{};
-  d.n = n; d.p = pr->p; d.k = pr->k;
+  d.n = n; d.ld = pr->ld; d.p = pr->p; d.k = pr->k;
   d.freeze_dict = pr->desc.freeze_dict;
   d.rng_mode = PB_RNG_PHILOX;
   d.seed = pr->desc.seed;
@@ -468,10 +514,11 @@ int pb_problem_submit_frame(pb_problem* pr, const double* frame_host, const uint
   const int epochs = pr->desc.epochs_per_frame;
   int tail = pr->desc.average_last < 1 ? 1 : (pr->desc.average_last > epochs ? epochs : pr->desc.average_last);
   for (int e = 0; e < epochs; ++e) {
+    d.resid_mode = e == 0 ? PB_RESID_FROM_VALUES : PB_RESID_CARRY;  // codes were just reset
     if ((rc = run_epoch(&d, pr->m_count, st))) return rc;
     if (e >= epochs - tail) {
       rc = launch_accumulate_atoms(false, nullptr, nullptr, pr->usage, pr->weights, pr->atoms, pr->est, n, pr->p,
-                                   pr->k, e > epochs - tail ? 1 : 0, st);
+                                   pr->k, e > epochs - tail ? 1 : 0, pr->ld, st);
       if (rc) return rc;
     }
   }

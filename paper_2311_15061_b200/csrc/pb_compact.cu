@@ -45,6 +45,14 @@ __device__ __forceinline__ float gsum(float v) {
 }
 
 // ---------------------------------------------------------------------------
+// Slot bookkeeping shared by the per-patch kernels: lane g of a G-lane group
+// holds slots j*G + g of its patch; `wmax` is the warp-uniform number of slots
+// any lane needs, so padded slots past it are skipped with uniform branches.
+template <int G>
+__device__ __forceinline__ int lane_slots(int cnt, int g) {
+  return cnt > g ? (cnt - g + G - 1) / G : 0;
+}
+
 template <int CMAX, int G>
 __global__ void __launch_bounds__(256) k_resid_compact(CompactArgs a) {
   extern __shared__ float ds[];
@@ -54,42 +62,66 @@ __global__ void __launch_bounds__(256) k_resid_compact(CompactArgs a) {
   const bool live = i < a.n;
   float acc[CMAX];
   int off[CMAX];
-  uint32_t pos[CMAX];
   int cnt = 0;
   int64_t r0 = 0;
   if (live) { cnt = a.counts[i]; r0 = a.rowptr[i]; }
+  const int wmax = __reduce_max_sync(0xffffffffu, lane_slots<G>(cnt, g));
 #pragma unroll
   for (int j = 0; j < CMAX; ++j) {
-    const int s = j * G + g;
-    const bool v = s < cnt;
-    off[j] = v ? a.csr_p[r0 + s] : a.p;
-    pos[j] = v ? a.csr_pos[r0 + s] : 0u;
-    acc[j] = v ? a.x_csc[pos[j]] : 0.0f;
+    off[j] = a.p;
+    acc[j] = 0.0f;
+    if (j < wmax) {
+      const int s = j * G + g;
+      if (s < cnt) {
+        off[j] = a.csr_p[r0 + s];
+        acc[j] = a.x_csc[a.csr_pos[r0 + s]];
+      }
+    }
   }
+  const int64_t ic = live ? i : 0;
   for (int k0 = 0; k0 < a.k; k0 += a.kc) {
     const int kn = min(a.kc, a.k - k0);
     __syncthreads();
     stage_atoms(ds, a.atoms, k0, kn, a.p, pp);
     __syncthreads();
-    if (!live) continue;
-    for (int kk = 0; kk < kn; ++kk) {
-      const int64_t zi = (int64_t)(k0 + kk) * a.n + i;
-      if (!a.usage[zi]) continue;
-      const float w = a.weights[zi];
-      const float* d = ds + kk * pp;
+    for (int kb = 0; kb < kn; kb += 8) {
+      // batch the (independent) code loads of 8 atoms before using any
+      float wv[8];
 #pragma unroll
-      for (int j = 0; j < CMAX; ++j) acc[j] = fmaf(-w, d[off[j]], acc[j]);
+      for (int q = 0; q < 8; ++q) {
+        const int64_t zi = (int64_t)(k0 + min(kb + q, kn - 1)) * a.ld + ic;
+        const uint8_t z = a.usage[zi];
+        const float w = a.weights[zi];
+        wv[q] = (live && kb + q < kn && z) ? -w : 0.0f;
+      }
+      if (a.wt && live && g == 0) {  // tile-blocked copy of w for the dictionary step
+        float4* dst = (float4*)(a.wt + (((i / kTile) * a.nblk8 + ((k0 + kb) >> 3)) * kTile + (i % kTile)) * kWB);
+        dst[0] = make_float4(wv[0] != 0.f ? -wv[0] : 0.f, wv[1] != 0.f ? -wv[1] : 0.f,
+                             wv[2] != 0.f ? -wv[2] : 0.f, wv[3] != 0.f ? -wv[3] : 0.f);
+        dst[1] = make_float4(wv[4] != 0.f ? -wv[4] : 0.f, wv[5] != 0.f ? -wv[5] : 0.f,
+                             wv[6] != 0.f ? -wv[6] : 0.f, wv[7] != 0.f ? -wv[7] : 0.f);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (!__any_sync(0xffffffffu, wv[q] != 0.0f)) continue;
+        const float* d = ds + (kb + q) * pp;
+#pragma unroll
+        for (int j = 0; j < CMAX; ++j)
+          if (j < wmax) acc[j] = fmaf(wv[q], d[off[j]], acc[j]);
+      }
     }
   }
   if (!live) return;
 #pragma unroll
-  for (int j = 0; j < CMAX; ++j)
-    if (j * G + g < cnt) a.r_csc[pos[j]] = acc[j];
+  for (int j = 0; j < CMAX; ++j) {
+    const int s = j * G + g;
+    if (j < wmax && s < cnt) a.r_csc[a.csr_pos[r0 + s]] = acc[j];
+  }
 }
 
 // ---------------------------------------------------------------------------
 template <int CMAX, int G, int MODE>
-__global__ void __launch_bounds__(256) k_code_compact(CompactArgs a) {
+__global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
   extern __shared__ float sm[];
   const int pp = a.p + 1;
   float* logit = sm;                     // K
@@ -99,6 +131,7 @@ __global__ void __launch_bounds__(256) k_code_compact(CompactArgs a) {
   const int g = threadIdx.x % G;
   const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
   const bool live = i < a.n;
+  const int64_t ic = live ? i : 0;
   const int lane = threadIdx.x & 31;
   const int epoch = a.sc->epoch + 1;
   const float geps = (float)a.sc->gamma_eps, gs = (float)a.sc->gamma_s;
@@ -114,16 +147,28 @@ __global__ void __launch_bounds__(256) k_code_compact(CompactArgs a) {
   int cnt = 0;
   int64_t r0 = 0;
   if (live) { cnt = a.counts[i]; r0 = a.rowptr[i]; }
+  const int wmax = __reduce_max_sync(0xffffffffu, lane_slots<G>(cnt, g));
 #pragma unroll
   for (int j = 0; j < CMAX; ++j) {
-    const int s = j * G + g;
-    const bool v = s < cnt;
-    off[j] = v ? a.csr_p[r0 + s] : a.p;
-    r[j] = v ? a.r_csc[a.csr_pos[r0 + s]] : 0.0f;
+    off[j] = a.p;
+    r[j] = 0.0f;
+    if (j < wmax) {
+      const int s = j * G + g;
+      if (s < cnt) {
+        off[j] = a.csr_p[r0 + s];
+        r[j] = a.r_csc[a.csr_pos[r0 + s]];
+      }
+    }
   }
   double sq_w = 0.0;
+  float wr0 = 0.f, wr1 = 0.f, wr2 = 0.f, wr3 = 0.f, wr4 = 0.f, wr5 = 0.f, wr6 = 0.f, wr7 = 0.f;
   u32x4 rnd{0, 0, 0, 0};
   float nrm0 = 0.f, nrm1 = 0.f;
+  // 1-deep software prefetch of the next atom's code (z, s) and replay draws
+  uint8_t zn = a.usage[ic];
+  float sn = a.weights[ic];
+  double un = 0.0, gnx = 0.0;
+  if (MODE == kRngReplay) { un = a.u_draw[ic]; gnx = a.g_draw[ic]; }
   for (int k0 = 0; k0 < a.k; k0 += a.kc) {
     const int kn = min(a.kc, a.k - k0);
     __syncthreads();
@@ -132,13 +177,29 @@ __global__ void __launch_bounds__(256) k_code_compact(CompactArgs a) {
     for (int kk = 0; kk < kn; ++kk) {
       const int k = k0 + kk;
       const float* d = ds + kk * pp;
+      const bool z_old = zn != 0;
+      const float s_old = sn;
+      const double ud = un, gd = gnx;
+      if (k + 1 < a.k) {
+        const int64_t zn_i = (int64_t)(k + 1) * a.ld + ic;
+        zn = a.usage[zn_i];
+        sn = a.weights[zn_i];
+        if (MODE == kRngReplay) {
+          const int64_t dn_i = (int64_t)(k + 1) * a.n + ic;
+          un = a.u_draw[dn_i];
+          gnx = a.g_draw[dn_i];
+        }
+      }
       float dj[CMAX];
       float u = 0.0f, v = 0.0f;
 #pragma unroll
       for (int j = 0; j < CMAX; ++j) {
-        dj[j] = d[off[j]];
-        u = fmaf(dj[j], dj[j], u);
-        v = fmaf(dj[j], r[j], v);
+        dj[j] = 0.0f;
+        if (j < wmax) {
+          dj[j] = d[off[j]];
+          u = fmaf(dj[j], dj[j], u);
+          v = fmaf(dj[j], r[j], v);
+        }
       }
       if (G > 1) {
         u = gsum<G>(u);
@@ -146,20 +207,17 @@ __global__ void __launch_bounds__(256) k_code_compact(CompactArgs a) {
       }
       bool z = false;
       if (live) {
-        const int64_t zi = (int64_t)k * a.n + i;
-        const bool z_old = a.usage[zi] != 0;
-        const float s_old = a.weights[zi];
+        const int64_t zi = (int64_t)k * a.ld + i;
         const float w_old = z_old ? s_old : 0.0f;
         // _code_params (bpfa.py:169-178)
         const float proj = fmaf(w_old, u, v);
         const float log_rho = logit[k] - 0.5f * geps * (s_old * s_old * u - 2.0f * s_old * proj);
         const float alpha = fmaf(geps, u, gs);
-        const float mean = geps * proj / alpha;
-        float gn;
+        float s_new;
         if (MODE == kRngReplay) {
-          const double ud = a.u_draw[zi];
-          gn = (float)a.g_draw[zi];
           z = (log(ud) - log1p(-ud)) < (double)log_rho;  // bpfa.py:262-263
+          const float gn = (float)gd;
+          s_new = z ? geps * proj / alpha + gn / sqrtf(alpha) : gn * inv_sqrt_gs;  // bpfa.py:265-269
         } else {
           if ((k & 1) == 0) {
             rnd = philox4x32_10(u32x4{(uint32_t)i, (uint32_t)(i >> 32), (uint32_t)(k >> 1),
@@ -168,17 +226,30 @@ __global__ void __launch_bounds__(256) k_code_compact(CompactArgs a) {
             box_muller(rnd.z, rnd.w, nrm0, nrm1);
           }
           const float uu = u01_24((k & 1) ? rnd.y : rnd.x);
-          gn = (k & 1) ? nrm1 : nrm0;
+          const float gn = (k & 1) ? nrm1 : nrm0;
           z = uu * (1.0f + __expf(-log_rho)) < 1.0f;  // U < sigmoid(log_rho)
+          const float ra = rsqrtf(alpha);
+          s_new = z ? fmaf(geps * proj, ra * ra, gn * ra) : gn * inv_sqrt_gs;
         }
-        const float s_new = z ? mean + gn / sqrtf(alpha) : gn * inv_sqrt_gs;  // bpfa.py:265-269
-        const float dw = w_old - (z ? s_new : 0.0f);
+        const float w_new = z ? s_new : 0.0f;
+        const float dw = w_old - w_new;
 #pragma unroll
-        for (int j = 0; j < CMAX; ++j) r[j] = fmaf(dw, dj[j], r[j]);
+        for (int j = 0; j < CMAX; ++j)
+          if (j < wmax) r[j] = fmaf(dw, dj[j], r[j]);
         if (g == 0) {
           a.usage[zi] = z ? 1 : 0;
           a.weights[zi] = s_new;
           sq_w += (double)s_new * (double)s_new;
+        }
+        // rotating 8-atom window of w for the tile-blocked copy (dictionary step)
+        wr0 = wr1; wr1 = wr2; wr2 = wr3; wr3 = wr4; wr4 = wr5; wr5 = wr6; wr6 = wr7; wr7 = w_new;
+        if (g == 0 && ((k & 7) == 7 || k == a.k - 1)) {
+          for (int t = k & 7; t < 7; ++t) {  // left-align a partial last block
+            wr0 = wr1; wr1 = wr2; wr2 = wr3; wr3 = wr4; wr4 = wr5; wr5 = wr6; wr6 = wr7; wr7 = 0.0f;
+          }
+          float4* dst = (float4*)(a.wt + (((i / kTile) * a.nblk8 + (k >> 3)) * kTile + (i % kTile)) * kWB);
+          dst[0] = make_float4(wr0, wr1, wr2, wr3);
+          dst[1] = make_float4(wr4, wr5, wr6, wr7);
         }
       }
       const unsigned bal = __ballot_sync(0xffffffffu, z && g == 0);
@@ -187,7 +258,12 @@ __global__ void __launch_bounds__(256) k_code_compact(CompactArgs a) {
   }
   double sq_r = 0.0;
 #pragma unroll
-  for (int j = 0; j < CMAX; ++j) sq_r += (double)r[j] * (double)r[j];
+  for (int j = 0; j < CMAX; ++j) {
+    sq_r += (double)r[j] * (double)r[j];
+    // the end-of-sweep residual is the next epoch's starting residual (carry mode)
+    const int s = j * G + g;
+    if (live && j < wmax && s < cnt) a.r_csc[a.csr_pos[r0 + s]] = r[j];
+  }
   const double bw = block_sum_d(sq_w, red);
   __syncthreads();
   const double br = block_sum_d(sq_r, red);
@@ -255,138 +331,276 @@ struct GramLayout {
   __device__ static constexpr int gidx(int j, int l) { return B + j * (j + 1) / 2 + l; }
 };
 
+// --- mbarrier + 1-D bulk async copy (TMA engine) helpers --------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// global -> shared bulk copy completing on an mbarrier (size and addresses 16-byte aligned)
+__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Dictionary step, persistent & cooperative (all CTAs co-resident).
+//
+// Work split (exactly balanced for any mask structure, deterministic):
+//   CTA c owns the element range [nnz*c/G, nnz*(c+1)/G) of the CSC-tile order;
+//   per tile it stages w = z*s of the previous and current atom blocks, then
+//   warp w of the CTA owns an equal contiguous slice of the tile's elements.
+//   A warp walks the columns its slice touches; lanes take every 32nd element
+//   of each column segment (coalesced), accumulate the NACC Gram/moment sums in
+//   registers, and transpose-reduce them at the end of the segment.  Segments
+//   wholly owned by one warp add straight into the CTA accumulator; the (at
+//   most two) boundary segments go to per-warp slots merged in warp order.
 template <int B>
-__global__ void __launch_bounds__(256) k_dict_gram(DictGramArgs a) {
+__global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
   using L = GramLayout<B>;
+  constexpr int NW = 16;
   extern __shared__ __align__(16) unsigned char smraw[];
   const int p = a.p;
-  // shared layout
-  float* wcur = (float*)smraw;                         // kTile * B   (aliased by red64 in the update phase)
-  float* wprev = wcur + kTile * B;                     // kTile * B
-  float* acc = (float*)(smraw + a.wbytes);             // p * NACC
-  float* dold = acc + (size_t)p * L::NACC;             // B * p
-  float* dprev = dold + B * p;                         // B * p   (delta of the previous block)
-  double* red64 = (double*)smraw;                      // p * NACC (aliases wcur/wprev)
+  static_assert(B == kWB, "the tile-blocked code copy W holds blocks of kWB atoms");
+  // [stage][cur|prev][kTile*B] staging of the tile-blocked code copy (async bulk copies),
+  // aliased by red64 in the update phase
+  float* wbuf = (float*)smraw;
+  float* acc = (float*)(smraw + a.wbytes);               // p * NACC
+  float* slots = acc + (size_t)p * L::NACC;              // NW * 2 * NACC
+  int* slot_col = (int*)(slots + NW * 2 * L::NACC);      // NW * 2
+  int* cps = slot_col + NW * 2;                          // 2 * (p + 1) (double-buffered tile colptr)
+  const int cpp = (p + 1 + 3) & ~3;
+  float* dold = (float*)(cps + 2 * cpp);                 // B * p
+  float* dprev = dold + B * p;                           // B * p
+  double* red64 = (double*)smraw;                        // p * NACC (aliases the staging)
+  __shared__ __align__(8) uint64_t mbar[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+  }
+  __syncthreads();
+  uint32_t phase_bits = 0;   // parity of each stage's mbarrier
+  uint32_t seq = 0;          // running tile-visit counter -> stage = seq & 1
 
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const double geps = a.sc->gamma_eps;
   const int epoch = a.sc->epoch + 1;
   const int nblk = (a.k + B - 1) / B;
-
-  // element-balanced static tile range of this CTA
   const int64_t nnz = a.tile_base[a.ntiles];
   const int64_t e_lo = nnz * blockIdx.x / gridDim.x, e_hi = nnz * (blockIdx.x + 1) / gridDim.x;
-  auto first_tile = [&](int64_t e) {  // first tile whose start >= e
-    int lo = 0, hi = a.ntiles;
+  // tiles overlapping [e_lo, e_hi): t_lo = last tile starting <= e_lo
+  int t_lo = 0, t_hi = 0;
+  {
+    int lo = 0, hi = a.ntiles - 1;
     while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (a.tile_base[mid] < e) lo = mid + 1; else hi = mid;
+      const int mid = (lo + hi + 1) >> 1;
+      if (a.tile_base[mid] <= e_lo) lo = mid; else hi = mid - 1;
     }
-    return lo;
+    t_lo = lo;
+    t_hi = t_lo;
+    while (t_hi < a.ntiles && a.tile_base[t_hi] < e_hi) ++t_hi;
+    if (e_hi <= e_lo) t_hi = t_lo;
+  }
+  uint64_t t_mark = a.prof ? gtimer() : 0;
+  auto prof = [&](int slot) {
+    if (a.prof && threadIdx.x == 0) {
+      const uint64_t now = gtimer();
+      a.prof[blockIdx.x * 8 + slot] += now - t_mark;
+      t_mark = now;
+    }
   };
-  const int t_lo = blockIdx.x == 0 ? 0 : first_tile(e_lo);
-  const int t_hi = blockIdx.x == gridDim.x - 1 ? a.ntiles : first_tile(e_hi);
 
   for (int blk = 0; blk <= nblk; ++blk) {
     const bool has_cur = blk < nblk, has_prev = blk > 0;
     const int k0 = blk * B;
     const int nb = has_cur ? min(B, a.k - k0) : 0;
     const int kp0 = k0 - B;
+    const int nbp = has_prev ? min(B, a.k - kp0) : 0;
     for (int t = threadIdx.x; t < p * L::NACC; t += blockDim.x) acc[t] = 0.0f;
     for (int t = threadIdx.x; t < B * p; t += blockDim.x) {
       const int j = t / p, pe = t - j * p;
       dold[t] = j < nb ? a.atoms[(int64_t)(k0 + j) * p + pe] : 0.0f;
     }
-    for (int tile = t_lo; tile < t_hi; ++tile) {
-      const int64_t ibase = (int64_t)tile * kTile;
-      const int tn = (int)min((int64_t)kTile, a.n - ibase);
-      __syncthreads();
-      for (int t = threadIdx.x; t < B * kTile; t += blockDim.x) {
-        const int j = t / kTile, il = t - j * kTile;
-        float wc = 0.0f, wp = 0.0f;
-        if (il < tn) {
-          if (j < nb) {
-            const int64_t zi = (int64_t)(k0 + j) * a.n + ibase + il;
-            wc = a.usage[zi] ? a.weights[zi] : 0.0f;
-          }
-          if (has_prev) {
-            const int64_t zi = (int64_t)(kp0 + j) * a.n + ibase + il;
-            wp = a.usage[zi] ? a.weights[zi] : 0.0f;
-          }
-        }
-        wcur[il * B + j] = wc;
-        wprev[il * B + j] = wp;
+    // async staging: bulk-copy the tile's W blocks (current, previous) into a stage
+    auto issue = [&](int tile, uint32_t stage) {
+      fence_proxy_async();
+      const uint32_t bytes = (has_cur ? kTile * B * 4u : 0u) + (has_prev ? kTile * B * 4u : 0u);
+      mbar_expect_tx(&mbar[stage], bytes);
+      float* dst = wbuf + (size_t)stage * 2 * kTile * B;
+      if (has_cur) bulk_copy_g2s(dst, a.wt + ((int64_t)tile * a.nblk8 + blk) * kTile * B, kTile * B * 4u, &mbar[stage]);
+      if (has_prev)
+        bulk_copy_g2s(dst + kTile * B, a.wt + ((int64_t)tile * a.nblk8 + blk - 1) * kTile * B, kTile * B * 4u,
+                      &mbar[stage]);
+    };
+    auto load_cps = [&](int tile, uint32_t stage) {
+      const int64_t tb0 = a.tile_base[tile];
+      for (int t = threadIdx.x; t <= p; t += blockDim.x)
+        cps[stage * cpp + t] = (int)(a.colptr[(int64_t)tile * (p + 1) + t] - tb0);
+    };
+    __syncthreads();
+    if (t_lo < t_hi) {
+      if (threadIdx.x == 0) issue(t_lo, seq & 1);
+      load_cps(t_lo, seq & 1);
+    }
+    for (int tile = t_lo; tile < t_hi; ++tile, ++seq) {
+      prof(7);
+      const uint32_t st = seq & 1;
+      __syncthreads();   // previous tile fully consumed: its stage and cps buffer are free
+      if (tile + 1 < t_hi) {
+        if (threadIdx.x == 0) issue(tile + 1, st ^ 1);
+        load_cps(tile + 1, st ^ 1);
       }
-      __syncthreads();
-      const int32_t* cp = a.colptr + (int64_t)tile * (p + 1);
-      for (int pe = wid; pe < p; pe += nw) {
-        const int cs = cp[pe], ce = cp[pe + 1];
-        if (ce == cs) continue;
-        float dl[B];
+      if (lane == 0) { slot_col[wid * 2] = -1; slot_col[wid * 2 + 1] = -1; }
+      const int64_t tb = a.tile_base[tile];
+      const int64_t rs = max(tb, e_lo), re = min(a.tile_base[tile + 1], e_hi);
+      const float* wcur = wbuf + (size_t)st * 2 * kTile * B;
+      const float* wprev = wcur + kTile * B;
+      const int* cpt = cps + st * cpp;
+      mbar_wait(&mbar[st], (phase_bits >> st) & 1u);
+      phase_bits ^= 1u << st;
+      prof(0);
+      const int m = (int)(re - rs);
+      const int ws = (int)(rs - tb) + (int)((int64_t)m * wid / NW), we = (int)(rs - tb) + (int)((int64_t)m * (wid + 1) / NW);
+      if (ws < we) {
+        // first / last column touched by this warp's slice (binary search, shared colptr)
+        int c_first = 0, c_last = 0;
+        {
+          int lo = 0, hi = p - 1;
+          while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (cpt[mid] <= ws) lo = mid; else hi = mid - 1; }
+          c_first = lo;
+          lo = c_first; hi = p - 1;
+          while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (cpt[mid] <= we - 1) lo = mid; else hi = mid - 1; }
+          c_last = lo;
+        }
+        const int64_t ebase = tb;
+        for (int c = c_first; c <= c_last; ++c) {
+          const int cs = max(ws, cpt[c]), ce = min(we, cpt[c + 1]);
+          if (cs >= ce) continue;
+          float dl[B];
 #pragma unroll
-        for (int j = 0; j < B; ++j) dl[j] = has_prev ? dprev[j * p + pe] : 0.0f;
-        float v[L::NP];
+          for (int j = 0; j < B; ++j) dl[j] = has_prev ? dprev[j * p + c] : 0.0f;
+          float v[L::NP];
 #pragma unroll
-        for (int q = 0; q < L::NP; ++q) v[q] = 0.0f;
-        for (int e = cs + lane; e < ce; e += 32) {
-          const int il = a.e_loc[e];
-          float r = a.r_csc[e];
-          if (has_prev) {
-            const float4* wp4 = (const float4*)(wprev + il * B);
+          for (int q = 0; q < L::NP; ++q) v[q] = 0.0f;
+          // software pipeline: the next 128 elements' loads are in flight while
+          // the current 128 are processed
+          int ilq[4], iln[4];
+          float rq[4], rn[4];
 #pragma unroll
-            for (int q = 0; q < B / 4; ++q) {
-              const float4 w4 = wp4[q];
-              r = fmaf(w4.x, dl[4 * q + 0], r);
-              r = fmaf(w4.y, dl[4 * q + 1], r);
-              r = fmaf(w4.z, dl[4 * q + 2], r);
-              r = fmaf(w4.w, dl[4 * q + 3], r);
+          for (int q = 0; q < 4; ++q) {
+            const int e = cs + q * 32 + lane;
+            iln[q] = e < ce ? (int)a.e_loc[ebase + e] : -1;
+            rn[q] = e < ce ? a.r_csc[ebase + e] : 0.0f;
+          }
+          for (int eb = cs; eb < ce; eb += 128) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              ilq[q] = iln[q];
+              rq[q] = rn[q];
+              const int e = eb + 128 + q * 32 + lane;
+              iln[q] = e < ce ? (int)a.e_loc[ebase + e] : -1;
+              rn[q] = e < ce ? a.r_csc[ebase + e] : 0.0f;
             }
-            a.r_csc[e] = r;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (ilq[q] < 0) continue;
+              const int il = ilq[q];
+              float r = rq[q];
+              if (has_prev) {
+                const float4* wp4 = (const float4*)(wprev + il * B);
+#pragma unroll
+                for (int h = 0; h < B / 4; ++h) {
+                  const float4 w4 = wp4[h];
+                  r = fmaf(w4.x, dl[4 * h + 0], r);
+                  r = fmaf(w4.y, dl[4 * h + 1], r);
+                  r = fmaf(w4.z, dl[4 * h + 2], r);
+                  r = fmaf(w4.w, dl[4 * h + 3], r);
+                }
+                a.r_csc[ebase + eb + q * 32 + lane] = r;
+              }
+              if (has_cur) {
+                float wc[B];
+                const float4* wc4 = (const float4*)(wcur + il * B);
+#pragma unroll
+                for (int h = 0; h < B / 4; ++h) {
+                  const float4 w4 = wc4[h];
+                  wc[4 * h + 0] = w4.x; wc[4 * h + 1] = w4.y; wc[4 * h + 2] = w4.z; wc[4 * h + 3] = w4.w;
+                }
+#pragma unroll
+                for (int j = 0; j < B; ++j) {
+                  v[j] = fmaf(wc[j], r, v[j]);
+#pragma unroll
+                  for (int l = 0; l <= j; ++l) v[L::gidx(j, l)] = fmaf(wc[j], wc[l], v[L::gidx(j, l)]);
+                }
+              }
+            }
           }
           if (has_cur) {
-            float wc[B];
-            const float4* wc4 = (const float4*)(wcur + il * B);
+            warp_transpose_reduce<L::NP>(v, lane);
+            const bool exclusive = cpt[c] >= ws && cpt[c + 1] <= we;
+            const int slot = c == c_first ? 0 : 1;
+            if ((lane & 1) == 0) {
+              constexpr int R = L::NP / 16;
+              const int base = R * (((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
+                                    ((lane >> 1) & 1));
 #pragma unroll
-            for (int q = 0; q < B / 4; ++q) {
-              const float4 w4 = wc4[q];
-              wc[4 * q + 0] = w4.x; wc[4 * q + 1] = w4.y; wc[4 * q + 2] = w4.z; wc[4 * q + 3] = w4.w;
+              for (int q = 0; q < R; ++q) {
+                if (base + q < L::NACC) {
+                  if (exclusive) acc[c * L::NACC + base + q] += v[q];
+                  else slots[(wid * 2 + slot) * L::NACC + base + q] = v[q];
+                }
+              }
             }
-#pragma unroll
-            for (int j = 0; j < B; ++j) {
-              v[j] = fmaf(wc[j], r, v[j]);
-#pragma unroll
-              for (int l = 0; l <= j; ++l) v[L::gidx(j, l)] = fmaf(wc[j], wc[l], v[L::gidx(j, l)]);
-            }
+            if (!exclusive && lane == 0) slot_col[wid * 2 + slot] = c;
           }
         }
-        if (has_cur) {
-          warp_transpose_reduce<L::NP>(v, lane);
-          if ((lane & 1) == 0) {
-            constexpr int R = L::NP / 16;
-            const int base = R * (((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
-                                  ((lane >> 1) & 1));
-#pragma unroll
-            for (int q = 0; q < R; ++q)
-              if (base + q < L::NACC) acc[pe * L::NACC + base + q] += v[q];
-          }
+      }
+      __syncthreads();
+      // merge the boundary segments in warp order (deterministic)
+      if (has_cur && threadIdx.x < L::NACC) {
+        for (int s2 = 0; s2 < NW * 2; ++s2) {
+          const int c = slot_col[s2];
+          if (c >= 0) acc[c * L::NACC + threadIdx.x] += slots[s2 * L::NACC + threadIdx.x];
         }
       }
     }
+    prof(1);
     if (!has_cur) break;
     __syncthreads();
     float* mine = a.partials + (size_t)blockIdx.x * p * L::NACC;
     for (int t = threadIdx.x; t < p * L::NACC; t += blockDim.x) mine[t] = acc[t];
     __threadfence();
+    prof(2);
     grid_sync(a.bar);
-    // distributed fixed-order reduction across CTAs
+    prof(3);
+    // cross-CTA reduction, one warp per value, fixed order (lane-strided, then a fixed shuffle tree)
     const int nv = p * L::NACC;
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nv; t += gridDim.x * blockDim.x) {
+    const int gw = blockIdx.x * NW + wid, nwarps = gridDim.x * NW;
+    for (int t = gw; t < nv; t += nwarps) {
       double s = 0.0;
-      for (int b = 0; b < (int)gridDim.x; ++b) s += (double)__ldcg(a.partials + (size_t)b * nv + t);
-      a.reduced[t] = s;
+      for (int b = lane; b < (int)gridDim.x; b += 32) s += (double)__ldcg(a.partials + (size_t)b * nv + t);
+      s = warp_sum_d(s);
+      if (lane == 0) a.reduced[t] = s;
     }
     __threadfence();
+    prof(4);
     grid_sync(a.bar);
+    prof(5);
     for (int t = threadIdx.x; t < nv; t += blockDim.x) red64[t] = __ldcg(a.reduced + t);
     __syncthreads();
     // sequential atom updates inside the block, identical in every CTA
@@ -420,6 +634,7 @@ __global__ void __launch_bounds__(256) k_dict_gram(DictGramArgs a) {
       for (int j = nb; j < B; ++j) dprev[j * p + pe] = 0.0f;
     }
     __syncthreads();
+    prof(6);
   }
 }
 
@@ -460,10 +675,10 @@ int launch_resid_compact(const CompactArgs& a_in, cudaStream_t st) {
   if (!pick_compact(a.cmax, c, g)) { set_error("patch has too many observed elements (%d)", a.cmax); return PB_EUNSUPPORTED; }
   normalize_cg(c, g);
   const int th = 256;
-  a.kc = (int)((64 * 1024) / ((size_t)(a.p + 1) * 4));
-  if (a.kc < 1) a.kc = 1;
+  a.kc = (int)((64 * 1024) / ((size_t)(a.p + 1) * 4)) & ~7;  // multiple of 8: W blocks align
+  if (a.kc < 8) a.kc = 8;
   if (a.kc > a.k) a.kc = a.k;
-  const size_t smem = (size_t)a.kc * (a.p + 1) * 4;
+  const size_t smem = (size_t)std::max(a.kc, 8) * (a.p + 1) * 4;
   const unsigned nb = (unsigned)ceil_div(a.n * g, th);
 #define PB_R(C, GG)                                                                                 \
   case C * 100 + GG: {                                                                              \
@@ -507,10 +722,12 @@ int launch_code_compact(const CompactArgs& a_in, int mode, int& nblocks, cudaStr
 template <int B>
 static int launch_dict_gram_b(DictGramArgs a, cudaStream_t st) {
   using L = GramLayout<B>;
-  const int th = 256;
-  const size_t wbytes = std::max((size_t)2 * kTile * B * 4, (size_t)a.p * L::NACC * 8);
+  const int th = 512;
+  if (a.ld % 4) { set_error("usage/weights row pitch must be a multiple of 4 (got %lld)", (long long)a.ld); return PB_EVALUE; }
+  const size_t wbytes = std::max((size_t)2 * 2 * kTile * B * 4, (size_t)a.p * L::NACC * 8);
   a.wbytes = (int)wbytes;
-  const size_t smem = wbytes + (size_t)a.p * L::NACC * 4 + (size_t)2 * B * a.p * 4;
+  const size_t smem = wbytes + (size_t)a.p * L::NACC * 4 + (size_t)16 * 2 * L::NACC * 4 + 16 * 2 * 4 +
+                      (size_t)2 * ((a.p + 1 + 3) & ~3) * 4 + (size_t)2 * B * a.p * 4;
   if (smem > 225 * 1024) { set_error("patch size %d too large for the dictionary step", a.p); return PB_EUNSUPPORTED; }
   PB_CUDA_TRY(cudaFuncSetAttribute(k_dict_gram<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;

@@ -16,6 +16,9 @@ struct CompactArgs {
   const float* x_csc;
   float* r_csc;
   int cmax;
+  // tile-blocked copy of w = z*s for the dictionary step: [tile][k/8][patch-in-tile][k%8]
+  float* wt;
+  int nblk8;
   // state
   uint8_t* usage;
   float* weights;
@@ -29,6 +32,7 @@ struct CompactArgs {
   double* block_sums;
   int32_t* m_count;
   int64_t n;
+  int64_t ld;           // row pitch of usage/weights (K, ld), ld >= n
   int p, k, kc;
   uint32_t key0, key1;
 };
@@ -39,6 +43,8 @@ struct DictGramArgs {
   const int32_t* colptr;
   const uint16_t* e_loc;
   int ntiles;
+  const float* wt;      // tile-blocked code copy [tile][k/8][patch][8]
+  int nblk8;
   float* r_csc;
   // state
   const uint8_t* usage;
@@ -50,9 +56,11 @@ struct DictGramArgs {
   float* partials;      // max_blocks * P * NACC
   double* reduced;      // P * NACC
   unsigned* bar;        // 2
+  unsigned long long* prof;  // optional [gridDim][8] phase nanoseconds (profiling)
   int max_blocks;
   int wbytes;
   int64_t n;
+  int64_t ld;           // row pitch of usage/weights (K, ld), ld >= n
   int p, k;
   uint32_t key0, key1;
 };

@@ -85,7 +85,7 @@ __global__ void k_tile_scan(const int32_t* __restrict__ tile_tot, int ntiles, in
   if (threadIdx.x == 0) tile_base[ntiles] = carry;
 }
 
-// Block-wide exclusive scan of small ints (blockDim.x == kTile == 1024).
+// Block-wide exclusive scan of small ints (blockDim.x a multiple of 32, <= 1024).
 __device__ __forceinline__ int block_excl_scan(int v, int* wsum, int& total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int x = v;
@@ -98,7 +98,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* wsum, int& total) {
   if (lane == 31) wsum[w] = x;
   __syncthreads();
   if (w == 0) {
-    const int s = wsum[lane];
+    const int s = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
     int z = s;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -113,40 +113,55 @@ __device__ __forceinline__ int block_excl_scan(int v, int* wsum, int& total) {
   return wsum[w] + x - v;
 }
 
-__global__ void __launch_bounds__(kTile) k_tile_fill(const uint8_t* __restrict__ obs, const float* __restrict__ values,
-                                                      const int32_t* __restrict__ counts, int64_t n, int p,
-                                                      const int64_t* __restrict__ tile_base,
-                                                      int32_t* __restrict__ colptr, uint16_t* __restrict__ e_loc,
-                                                      float* __restrict__ x_csc, int64_t* __restrict__ rowptr,
-                                                      uint16_t* __restrict__ csr_p, uint32_t* __restrict__ csr_pos) {
+// One block of kFillThreads threads per tile; thread t owns the adjacent local
+// patches 2t and 2t+1, so a block-wide exclusive scan of per-thread pair sums
+// keeps every column in ascending patch order.
+__global__ void __launch_bounds__(kFillThreads) k_tile_fill(
+    const uint8_t* __restrict__ obs, const float* __restrict__ values, const int32_t* __restrict__ counts, int64_t n,
+    int p, const int64_t* __restrict__ tile_base, int32_t* __restrict__ colptr, uint16_t* __restrict__ e_loc,
+    float* __restrict__ x_csc, int64_t* __restrict__ rowptr, uint16_t* __restrict__ csr_p,
+    uint32_t* __restrict__ csr_pos) {
+  static_assert(kTile == 2 * kFillThreads, "two patches per fill thread");
   __shared__ int wsum[33];
   const int t = blockIdx.x;
-  const int li = threadIdx.x;
-  const int64_t gi = (int64_t)t * kTile + li;
-  const bool live = gi < n;
+  const int l0 = 2 * threadIdx.x;
+  const int64_t g0 = (int64_t)t * kTile + l0, g1 = g0 + 1;
+  const bool live0 = g0 < n, live1 = g1 < n;
   const int64_t tb = tile_base[t];
   int tot;
-  const int my_cnt = live ? counts[gi] : 0;
-  const int64_t my_row = tb + block_excl_scan(my_cnt, wsum, tot);
-  if (live) rowptr[gi] = my_row;
-  if (gi == n - 1) rowptr[n] = my_row + my_cnt;
+  const int c0 = live0 ? counts[g0] : 0, c1 = live1 ? counts[g1] : 0;
+  const int64_t row0 = tb + block_excl_scan(c0 + c1, wsum, tot);
+  const int64_t row1 = row0 + c0;
+  if (live0) rowptr[g0] = row0;
+  if (live1) rowptr[g1] = row1;
+  if (g0 == n - 1) rowptr[n] = row0 + c0;
+  if (g1 == n - 1) rowptr[n] = row1 + c1;
   int64_t col = tb;
-  int j = 0;
+  int j0 = 0, j1 = 0;
   for (int pe = 0; pe < p; ++pe) {
-    const int o = (live && obs[(int64_t)pe * n + gi]) ? 1 : 0;
-    const int rank = block_excl_scan(o, wsum, tot);
-    if (li == 0) colptr[(int64_t)t * (p + 1) + pe] = (int32_t)col;
-    if (o) {
+    const int o0 = (live0 && obs[(int64_t)pe * n + g0]) ? 1 : 0;
+    const int o1 = (live1 && obs[(int64_t)pe * n + g1]) ? 1 : 0;
+    const int rank = block_excl_scan(o0 + o1, wsum, tot);
+    if (threadIdx.x == 0) colptr[(int64_t)t * (p + 1) + pe] = (int32_t)col;
+    if (o0) {
       const int64_t pos = col + rank;
-      e_loc[pos] = (uint16_t)li;
-      x_csc[pos] = values[(int64_t)pe * n + gi];
-      csr_p[my_row + j] = (uint16_t)pe;
-      csr_pos[my_row + j] = (uint32_t)pos;
-      ++j;
+      e_loc[pos] = (uint16_t)l0;
+      x_csc[pos] = values[(int64_t)pe * n + g0];
+      csr_p[row0 + j0] = (uint16_t)pe;
+      csr_pos[row0 + j0] = (uint32_t)pos;
+      ++j0;
+    }
+    if (o1) {
+      const int64_t pos = col + rank + o0;
+      e_loc[pos] = (uint16_t)(l0 + 1);
+      x_csc[pos] = values[(int64_t)pe * n + g1];
+      csr_p[row1 + j1] = (uint16_t)pe;
+      csr_pos[row1 + j1] = (uint32_t)pos;
+      ++j1;
     }
     col += tot;
   }
-  if (li == 0) colptr[(int64_t)t * (p + 1) + p] = (int32_t)col;
+  if (threadIdx.x == 0) colptr[(int64_t)t * (p + 1) + p] = (int32_t)col;
 }
 
 // Refresh the CSC values for a new frame under a cached mask (live path).
@@ -198,7 +213,7 @@ int launch_build_index(PatchIndex& ix, const uint8_t* obs, const float* values, 
   PB_CUDA_TRY(cudaMemsetAsync(ix.cmax_dev, 0, 4, st));
   k_tile_totals<<<ix.ntiles, 256, 0, st>>>(counts, ix.n, ix.tile_tot, ix.cmax_dev);
   k_tile_scan<<<1, 1024, 0, st>>>(ix.tile_tot, ix.ntiles, ix.tile_base);
-  k_tile_fill<<<ix.ntiles, kTile, 0, st>>>(obs, values, counts, ix.n, ix.p, ix.tile_base, ix.colptr, ix.e_loc,
+  k_tile_fill<<<ix.ntiles, kFillThreads, 0, st>>>(obs, values, counts, ix.n, ix.p, ix.tile_base, ix.colptr, ix.e_loc,
                                            ix.x_csc, ix.rowptr, ix.csr_p, ix.csr_pos);
   PB_LAUNCH_CHECK();
   return PB_OK;

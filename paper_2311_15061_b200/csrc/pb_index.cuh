@@ -4,7 +4,9 @@
 
 namespace pb {
 
-constexpr int kTile = 1024;  // patches per CSC tile (one build block, one dict-step work unit)
+constexpr int kTile = 1024;        // patches per CSC tile (one dict-step work unit)
+constexpr int kFillThreads = 512;  // index-build block size (two patches per thread)
+constexpr int kWB = 8;             // atoms per block of the tile-blocked code copy W
 
 struct PatchIndex {
   int64_t n;

@@ -22,7 +22,7 @@ template <int VPT, int G, bool RESID>
 __global__ void __launch_bounds__(256) k_accumulate_atoms(
     const float* __restrict__ values, const uint8_t* __restrict__ obs, const uint8_t* __restrict__ usage,
     const float* __restrict__ weights, const float* __restrict__ atoms, float* __restrict__ out, int64_t n, int p,
-    int k_len, int kc, int accumulate) {
+    int k_len, int kc, int accumulate, int64_t ld) {
   extern __shared__ float ds[];  // kc * p
   const int g = threadIdx.x % G;
   const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(256) k_accumulate_atoms(
     __syncthreads();
     if (live) {
       for (int kk = 0; kk < kn; ++kk) {
-        const int64_t zi = (int64_t)(k0 + kk) * n + i;
+        const int64_t zi = (int64_t)(k0 + kk) * ld + i;
         if (!usage[zi]) continue;
         const float w = RESID ? -weights[zi] : weights[zi];
         const float* d = ds + kk * PP + g;
@@ -313,7 +313,8 @@ static int pick_kc(int k_len, int p, size_t budget) {
 
 int launch_accumulate_atoms(bool resid, const float* values, const uint8_t* obs, const uint8_t* usage,
                             const float* weights, const float* atoms, float* out, int64_t n, int p, int k_len,
-                            int accumulate, cudaStream_t st) {
+                            int accumulate, int64_t ld, cudaStream_t st) {
+  if (ld < n) ld = n;
   int vpt, g;
   if (!pick_layout(p, vpt, g)) { set_error("patch size %d exceeds 2048", p); return PB_EUNSUPPORTED; }
   const int th = 256;
@@ -324,7 +325,7 @@ int launch_accumulate_atoms(bool resid, const float* values, const uint8_t* obs,
   case V * 100 + GG: {                                                                                     \
     auto kern = resid ? k_accumulate_atoms<V, GG, true> : k_accumulate_atoms<V, GG, false>;                \
     PB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));       \
-    kern<<<(unsigned)nb, th, smem, st>>>(values, obs, usage, weights, atoms, out, n, p, k_len, kc, accumulate); \
+    kern<<<(unsigned)nb, th, smem, st>>>(values, obs, usage, weights, atoms, out, n, p, k_len, kc, accumulate, ld); \
     break;                                                                                                 \
   }
   PB_DISPATCH_VG(vpt, g, PB_ACC)

@@ -25,7 +25,7 @@ int launch_coverage(const Grid&, int32_t*, cudaStream_t);
 // pb_sweep.cu
 int launch_accumulate_atoms(bool resid, const float* values, const uint8_t* obs, const uint8_t* usage,
                             const float* weights, const float* atoms, float* out, int64_t n, int p, int k_len,
-                            int accumulate, cudaStream_t st);
+                            int accumulate, int64_t ld, cudaStream_t st);
 int launch_finish_stats(const double*, int, SweepScalars*, cudaStream_t);
 int launch_draw_pi_gamma(double*, const int32_t*, SweepScalars*, int, int64_t, int64_t, const double*, uint32_t,
                          uint32_t, cudaStream_t);

@@ -249,3 +249,27 @@ def test_synthetic_dictionary_recovery_beats_mean_fill(cuda_device):
     fill = np.where(cnt > 0, (np.where(observed, clean, 0).sum(1, keepdims=True) / np.maximum(cnt, 1)), 0)
     base = float(np.mean((np.broadcast_to(fill, clean.shape)[held] - clean[held]) ** 2))
     assert model < 0.1 * base, (model, base)
+
+
+def test_residual_carry_matches_recompute(cuda_device):
+    """Carrying the end-of-sweep residual into the next epoch (PB_RESID_CARRY)
+    equals recomputing residual_full each epoch (the reference's behaviour,
+    bpfa.py:297) up to f32 rounding drift; the R = X start of fresh codes is exact."""
+    from paper_2311_15061_b200 import inputs
+
+    img = inputs.synthetic_texture((48, 48), seed=2)
+    mask = inputs.make_mask(img.shape, 0.25, "uniform-random", 2)
+    hp = gb.Hyperparams(num_atoms=12)
+    pm = pp.extract_patches(img, mask, pp.PatchSpec((8, 8)), True)
+    a = gb.init_state(pm, hp, 5, "prior")
+    b = gb.init_state(pm, hp, 5, "prior")
+    for _ in range(4):
+        gb.gibbs_epoch(a, pm, hp, rng="philox", check=False)       # carry after the first epoch
+        b._resid_key = None
+        b._zero_key = None if b.epoch > 0 else b._zero_key
+        gb.gibbs_epoch(b, pm, hp, rng="philox", check=False)       # forced recompute
+    ha, hb = a.to_host(), b.to_host()
+    assert (ha["usage"] != hb["usage"]).sum() <= 2
+    ok = ~(ha["usage"] != hb["usage"]).any(axis=1)
+    assert np.abs(ha["weights"][ok] - hb["weights"][ok]).max() <= 1e-3
+    assert np.abs(ha["atoms"] - hb["atoms"]).max() <= 1e-4

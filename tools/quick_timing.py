@@ -24,12 +24,19 @@ for cid in [int(a) for a in sys.argv[1:]] or [1, 3, 2]:
     hp = gb.Hyperparams(num_atoms=c["k"])
     st, est = gb.infer(pm, hp, 1, 0, rng="philox")  # warm-up
     torch.cuda.synchronize()
+    import ctypes
+    from paper_2311_15061_b200 import _lib
+    lib = _lib.load()
+    lib.pb_phase_timing(1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     st, est = gb.infer(pm, hp, c["epochs"], 0, rng="philox")
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    ph = (ctypes.c_double * 4)(); ne = ctypes.c_int64()
+    lib.pb_phase_read(ph, ctypes.byref(ne)); lib.pb_phase_timing(0)
+    print("  phases ms/epoch [resid, dict, code, stats]:", [round(ph[i] / max(1, ne.value), 3) for i in range(4)])
     rec = pp.reconstitute(pm, est, dc_original=img, dc_mask=mask)
     from paper_2311_15061_b200.metrics import psnr
     upd = pm.num_patches * c["k"] * c["epochs"]
