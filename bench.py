@@ -120,13 +120,14 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.lines = []          # (monotonic time, csv line)
+        self.window = None       # (t0, t1) of the timed region
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "25"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True, bufsize=1)
             threading.Thread(target=self._read, daemon=True).start()
         except OSError:
             self.proc = None
@@ -134,7 +135,10 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
 
     def __exit__(self, *exc):
         if self.proc:
@@ -144,7 +148,14 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        if self.window:
+            t0, t1 = self.window
+            inside = [x for x in lines if t0 <= x[0] <= t1 + 0.03]
+            if not inside and lines:  # region shorter than the sampling period: nearest sample
+                inside = [min(lines, key=lambda x: abs(x[0] - 0.5 * (t0 + t1)))]
+            lines = inside
+        for _, ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 8:
                 continue
@@ -226,6 +237,7 @@ def run_gpu_arm(args):
     hp = gb.Hyperparams(num_atoms=CFG["k"])
     n, k, p = pm.num_patches, CFG["k"], pm.patch_size
     st = gb.init_state(pm, hp, CFG["seed"] + rank, "prior")
+    clk = ClockSampler(local).__enter__()
     for _ in range(args.warmup):
         gb.gibbs_epoch(st, pm, hp, rng="philox", check=False)
     torch.cuda.synchronize()
@@ -234,12 +246,15 @@ def run_gpu_arm(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier(world)
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            gb.gibbs_epoch(st, pm, hp, rng="philox", check=False)
-        e1.record(stream)
-        torch.cuda.synchronize()
+    t_start = time.monotonic()
+    e0.record(stream)
+    for _ in range(args.steps):
+        gb.gibbs_epoch(st, pm, hp, rng="philox", check=False)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk.mark(t_start, time.monotonic())
+    time.sleep(0.06)
+    clk.__exit__(None, None, None)
     barrier(world)
     ms = max_over_ranks(e0.elapsed_time(e1), world)
     phase = (ctypes.c_double * 4)()
@@ -251,7 +266,8 @@ def run_gpu_arm(args):
     value = world * n * k * args.steps / (ms * 1e-3)
 
     # --- roofline of the dominant kernel ------------------------------------
-    names = ["k_accumulate_atoms(residual)", "k_dict_step", "k_code_step", "k_finish_stats+k_draw_pi_gamma"]
+    names = ["k_resid_compact (residual / carry)", "k_dict_gram (dictionary step)", "k_code_compact (code step)",
+             "k_finish_stats+k_draw_pi_gamma"]
     per = [phase[i] / max(1, nph.value) for i in range(4)]
     dom = int(np.argmax(per))
     obs_per_patch = pm.n_obs / n

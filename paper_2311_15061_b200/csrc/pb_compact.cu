@@ -126,7 +126,8 @@ __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
   const int pp = a.p + 1;
   float* logit = sm;                     // K
   int* mcnt = (int*)(logit + a.k);       // K
-  float* ds = (float*)(mcnt + a.k);      // kc * pp
+  float* wwin = (float*)(mcnt + a.k);    // (blockDim / G) * 9
+  float* ds = wwin + (blockDim.x / G) * 9;  // kc * pp
   __shared__ double red[32];
   const int g = threadIdx.x % G;
   const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
@@ -161,7 +162,6 @@ __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
     }
   }
   double sq_w = 0.0;
-  float wr0 = 0.f, wr1 = 0.f, wr2 = 0.f, wr3 = 0.f, wr4 = 0.f, wr5 = 0.f, wr6 = 0.f, wr7 = 0.f;
   u32x4 rnd{0, 0, 0, 0};
   float nrm0 = 0.f, nrm1 = 0.f;
   // 1-deep software prefetch of the next atom's code (z, s) and replay draws
@@ -241,15 +241,17 @@ __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
           a.weights[zi] = s_new;
           sq_w += (double)s_new * (double)s_new;
         }
-        // rotating 8-atom window of w for the tile-blocked copy (dictionary step)
-        wr0 = wr1; wr1 = wr2; wr2 = wr3; wr3 = wr4; wr4 = wr5; wr5 = wr6; wr6 = wr7; wr7 = w_new;
-        if (g == 0 && ((k & 7) == 7 || k == a.k - 1)) {
-          for (int t = k & 7; t < 7; ++t) {  // left-align a partial last block
-            wr0 = wr1; wr1 = wr2; wr2 = wr3; wr3 = wr4; wr4 = wr5; wr5 = wr6; wr6 = wr7; wr7 = 0.0f;
+        // 8-atom window of w (shared memory, pitch 9: conflict-free) for the
+        // tile-blocked copy the dictionary step bulk-loads
+        if (g == 0) {
+          float* wrow = wwin + (threadIdx.x / G) * 9;
+          wrow[k & 7] = w_new;
+          if ((k & 7) == 7 || k == a.k - 1) {
+            for (int t = (k & 7) + 1; t < 8; ++t) wrow[t] = 0.0f;  // partial last block
+            float4* dst = (float4*)(a.wt + (((i / kTile) * a.nblk8 + (k >> 3)) * kTile + (i % kTile)) * kWB);
+            dst[0] = make_float4(wrow[0], wrow[1], wrow[2], wrow[3]);
+            dst[1] = make_float4(wrow[4], wrow[5], wrow[6], wrow[7]);
           }
-          float4* dst = (float4*)(a.wt + (((i / kTile) * a.nblk8 + (k >> 3)) * kTile + (i % kTile)) * kWB);
-          dst[0] = make_float4(wr0, wr1, wr2, wr3);
-          dst[1] = make_float4(wr4, wr5, wr6, wr7);
         }
       }
       const unsigned bal = __ballot_sync(0xffffffffu, z && g == 0);
@@ -701,7 +703,7 @@ int launch_code_compact(const CompactArgs& a_in, int mode, int& nblocks, cudaStr
   a.kc = (int)((100 * 1024) / ((size_t)(a.p + 1) * 4));
   if (a.kc < 1) a.kc = 1;
   if (a.kc > a.k) a.kc = a.k;
-  const size_t smem = (size_t)a.kc * (a.p + 1) * 4 + (size_t)a.k * 8;
+  const size_t smem = (size_t)a.kc * (a.p + 1) * 4 + (size_t)a.k * 8 + (size_t)(th / g) * 9 * 4;
   if (smem > 220 * 1024) { set_error("too many atoms for the code step (K=%d)", a.k); return PB_EUNSUPPORTED; }
   const unsigned nb = (unsigned)ceil_div(a.n * g, th);
   nblocks = (int)nb;
