@@ -120,6 +120,110 @@ __global__ void __launch_bounds__(256) k_resid_compact(CompactArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Code step.  Per-thread loop state kept in registers across the atom loop.
+struct CodeThread {
+  double sq_w;
+  u32x4 rnd;
+  float nrm0, nrm1;
+  float sn;
+  uint8_t zn;
+  double un, gnx;
+};
+
+struct CodeConst {
+  int64_t i, ic;
+  bool live;
+  int g, lane, epoch;
+  float geps, gs, inv_sqrt_gs;
+  const float* logit;
+  int* mcnt;
+  float* wwin;
+};
+
+// Atoms [k0, k0+kn) for one patch with W live register slots (slots >= W are
+// padding for the whole warp; padded slots inside W read the zero column).
+template <int CMAX, int W, int G, int MODE>
+__device__ __forceinline__ void code_atoms(const CompactArgs& a, const CodeConst& c, int k0, int kn, const float* ds,
+                                           int pp, float (&r)[CMAX], const int (&off)[CMAX], CodeThread& t) {
+  for (int kk = 0; kk < kn; ++kk) {
+    const int k = k0 + kk;
+    const float* d = ds + kk * pp;
+    const bool z_old = t.zn != 0;
+    const float s_old = t.sn;
+    const double ud = t.un, gd = t.gnx;
+    if (k + 1 < a.k) {  // 1-deep prefetch of the next atom's code and replay draws
+      const int64_t zn_i = (int64_t)(k + 1) * a.ld + c.ic;
+      t.zn = a.usage[zn_i];
+      t.sn = a.weights[zn_i];
+      if (MODE == kRngReplay) {
+        const int64_t dn_i = (int64_t)(k + 1) * a.n + c.ic;
+        t.un = a.u_draw[dn_i];
+        t.gnx = a.g_draw[dn_i];
+      }
+    }
+    float dj[W];
+    float u = 0.0f, v = 0.0f;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      dj[j] = d[off[j]];
+      u = fmaf(dj[j], dj[j], u);
+      v = fmaf(dj[j], r[j], v);
+    }
+    if (G > 1) {
+      u = gsum<G>(u);
+      v = gsum<G>(v);
+    }
+    bool z = false;
+    if (c.live) {
+      const int64_t zi = (int64_t)k * a.ld + c.i;
+      const float w_old = z_old ? s_old : 0.0f;
+      // _code_params (bpfa.py:169-178)
+      const float proj = fmaf(w_old, u, v);
+      const float log_rho = c.logit[k] - 0.5f * c.geps * (s_old * s_old * u - 2.0f * s_old * proj);
+      const float alpha = fmaf(c.geps, u, c.gs);
+      float s_new;
+      if (MODE == kRngReplay) {
+        z = (log(ud) - log1p(-ud)) < (double)log_rho;  // bpfa.py:262-263
+        const float gn = (float)gd;
+        s_new = z ? c.geps * proj / alpha + gn / sqrtf(alpha) : gn * c.inv_sqrt_gs;  // bpfa.py:265-269
+      } else {
+        if ((k & 1) == 0) {
+          t.rnd = philox4x32_10(u32x4{(uint32_t)c.i, (uint32_t)(c.i >> 32), (uint32_t)(k >> 1),
+                                      ((uint32_t)c.epoch & 0xFFFFFFu) | (kDomCode << 24)},
+                                a.key0, a.key1);
+          box_muller(t.rnd.z, t.rnd.w, t.nrm0, t.nrm1);
+        }
+        const float uu = u01_24((k & 1) ? t.rnd.y : t.rnd.x);
+        const float gn = (k & 1) ? t.nrm1 : t.nrm0;
+        z = uu * (1.0f + __expf(-log_rho)) < 1.0f;  // U < sigmoid(log_rho)
+        const float ra = rsqrtf(alpha);
+        s_new = z ? fmaf(c.geps * proj, ra * ra, gn * ra) : gn * c.inv_sqrt_gs;
+      }
+      const float w_new = z ? s_new : 0.0f;
+      const float dw = w_old - w_new;
+#pragma unroll
+      for (int j = 0; j < W; ++j) r[j] = fmaf(dw, dj[j], r[j]);
+      if (c.g == 0) {
+        a.usage[zi] = z ? 1 : 0;
+        a.weights[zi] = s_new;
+        t.sq_w += (double)s_new * (double)s_new;
+        // 8-atom window of w (shared memory, pitch 9: conflict-free) for the
+        // tile-blocked copy the dictionary step bulk-loads
+        float* wrow = c.wwin + (threadIdx.x / G) * 9;
+        wrow[k & 7] = w_new;
+        if ((k & 7) == 7 || k == a.k - 1) {
+          for (int q = (k & 7) + 1; q < 8; ++q) wrow[q] = 0.0f;  // partial last block
+          float4* dst = (float4*)(a.wt + (((c.i / kTile) * a.nblk8 + (k >> 3)) * kTile + (c.i % kTile)) * kWB);
+          dst[0] = make_float4(wrow[0], wrow[1], wrow[2], wrow[3]);
+          dst[1] = make_float4(wrow[4], wrow[5], wrow[6], wrow[7]);
+        }
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, z && c.g == 0);
+    if (c.lane == 0 && bal) atomicAdd(&c.mcnt[k], __popc(bal));
+  }
+}
+
 template <int CMAX, int G, int MODE>
 __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
   extern __shared__ float sm[];
@@ -129,14 +233,19 @@ __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
   float* wwin = (float*)(mcnt + a.k);    // (blockDim / G) * 9
   float* ds = wwin + (blockDim.x / G) * 9;  // kc * pp
   __shared__ double red[32];
-  const int g = threadIdx.x % G;
-  const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
-  const bool live = i < a.n;
-  const int64_t ic = live ? i : 0;
-  const int lane = threadIdx.x & 31;
-  const int epoch = a.sc->epoch + 1;
-  const float geps = (float)a.sc->gamma_eps, gs = (float)a.sc->gamma_s;
-  const float inv_sqrt_gs = (float)(1.0 / sqrt(a.sc->gamma_s));
+  CodeConst c;
+  c.g = threadIdx.x % G;
+  c.i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  c.live = c.i < a.n;
+  c.ic = c.live ? c.i : 0;
+  c.lane = threadIdx.x & 31;
+  c.epoch = a.sc->epoch + 1;
+  c.geps = (float)a.sc->gamma_eps;
+  c.gs = (float)a.sc->gamma_s;
+  c.inv_sqrt_gs = (float)(1.0 / sqrt(a.sc->gamma_s));
+  c.logit = logit;
+  c.mcnt = mcnt;
+  c.wwin = wwin;
 
   for (int k = threadIdx.x; k < a.k; k += blockDim.x) {
     const double pk = fmin(fmax(a.pi[k], 1e-15), 1.0 - 1e-15);  // bpfa.py:173
@@ -147,115 +256,46 @@ __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
   int off[CMAX];
   int cnt = 0;
   int64_t r0 = 0;
-  if (live) { cnt = a.counts[i]; r0 = a.rowptr[i]; }
-  const int wmax = __reduce_max_sync(0xffffffffu, lane_slots<G>(cnt, g));
+  if (c.live) { cnt = a.counts[c.i]; r0 = a.rowptr[c.i]; }
+  const int wmax = __reduce_max_sync(0xffffffffu, lane_slots<G>(cnt, c.g));
 #pragma unroll
   for (int j = 0; j < CMAX; ++j) {
     off[j] = a.p;
     r[j] = 0.0f;
     if (j < wmax) {
-      const int s = j * G + g;
+      const int s = j * G + c.g;
       if (s < cnt) {
         off[j] = a.csr_p[r0 + s];
         r[j] = a.r_csc[a.csr_pos[r0 + s]];
       }
     }
   }
-  double sq_w = 0.0;
-  u32x4 rnd{0, 0, 0, 0};
-  float nrm0 = 0.f, nrm1 = 0.f;
-  // 1-deep software prefetch of the next atom's code (z, s) and replay draws
-  uint8_t zn = a.usage[ic];
-  float sn = a.weights[ic];
-  double un = 0.0, gnx = 0.0;
-  if (MODE == kRngReplay) { un = a.u_draw[ic]; gnx = a.g_draw[ic]; }
-  for (int k0 = 0; k0 < a.k; k0 += a.kc) {
-    const int kn = min(a.kc, a.k - k0);
+  CodeThread t;
+  t.sq_w = 0.0;
+  t.rnd = u32x4{0, 0, 0, 0};
+  t.nrm0 = t.nrm1 = 0.f;
+  t.zn = a.usage[c.ic];
+  t.sn = a.weights[c.ic];
+  t.un = t.gnx = 0.0;
+  if (MODE == kRngReplay) { t.un = a.u_draw[c.ic]; t.gnx = a.g_draw[c.ic]; }
+  if (a.kc >= a.k) {
+    // whole dictionary resident: stage once, then run the atom loop with the
+    // warp's live slot count as a compile-time constant (no padded-slot work)
     __syncthreads();
-    stage_atoms(ds, a.atoms, k0, kn, a.p, pp);
+    stage_atoms(ds, a.atoms, 0, a.k, a.p, pp);
     __syncthreads();
-    for (int kk = 0; kk < kn; ++kk) {
-      const int k = k0 + kk;
-      const float* d = ds + kk * pp;
-      const bool z_old = zn != 0;
-      const float s_old = sn;
-      const double ud = un, gd = gnx;
-      if (k + 1 < a.k) {
-        const int64_t zn_i = (int64_t)(k + 1) * a.ld + ic;
-        zn = a.usage[zn_i];
-        sn = a.weights[zn_i];
-        if (MODE == kRngReplay) {
-          const int64_t dn_i = (int64_t)(k + 1) * a.n + ic;
-          un = a.u_draw[dn_i];
-          gnx = a.g_draw[dn_i];
-        }
-      }
-      float dj[CMAX];
-      float u = 0.0f, v = 0.0f;
-#pragma unroll
-      for (int j = 0; j < CMAX; ++j) {
-        dj[j] = 0.0f;
-        if (j < wmax) {
-          dj[j] = d[off[j]];
-          u = fmaf(dj[j], dj[j], u);
-          v = fmaf(dj[j], r[j], v);
-        }
-      }
-      if (G > 1) {
-        u = gsum<G>(u);
-        v = gsum<G>(v);
-      }
-      bool z = false;
-      if (live) {
-        const int64_t zi = (int64_t)k * a.ld + i;
-        const float w_old = z_old ? s_old : 0.0f;
-        // _code_params (bpfa.py:169-178)
-        const float proj = fmaf(w_old, u, v);
-        const float log_rho = logit[k] - 0.5f * geps * (s_old * s_old * u - 2.0f * s_old * proj);
-        const float alpha = fmaf(geps, u, gs);
-        float s_new;
-        if (MODE == kRngReplay) {
-          z = (log(ud) - log1p(-ud)) < (double)log_rho;  // bpfa.py:262-263
-          const float gn = (float)gd;
-          s_new = z ? geps * proj / alpha + gn / sqrtf(alpha) : gn * inv_sqrt_gs;  // bpfa.py:265-269
-        } else {
-          if ((k & 1) == 0) {
-            rnd = philox4x32_10(u32x4{(uint32_t)i, (uint32_t)(i >> 32), (uint32_t)(k >> 1),
-                                      ((uint32_t)epoch & 0xFFFFFFu) | (kDomCode << 24)},
-                                a.key0, a.key1);
-            box_muller(rnd.z, rnd.w, nrm0, nrm1);
-          }
-          const float uu = u01_24((k & 1) ? rnd.y : rnd.x);
-          const float gn = (k & 1) ? nrm1 : nrm0;
-          z = uu * (1.0f + __expf(-log_rho)) < 1.0f;  // U < sigmoid(log_rho)
-          const float ra = rsqrtf(alpha);
-          s_new = z ? fmaf(geps * proj, ra * ra, gn * ra) : gn * inv_sqrt_gs;
-        }
-        const float w_new = z ? s_new : 0.0f;
-        const float dw = w_old - w_new;
-#pragma unroll
-        for (int j = 0; j < CMAX; ++j)
-          if (j < wmax) r[j] = fmaf(dw, dj[j], r[j]);
-        if (g == 0) {
-          a.usage[zi] = z ? 1 : 0;
-          a.weights[zi] = s_new;
-          sq_w += (double)s_new * (double)s_new;
-        }
-        // 8-atom window of w (shared memory, pitch 9: conflict-free) for the
-        // tile-blocked copy the dictionary step bulk-loads
-        if (g == 0) {
-          float* wrow = wwin + (threadIdx.x / G) * 9;
-          wrow[k & 7] = w_new;
-          if ((k & 7) == 7 || k == a.k - 1) {
-            for (int t = (k & 7) + 1; t < 8; ++t) wrow[t] = 0.0f;  // partial last block
-            float4* dst = (float4*)(a.wt + (((i / kTile) * a.nblk8 + (k >> 3)) * kTile + (i % kTile)) * kWB);
-            dst[0] = make_float4(wrow[0], wrow[1], wrow[2], wrow[3]);
-            dst[1] = make_float4(wrow[4], wrow[5], wrow[6], wrow[7]);
-          }
-        }
-      }
-      const unsigned bal = __ballot_sync(0xffffffffu, z && g == 0);
-      if (lane == 0 && bal) atomicAdd(&mcnt[k], __popc(bal));
+    const int wc = (wmax + 7) & ~7;
+    if (wc <= 8 || CMAX == 8) code_atoms<CMAX, (CMAX < 8 ? CMAX : 8), G, MODE>(a, c, 0, a.k, ds, pp, r, off, t);
+    else if (wc <= 16 || CMAX == 16) code_atoms<CMAX, (CMAX < 16 ? CMAX : 16), G, MODE>(a, c, 0, a.k, ds, pp, r, off, t);
+    else if (wc <= 24 || CMAX == 24) code_atoms<CMAX, (CMAX < 24 ? CMAX : 24), G, MODE>(a, c, 0, a.k, ds, pp, r, off, t);
+    else code_atoms<CMAX, CMAX, G, MODE>(a, c, 0, a.k, ds, pp, r, off, t);
+  } else {
+    for (int k0 = 0; k0 < a.k; k0 += a.kc) {
+      const int kn = min(a.kc, a.k - k0);
+      __syncthreads();
+      stage_atoms(ds, a.atoms, k0, kn, a.p, pp);
+      __syncthreads();
+      code_atoms<CMAX, CMAX, G, MODE>(a, c, k0, kn, ds, pp, r, off, t);
     }
   }
   double sq_r = 0.0;
@@ -263,10 +303,10 @@ __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
   for (int j = 0; j < CMAX; ++j) {
     sq_r += (double)r[j] * (double)r[j];
     // the end-of-sweep residual is the next epoch's starting residual (carry mode)
-    const int s = j * G + g;
-    if (live && j < wmax && s < cnt) a.r_csc[a.csr_pos[r0 + s]] = r[j];
+    const int s = j * G + c.g;
+    if (c.live && j < wmax && s < cnt) a.r_csc[a.csr_pos[r0 + s]] = r[j];
   }
-  const double bw = block_sum_d(sq_w, red);
+  const double bw = block_sum_d(t.sq_w, red);
   __syncthreads();
   const double br = block_sum_d(sq_r, red);
   if (threadIdx.x == 0) {
