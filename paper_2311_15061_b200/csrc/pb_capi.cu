@@ -1,6 +1,7 @@
 // pb200 — C ABI (include/pb200.h) over the sm_100a kernels, plus the native
 // stateful "problem" used for the host-buffer live-frame path.
 #include <stdarg.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -170,6 +171,7 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
     g.draws = d->rng_mode == PB_RNG_REPLAY ? d->atom_draws : nullptr;
     g.sc = sc; g.partials = ws.partials; g.reduced = ws.reduced; g.bar = ws.bar; g.max_blocks = kMaxDictBlocks;
     g.prof = g_dict_prof;
+    { const char* e = getenv("PB_DICT_DEBUG"); g.dbg = e ? atoi(e) : 0; }
     g.n = d->n; g.p = d->p; g.k = d->k; g.key0 = k0; g.key1 = k1;
     g.ld = c.ld;
     if ((rc = launch_dict_gram(g, st))) return rc;

@@ -37,6 +37,15 @@ __device__ __forceinline__ void stage_atoms(float* ds, const float* __restrict__
   }
 }
 
+// Float offset of 16-byte chunk h (0/1) of patch row il inside a tile block of
+// the code copy W ([kTile][8] floats).  Chunks are XOR-swizzled across each
+// 128-byte line so the dictionary step's row gathers spread over all banks.
+__device__ __forceinline__ int wsw(int il, int h) {
+  const int line = il >> 2;
+  const int cw = ((il & 3) << 1) | h;
+  return line * 32 + ((cw ^ (line & 7)) << 2);
+}
+
 template <int G>
 __device__ __forceinline__ float gsum(float v) {
 #pragma unroll
@@ -95,11 +104,12 @@ __global__ void __launch_bounds__(256) k_resid_compact(CompactArgs a) {
         wv[q] = (live && kb + q < kn && z) ? -w : 0.0f;
       }
       if (a.wt && live && g == 0) {  // tile-blocked copy of w for the dictionary step
-        float4* dst = (float4*)(a.wt + (((i / kTile) * a.nblk8 + ((k0 + kb) >> 3)) * kTile + (i % kTile)) * kWB);
-        dst[0] = make_float4(wv[0] != 0.f ? -wv[0] : 0.f, wv[1] != 0.f ? -wv[1] : 0.f,
-                             wv[2] != 0.f ? -wv[2] : 0.f, wv[3] != 0.f ? -wv[3] : 0.f);
-        dst[1] = make_float4(wv[4] != 0.f ? -wv[4] : 0.f, wv[5] != 0.f ? -wv[5] : 0.f,
-                             wv[6] != 0.f ? -wv[6] : 0.f, wv[7] != 0.f ? -wv[7] : 0.f);
+        float* blk = a.wt + ((i / kTile) * a.nblk8 + ((k0 + kb) >> 3)) * kTile * kWB;
+        const int il = (int)(i % kTile);
+        *(float4*)(blk + wsw(il, 0)) = make_float4(wv[0] != 0.f ? -wv[0] : 0.f, wv[1] != 0.f ? -wv[1] : 0.f,
+                                                   wv[2] != 0.f ? -wv[2] : 0.f, wv[3] != 0.f ? -wv[3] : 0.f);
+        *(float4*)(blk + wsw(il, 1)) = make_float4(wv[4] != 0.f ? -wv[4] : 0.f, wv[5] != 0.f ? -wv[5] : 0.f,
+                                                   wv[6] != 0.f ? -wv[6] : 0.f, wv[7] != 0.f ? -wv[7] : 0.f);
       }
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -213,9 +223,10 @@ __device__ __forceinline__ void code_atoms(const CompactArgs& a, const CodeConst
         wrow[k & 7] = w_new;
         if ((k & 7) == 7 || k == a.k - 1) {
           for (int q = (k & 7) + 1; q < 8; ++q) wrow[q] = 0.0f;  // partial last block
-          float4* dst = (float4*)(a.wt + (((c.i / kTile) * a.nblk8 + (k >> 3)) * kTile + (c.i % kTile)) * kWB);
-          dst[0] = make_float4(wrow[0], wrow[1], wrow[2], wrow[3]);
-          dst[1] = make_float4(wrow[4], wrow[5], wrow[6], wrow[7]);
+          float* blk = a.wt + ((c.i / kTile) * a.nblk8 + (k >> 3)) * kTile * kWB;
+          const int il = (int)(c.i % kTile);
+          *(float4*)(blk + wsw(il, 0)) = make_float4(wrow[0], wrow[1], wrow[2], wrow[3]);
+          *(float4*)(blk + wsw(il, 1)) = make_float4(wrow[4], wrow[5], wrow[6], wrow[7]);
         }
       }
     }
@@ -412,6 +423,8 @@ __device__ __forceinline__ uint64_t gtimer() {
 //   registers, and transpose-reduce them at the end of the segment.  Segments
 //   wholly owned by one warp add straight into the CTA accumulator; the (at
 //   most two) boundary segments go to per-warp slots merged in warp order.
+constexpr int kTbCache = 1024;  // tile bases cached in shared memory per CTA
+
 template <int B>
 __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
   using L = GramLayout<B>;
@@ -425,9 +438,10 @@ __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
   float* acc = (float*)(smraw + a.wbytes);               // p * NACC
   float* slots = acc + (size_t)p * L::NACC;              // NW * 2 * NACC
   int* slot_col = (int*)(slots + NW * 2 * L::NACC);      // NW * 2
-  int* cps = slot_col + NW * 2;                          // 2 * (p + 1) (double-buffered tile colptr)
-  const int cpp = (p + 1 + 3) & ~3;
-  float* dold = (float*)(cps + 2 * cpp);                 // B * p
+  const int cpp = colptr_pitch(p);
+  int* cps = slot_col + NW * 2;                          // 2 * cpp (double-buffered tile colptr, bulk-copied)
+  int64_t* tbs = (int64_t*)(cps + 2 * cpp);             // kTbCache tile bases of this CTA
+  float* dold = (float*)(tbs + kTbCache);                // B * p
   float* dprev = dold + B * p;                           // B * p
   double* red64 = (double*)smraw;                        // p * NACC (aliases the staging)
   __shared__ __align__(8) uint64_t mbar[2];
@@ -458,6 +472,11 @@ __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
     while (t_hi < a.ntiles && a.tile_base[t_hi] < e_hi) ++t_hi;
     if (e_hi <= e_lo) t_hi = t_lo;
   }
+  const bool tb_cached = t_hi - t_lo + 1 <= kTbCache;
+  if (tb_cached)
+    for (int t = threadIdx.x; t <= t_hi - t_lo; t += blockDim.x) tbs[t] = a.tile_base[t_lo + t];
+  __syncthreads();
+  auto tile_start = [&](int t) { return tb_cached ? tbs[t - t_lo] : a.tile_base[t]; };
   uint64_t t_mark = a.prof ? gtimer() : 0;
   auto prof = [&](int slot) {
     if (a.prof && threadIdx.x == 0) {
@@ -481,119 +500,60 @@ __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
     // async staging: bulk-copy the tile's W blocks (current, previous) into a stage
     auto issue = [&](int tile, uint32_t stage) {
       fence_proxy_async();
-      const uint32_t bytes = (has_cur ? kTile * B * 4u : 0u) + (has_prev ? kTile * B * 4u : 0u);
+      const uint32_t bytes = (has_cur ? kTile * B * 4u : 0u) + (has_prev ? kTile * B * 4u : 0u) + cpp * 4u;
       mbar_expect_tx(&mbar[stage], bytes);
+      bulk_copy_g2s(cps + stage * cpp, a.colptr + (int64_t)tile * cpp, cpp * 4u, &mbar[stage]);
       float* dst = wbuf + (size_t)stage * 2 * kTile * B;
       if (has_cur) bulk_copy_g2s(dst, a.wt + ((int64_t)tile * a.nblk8 + blk) * kTile * B, kTile * B * 4u, &mbar[stage]);
       if (has_prev)
         bulk_copy_g2s(dst + kTile * B, a.wt + ((int64_t)tile * a.nblk8 + blk - 1) * kTile * B, kTile * B * 4u,
                       &mbar[stage]);
     };
-    auto load_cps = [&](int tile, uint32_t stage) {
-      const int64_t tb0 = a.tile_base[tile];
-      for (int t = threadIdx.x; t <= p; t += blockDim.x)
-        cps[stage * cpp + t] = (int)(a.colptr[(int64_t)tile * (p + 1) + t] - tb0);
-    };
     __syncthreads();
     if (t_lo < t_hi) {
-      if (threadIdx.x == 0) issue(t_lo, seq & 1);
-      load_cps(t_lo, seq & 1);
+      if (threadIdx.x == 0 && !(a.dbg & 4)) issue(t_lo, seq & 1);
     }
     for (int tile = t_lo; tile < t_hi; ++tile, ++seq) {
       prof(7);
       const uint32_t st = seq & 1;
       __syncthreads();   // previous tile fully consumed: its stage and cps buffer are free
       if (tile + 1 < t_hi) {
-        if (threadIdx.x == 0) issue(tile + 1, st ^ 1);
-        load_cps(tile + 1, st ^ 1);
+        if (threadIdx.x == 0 && !(a.dbg & 4)) issue(tile + 1, st ^ 1);
       }
       if (lane == 0) { slot_col[wid * 2] = -1; slot_col[wid * 2 + 1] = -1; }
-      const int64_t tb = a.tile_base[tile];
-      const int64_t rs = max(tb, e_lo), re = min(a.tile_base[tile + 1], e_hi);
+      const int64_t tb = tile_start(tile);
+      const int64_t rs = max(tb, e_lo), re = min(tile_start(tile + 1), e_hi);
       const float* wcur = wbuf + (size_t)st * 2 * kTile * B;
       const float* wprev = wcur + kTile * B;
       const int* cpt = cps + st * cpp;
-      mbar_wait(&mbar[st], (phase_bits >> st) & 1u);
+      if (!(a.dbg & 4)) mbar_wait(&mbar[st], (phase_bits >> st) & 1u);
       phase_bits ^= 1u << st;
       prof(0);
       const int m = (int)(re - rs);
       const int ws = (int)(rs - tb) + (int)((int64_t)m * wid / NW), we = (int)(rs - tb) + (int)((int64_t)m * (wid + 1) / NW);
-      if (ws < we) {
-        // first / last column touched by this warp's slice (binary search, shared colptr)
-        int c_first = 0, c_last = 0;
+      if (ws < we && !(a.dbg & 8)) {
+        // Stream the warp's slice [ws, we) in 128-element chunks with the next
+        // chunk's loads in flight, independent of column boundaries; the
+        // per-column sums are flushed (transpose-reduced) where a column ends.
+        int c = 0;
         {
           int lo = 0, hi = p - 1;
           while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (cpt[mid] <= ws) lo = mid; else hi = mid - 1; }
-          c_first = lo;
-          lo = c_first; hi = p - 1;
-          while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (cpt[mid] <= we - 1) lo = mid; else hi = mid - 1; }
-          c_last = lo;
+          c = lo;
         }
+        const int c_first = c;
+        int cend = min(we, cpt[c + 1]);
         const int64_t ebase = tb;
-        for (int c = c_first; c <= c_last; ++c) {
-          const int cs = max(ws, cpt[c]), ce = min(we, cpt[c + 1]);
-          if (cs >= ce) continue;
-          float dl[B];
+        float dl[B];
 #pragma unroll
-          for (int j = 0; j < B; ++j) dl[j] = has_prev ? dprev[j * p + c] : 0.0f;
-          float v[L::NP];
+        for (int j = 0; j < B; ++j) dl[j] = has_prev ? dprev[j * p + c] : 0.0f;
+        float v[L::NP];
 #pragma unroll
-          for (int q = 0; q < L::NP; ++q) v[q] = 0.0f;
-          // software pipeline: the next 128 elements' loads are in flight while
-          // the current 128 are processed
-          int ilq[4], iln[4];
-          float rq[4], rn[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int e = cs + q * 32 + lane;
-            iln[q] = e < ce ? (int)a.e_loc[ebase + e] : -1;
-            rn[q] = e < ce ? a.r_csc[ebase + e] : 0.0f;
-          }
-          for (int eb = cs; eb < ce; eb += 128) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              ilq[q] = iln[q];
-              rq[q] = rn[q];
-              const int e = eb + 128 + q * 32 + lane;
-              iln[q] = e < ce ? (int)a.e_loc[ebase + e] : -1;
-              rn[q] = e < ce ? a.r_csc[ebase + e] : 0.0f;
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              if (ilq[q] < 0) continue;
-              const int il = ilq[q];
-              float r = rq[q];
-              if (has_prev) {
-                const float4* wp4 = (const float4*)(wprev + il * B);
-#pragma unroll
-                for (int h = 0; h < B / 4; ++h) {
-                  const float4 w4 = wp4[h];
-                  r = fmaf(w4.x, dl[4 * h + 0], r);
-                  r = fmaf(w4.y, dl[4 * h + 1], r);
-                  r = fmaf(w4.z, dl[4 * h + 2], r);
-                  r = fmaf(w4.w, dl[4 * h + 3], r);
-                }
-                a.r_csc[ebase + eb + q * 32 + lane] = r;
-              }
-              if (has_cur) {
-                float wc[B];
-                const float4* wc4 = (const float4*)(wcur + il * B);
-#pragma unroll
-                for (int h = 0; h < B / 4; ++h) {
-                  const float4 w4 = wc4[h];
-                  wc[4 * h + 0] = w4.x; wc[4 * h + 1] = w4.y; wc[4 * h + 2] = w4.z; wc[4 * h + 3] = w4.w;
-                }
-#pragma unroll
-                for (int j = 0; j < B; ++j) {
-                  v[j] = fmaf(wc[j], r, v[j]);
-#pragma unroll
-                  for (int l = 0; l <= j; ++l) v[L::gidx(j, l)] = fmaf(wc[j], wc[l], v[L::gidx(j, l)]);
-                }
-              }
-            }
-          }
-          if (has_cur) {
-            warp_transpose_reduce<L::NP>(v, lane);
+        for (int q = 0; q < L::NP; ++q) v[q] = 0.0f;
+        auto flush = [&]() {  // column c's segment of this slice is complete
+          const int cs = max(ws, cpt[c]);
+          if (has_cur && cs < cend) {
+            if (!(a.dbg & 2)) warp_transpose_reduce<L::NP>(v, lane);
             const bool exclusive = cpt[c] >= ws && cpt[c + 1] <= we;
             const int slot = c == c_first ? 0 : 1;
             if ((lane & 1) == 0) {
@@ -609,6 +569,77 @@ __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
               }
             }
             if (!exclusive && lane == 0) slot_col[wid * 2 + slot] = c;
+#pragma unroll
+            for (int q = 0; q < L::NP; ++q) v[q] = 0.0f;
+          }
+          ++c;
+          if (c < p) {
+            cend = min(we, cpt[c + 1]);
+#pragma unroll
+            for (int j = 0; j < B; ++j) dl[j] = has_prev ? dprev[j * p + c] : 0.0f;
+          }
+        };
+        int iln[4];
+        float rn[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int e = ws + q * 32 + lane;
+          iln[q] = e < we ? (int)a.e_loc[ebase + e] : -1;
+          rn[q] = e < we ? a.r_csc[ebase + e] : 0.0f;
+        }
+        for (int eb = ws; eb < we; eb += 128) {
+          int ilq[4];
+          float rq[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            ilq[q] = iln[q];
+            rq[q] = rn[q];
+            const int e = eb + 128 + q * 32 + lane;
+            iln[q] = e < we ? (int)a.e_loc[ebase + e] : -1;
+            rn[q] = e < we ? a.r_csc[ebase + e] : 0.0f;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int s0 = eb + q * 32;
+            if (s0 >= we) break;
+            const int s1 = min(s0 + 32, we);
+            const int e = s0 + lane;
+            int lo = s0;
+            while (lo < s1) {  // warp-uniform: split the 32 elements at column ends
+              const int hi = min(s1, cend);
+              if (e >= lo && e < hi && !(a.dbg & 1)) {
+                const int il = ilq[q];
+                float r = rq[q];
+                if (has_prev) {
+                  float sh[B / 4];
+#pragma unroll
+                  for (int h = 0; h < B / 4; ++h) {  // independent partial sums: short FMA chains
+                    const float4 w4 = *(const float4*)(wprev + wsw(il, h));
+                    sh[h] = fmaf(w4.w, dl[4 * h + 3],
+                                 fmaf(w4.z, dl[4 * h + 2], fmaf(w4.y, dl[4 * h + 1], w4.x * dl[4 * h])));
+                  }
+#pragma unroll
+                  for (int h = 0; h < B / 4; ++h) r += sh[h];
+                  a.r_csc[ebase + e] = r;
+                }
+                if (has_cur) {
+                  float wc[B];
+#pragma unroll
+                  for (int h = 0; h < B / 4; ++h) {
+                    const float4 w4 = *(const float4*)(wcur + wsw(il, h));
+                    wc[4 * h + 0] = w4.x; wc[4 * h + 1] = w4.y; wc[4 * h + 2] = w4.z; wc[4 * h + 3] = w4.w;
+                  }
+#pragma unroll
+                  for (int j = 0; j < B; ++j) {
+                    v[j] = fmaf(wc[j], r, v[j]);
+#pragma unroll
+                    for (int l = 0; l <= j; ++l) v[L::gidx(j, l)] = fmaf(wc[j], wc[l], v[L::gidx(j, l)]);
+                  }
+                }
+              }
+              if (hi == cend) flush();
+              lo = hi;
+            }
           }
         }
       }
@@ -769,7 +800,7 @@ static int launch_dict_gram_b(DictGramArgs a, cudaStream_t st) {
   const size_t wbytes = std::max((size_t)2 * 2 * kTile * B * 4, (size_t)a.p * L::NACC * 8);
   a.wbytes = (int)wbytes;
   const size_t smem = wbytes + (size_t)a.p * L::NACC * 4 + (size_t)16 * 2 * L::NACC * 4 + 16 * 2 * 4 +
-                      (size_t)2 * ((a.p + 1 + 3) & ~3) * 4 + (size_t)2 * B * a.p * 4;
+                      (size_t)2 * colptr_pitch(a.p) * 4 + (size_t)kTbCache * 8 + (size_t)2 * B * a.p * 4;
   if (smem > 225 * 1024) { set_error("patch size %d too large for the dictionary step", a.p); return PB_EUNSUPPORTED; }
   PB_CUDA_TRY(cudaFuncSetAttribute(k_dict_gram<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;

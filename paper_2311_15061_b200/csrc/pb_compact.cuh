@@ -57,6 +57,7 @@ struct DictGramArgs {
   double* reduced;      // P * NACC
   unsigned* bar;        // 2
   unsigned long long* prof;  // optional [gridDim][8] phase nanoseconds (profiling)
+  int dbg;              // profiling-only: 1 skip element math, 2 skip segment reductions
   int max_blocks;
   int wbytes;
   int64_t n;

@@ -10,7 +10,8 @@
 //     of kTile consecutive patches; inside a tile, elements are grouped by
 //     patch offset p (column) and sorted by patch.  Per element: e_loc (u16,
 //     patch index inside the tile), x_csc (the observed value), and the
-//     residual lives in this order.  colptr[t][p] = first element of column p.
+//     residual lives in this order.  colptr[t][p] = first element of column p
+//     relative to the tile start (rows padded to 16 bytes for bulk copies).
 //   CSR order (the code step's order): per patch, its observed offsets in
 //     ascending p: csr_p (u16) and csr_pos (u32, the element's CSC position),
 //     slots [rowptr[i], rowptr[i] + count[i]).
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(kFillThreads) k_tile_fill(
     const int o0 = (live0 && obs[(int64_t)pe * n + g0]) ? 1 : 0;
     const int o1 = (live1 && obs[(int64_t)pe * n + g1]) ? 1 : 0;
     const int rank = block_excl_scan(o0 + o1, wsum, tot);
-    if (threadIdx.x == 0) colptr[(int64_t)t * (p + 1) + pe] = (int32_t)col;
+    if (threadIdx.x == 0) colptr[(int64_t)t * colptr_pitch(p) + pe] = (int32_t)(col - tb);
     if (o0) {
       const int64_t pos = col + rank;
       e_loc[pos] = (uint16_t)l0;
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(kFillThreads) k_tile_fill(
     }
     col += tot;
   }
-  if (threadIdx.x == 0) colptr[(int64_t)t * (p + 1) + p] = (int32_t)col;
+  if (threadIdx.x == 0) colptr[(int64_t)t * colptr_pitch(p) + p] = (int32_t)(col - tb);
 }
 
 // Refresh the CSC values for a new frame under a cached mask (live path).
@@ -181,7 +182,7 @@ int index_bytes(int64_t n, int p, int64_t nnz_upper, size_t* out) {
   auto a = [&](size_t x) { b += (x + 255) & ~size_t(255); };
   a((size_t)ntiles * 4);              // tile_tot
   a((size_t)(ntiles + 1) * 8);        // tile_base
-  a((size_t)ntiles * (p + 1) * 4);    // colptr
+  a((size_t)ntiles * colptr_pitch(p) * 4);    // colptr
   a((size_t)(n + 1) * 8);             // rowptr
   a((size_t)nnz_upper * 2);           // e_loc
   a((size_t)nnz_upper * 4);           // x_csc
@@ -199,7 +200,7 @@ void carve_index(PatchIndex& ix, char* base, int64_t n, int p, int64_t nnz_upper
   ix.n = n; ix.p = p; ix.ntiles = (int)ntiles;
   ix.tile_tot = (int32_t*)take((size_t)ntiles * 4);
   ix.tile_base = (int64_t*)take((size_t)(ntiles + 1) * 8);
-  ix.colptr = (int32_t*)take((size_t)ntiles * (p + 1) * 4);
+  ix.colptr = (int32_t*)take((size_t)ntiles * colptr_pitch(p) * 4);
   ix.rowptr = (int64_t*)take((size_t)(n + 1) * 8);
   ix.e_loc = (uint16_t*)take((size_t)nnz_upper * 2);
   ix.x_csc = (float*)take((size_t)nnz_upper * 4);

@@ -8,13 +8,15 @@ constexpr int kTile = 1024;        // patches per CSC tile (one dict-step work u
 constexpr int kFillThreads = 512;  // index-build block size (two patches per thread)
 constexpr int kWB = 8;             // atoms per block of the tile-blocked code copy W
 
+__host__ __device__ constexpr int colptr_pitch(int p) { return (p + 1 + 3) & ~3; }
+
 struct PatchIndex {
   int64_t n;
   int p;
   int ntiles;
   int32_t* tile_tot;    // [ntiles]
   int64_t* tile_base;   // [ntiles + 1] first element of each tile; tile_base[ntiles] = nnz
-  int32_t* colptr;      // [ntiles][p + 1] global element offset of each column
+  int32_t* colptr;      // [ntiles][colptr_pitch(p)] tile-relative first element of each column (p+1 used)
   int64_t* rowptr;      // [n + 1] first CSR slot of each patch
   uint16_t* e_loc;      // [nnz] CSC: patch index inside its tile
   float* x_csc;         // [nnz] CSC: observed (mean-subtracted) value

@@ -51,14 +51,23 @@ __global__ void __launch_bounds__(256) k_accumulate_atoms(
       ds[t] = pe < p ? atoms[(int64_t)(k0 + kk) * p + pe] : 0.0f;
     }
     __syncthreads();
-    if (live) {
-      for (int kk = 0; kk < kn; ++kk) {
-        const int64_t zi = (int64_t)(k0 + kk) * ld + i;
-        if (!usage[zi]) continue;
-        const float w = RESID ? -weights[zi] : weights[zi];
-        const float* d = ds + kk * PP + g;
+    const int64_t ic = live ? i : 0;
+    for (int kb = 0; kb < kn; kb += 8) {
+      // the 8 atoms' (usage, weight) loads are independent: issue them all first
+      float wv[8];
 #pragma unroll
-        for (int j = 0; j < VPT; ++j) acc[j] = fmaf(w, d[j * G], acc[j]);
+      for (int q = 0; q < 8; ++q) {
+        const int64_t zi = (int64_t)(k0 + min(kb + q, kn - 1)) * ld + ic;
+        const uint8_t z = usage[zi];
+        const float w = weights[zi];
+        wv[q] = (live && kb + q < kn && z) ? (RESID ? -w : w) : 0.0f;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (!__any_sync(0xffffffffu, wv[q] != 0.0f)) continue;
+        const float* d = ds + (kb + q) * PP + g;
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) acc[j] = fmaf(wv[q], d[j * G], acc[j]);
       }
     }
   }

@@ -134,7 +134,7 @@ def _carve(buf, n, p, nnz):
     nt = -(-n // kt)
     out, off = {}, 0
     for name, cnt, dt in [("tile_tot", nt, np.int32), ("tile_base", nt + 1, np.int64),
-                          ("colptr", nt * (p + 1), np.int32), ("rowptr", n + 1, np.int64),
+                          ("colptr", nt * ((p + 1 + 3) & ~3), np.int32), ("rowptr", n + 1, np.int64),
                           ("e_loc", nnz, np.uint16), ("x_csc", nnz, np.float32), ("csr_p", nnz, np.uint16),
                           ("csr_pos", nnz, np.uint32)]:
         nb = cnt * np.dtype(dt).itemsize
@@ -168,7 +168,8 @@ def test_observed_element_index_exact(cuda_device, shape, patch, ratio, kind):
     tile = rows // 1024
     assert np.array_equal(b["e_loc"][pos].astype(np.int64), rows - tile * 1024)
     assert np.array_equal(b["x_csc"][pos], vals[rows, cols].astype(np.float32))
-    cp = b["colptr"].reshape(-1, p + 1)
+    tb = b["tile_base"].astype(np.int64)
+    cp = b["colptr"].reshape(-1, (p + 1 + 3) & ~3)[:, :p + 1].astype(np.int64) + tb[:-1, None]  # tile-relative
     assert np.all((pos >= cp[tile, cols]) & (pos < cp[tile, cols + 1]))
     # CSC order inside a column: ascending patch
     for t in range(cp.shape[0]):

@@ -14,13 +14,20 @@ CFGS = {
     1: dict(shape=(256, 256), ratio=0.25, kind="uniform-random", patch=(8, 8), k=64, epochs=10),
     3: dict(shape=(512, 512), ratio=0.25, kind="line-hop", patch=(8, 8), k=256, epochs=2),
     2: dict(shape=(1024, 1024), ratio=0.10, kind="uniform-random", patch=(10, 10), k=256, epochs=3),
+    4: dict(shape=(256, 256, 128), ratio=0.20, kind="uniform-random", patch=(8, 8, 4), k=512, epochs=2),
+    5: dict(shape=(4096, 4096), ratio=0.10, kind="uniform-random", patch=(8, 8), k=256, epochs=2),
 }
 
 for cid in [int(a) for a in sys.argv[1:]] or [1, 3, 2]:
     c = CFGS[cid]
-    img = inputs.synthetic_texture(c["shape"], seed=0)
+    if len(c["shape"]) == 2:
+        img = inputs.synthetic_texture(c["shape"], seed=0)
+    else:  # hyperspectral-like cube: per-band texture with a smooth spectral modulation
+        base = inputs.synthetic_texture(c["shape"][:2], seed=0)
+        spec = 0.5 + 0.5 * np.sin(np.linspace(0, 3 * np.pi, c["shape"][2]))
+        img = base[:, :, None] * spec[None, None, :]
     mask = inputs.make_mask(c["shape"], c["ratio"], c["kind"], 0)
-    pm = pp.extract_patches(img, mask, pp.PatchSpec(c["patch"]), True)
+    pm = pp.extract_patches(img, mask, pp.PatchSpec(c["patch"]), len(c["shape"]) == 2)
     hp = gb.Hyperparams(num_atoms=c["k"])
     st, est = gb.infer(pm, hp, 1, 0, rng="philox")  # warm-up
     torch.cuda.synchronize()
