@@ -69,6 +69,12 @@ int pb_extract_patches(const pb_grid_desc* g, const void* tensor, int32_t tensor
                        int32_t mean_subtract, float* values, uint8_t* observed, float* means,
                        int32_t* counts, void* stream);
 
+/* A shard of the patch matrix: global patches [first_patch, first_patch + num_patches)
+ * into (P, num_patches) outputs (multi-GPU sharding by contiguous patch ranges). */
+int pb_extract_patch_range(const pb_grid_desc* g, const void* tensor, int32_t tensor_f64, const uint8_t* mask,
+                           int32_t mean_subtract, int64_t first_patch, int64_t num_patches, float* values,
+                           uint8_t* observed, float* means, int32_t* counts, void* stream);
+
 /* reconstitute + apply_data_consistency (patches.py:188-229).
  * out[x] = sum_{i covers x} (est_scale*est[p,i] + means[i]) / coverage(x);
  * if dc: out[x] = original[x] where mask[x].  out/original are f64 if io_f64 else f32.
@@ -76,6 +82,12 @@ int pb_extract_patches(const pb_grid_desc* g, const void* tensor, int32_t tensor
 int pb_reconstitute(const pb_grid_desc* g, const float* est, float est_scale, const float* means,
                     const void* original, const uint8_t* mask, int32_t dc, int32_t io_f64, void* out,
                     unsigned long long* uncovered, void* stream);
+
+/* Overlap-add of a shard (patches [first_patch, first_patch + num_patches), est/means
+ * shard-local): raw f64 sums of (est_scale*est + mean) per element, no division.
+ * Summing these across ranks and dividing by coverage gives reconstitute(). */
+int pb_ola_partial(const pb_grid_desc* g, const float* est, float est_scale, const float* means, int64_t first_patch,
+                   int64_t num_patches, double* acc_out, void* stream);
 
 /* coverage_map (patches.py:181-185), int32 of the tensor shape. */
 int pb_coverage_map(const pb_grid_desc* g, int32_t* out, void* stream);
@@ -137,6 +149,12 @@ typedef struct pb_scalars {
   int32_t diverged;  /* set by the device pi/gamma draw on non-finite state */
 } pb_scalars;
 
+/* Collective hook for sharded (multi-GPU) epochs: sum `count` elements of
+ * `device_buf` (dtype 0 = f64, 1 = int32) across all ranks, stream-ordered on
+ * `stream`, result in place.  Return 0 on success.  Implemented by the caller
+ * (NCCL through torch.distributed in the Python package). */
+typedef int (*pb_allreduce_fn)(void* ctx, void* device_buf, int64_t count, int32_t dtype, void* stream);
+
 typedef struct pb_epoch_desc {
   int64_t n;
   int64_t ld;               /* row pitch of usage/weights (K, ld); 0 => n */
@@ -164,6 +182,12 @@ typedef struct pb_epoch_desc {
   const double* code_g;     /* (K,N) normals,  stream (seed,3,epoch,k) standard_normal(N) */
   /* workspace from pb_epoch_workspace_bytes() */
   void* workspace;
+  /* sharding: this rank holds global patches [i_offset, i_offset + n) of n_global;
+   * n_obs is the global observed count.  allreduce == NULL => single rank. */
+  int64_t i_offset;
+  int64_t n_global;
+  pb_allreduce_fn allreduce;
+  void* allreduce_ctx;
 } pb_epoch_desc;
 
 size_t pb_epoch_workspace_bytes(int64_t n, int32_t p, int32_t k, int64_t nnz);

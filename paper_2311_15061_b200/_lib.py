@@ -47,13 +47,17 @@ class PatchIndex(ctypes.Structure):
                 ("buffer", c_vp)]
 
 
+ALLREDUCE_FN = ctypes.CFUNCTYPE(c_i32, c_vp, c_vp, c_i64, c_i32, c_vp)
+
+
 class EpochDesc(ctypes.Structure):
     _fields_ = [("n", c_i64), ("ld", c_i64), ("p", c_i32), ("k", c_i32), ("freeze_dict", c_i32), ("rng_mode", c_i32),
                 ("resid_mode", c_i32), ("seed", c_u64), ("n_obs", c_i64), ("hyper", c_f64 * 6),
                 ("values", c_vp), ("observed", c_vp), ("counts", c_vp), ("index", ctypes.POINTER(PatchIndex)),
                 ("atoms", c_vp), ("pi", c_vp), ("usage", c_vp),
                 ("weights", c_vp), ("scalars", c_vp), ("atom_draws", c_vp), ("code_u", c_vp),
-                ("code_g", c_vp), ("workspace", c_vp)]
+                ("code_g", c_vp), ("workspace", c_vp), ("i_offset", c_i64), ("n_global", c_i64),
+                ("allreduce", ALLREDUCE_FN), ("allreduce_ctx", c_vp)]
 
 
 class ProblemDesc(ctypes.Structure):
@@ -70,9 +74,12 @@ SIGNATURES = {
     "pb_grid_counts": (c_i32, [ctypes.POINTER(GridDesc), c_vp, c_vp, c_vp]),
     "pb_extract_patches": (c_i32, [ctypes.POINTER(GridDesc), c_vp, c_i32, c_vp, c_i32, c_vp, c_vp, c_vp,
                                    c_vp, c_vp]),
+    "pb_extract_patch_range": (c_i32, [ctypes.POINTER(GridDesc), c_vp, c_i32, c_vp, c_i32, c_i64, c_i64, c_vp,
+                                       c_vp, c_vp, c_vp, c_vp]),
     "pb_reconstitute": (c_i32, [ctypes.POINTER(GridDesc), c_vp, c_f32, c_vp, c_vp, c_vp, c_i32, c_i32,
                                 c_vp, c_vp, c_vp]),
     "pb_coverage_map": (c_i32, [ctypes.POINTER(GridDesc), c_vp, c_vp]),
+    "pb_ola_partial": (c_i32, [ctypes.POINTER(GridDesc), c_vp, c_f32, c_vp, c_i64, c_i64, c_vp, c_vp]),
     "pb_residual_full": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_i64, c_vp]),
     "pb_compose_estimates": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_i64, c_i32, c_vp]),
     "pb_atom_moments": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp]),

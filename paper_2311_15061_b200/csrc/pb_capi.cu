@@ -54,6 +54,7 @@ struct EpochWs {
   unsigned* bar;
   double* block_sums;
   int32_t* m_count;
+  float* delta_g;   // split-mode atom shifts of the previous block [8][P]
 };
 static const int kMaxDictBlocks = 148 * 8;
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -68,7 +69,9 @@ static size_t ws_bytes(int64_t n, int p, int k, int64_t nnz, EpochWs* ws, char* 
   char* bar = take(16);
   char* bs = take((size_t)ceil_div(n * 32, 256) * 2 * 8);  // upper bound of code-step blocks
   char* mc = take((size_t)k * 4);
+  char* dg = take((size_t)8 * p * 4);
   if (ws) {
+    ws->delta_g = (float*)dg;
     ws->r_csc = (float*)r; ws->wt = (float*)wt; ws->wt_bytes = wtb;
     ws->partials = (float*)pa; ws->reduced = (double*)rd;
     ws->bar = (unsigned*)bar; ws->block_sums = (double*)bs; ws->m_count = (int32_t*)mc;
@@ -147,6 +150,8 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
   c.block_sums = ws.block_sums; c.m_count = ws.m_count;
   c.n = d->n; c.p = d->p; c.k = d->k; c.key0 = k0; c.key1 = k1;
   c.ld = d->ld > d->n ? d->ld : d->n;
+  c.i_offset = d->i_offset;
+  const int64_t n_global = d->n_global > 0 ? d->n_global : d->n;
   phase_mark(kPhResid, st);
   int rc = PB_OK;
   if (d->resid_mode == PB_RESID_RECOMPUTE) {
@@ -174,15 +179,36 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
     { const char* e = getenv("PB_DICT_DEBUG"); g.dbg = e ? atoi(e) : 0; }
     g.n = d->n; g.p = d->p; g.k = d->k; g.key0 = k0; g.key1 = k1;
     g.ld = c.ld;
-    if ((rc = launch_dict_gram(g, st))) return rc;
+    if (!d->allreduce) {
+      if ((rc = launch_dict_gram(g, st))) return rc;   // fused: all passes in one persistent launch
+    } else {
+      // split (sharded) mode: per atom block, local pass -> allreduce of the
+      // 44*P moment sums across ranks -> identical atom draws on every rank
+      g.split = 1;
+      g.delta_g = ws.delta_g;
+      const int nblk = dict_gram_blocks(d->k);
+      for (int b = 0; b <= nblk; ++b) {
+        g.blk_begin = b;
+        if ((rc = launch_dict_gram(g, st))) return rc;
+        if (b == nblk) break;
+        if ((rc = d->allreduce(d->allreduce_ctx, ws.reduced, (int64_t)dict_gram_reduced_bytes(d->p) / 8, 0, st)))
+          { set_error("allreduce callback failed (%d)", rc); return PB_ECUDA; }
+        if ((rc = launch_dict_update(g, b, st))) return rc;
+      }
+    }
   }
   int nblocks = 0;
   phase_mark(kPhCode, st);
   if ((rc = launch_code_compact(c, d->rng_mode, nblocks, st))) return rc;
   phase_mark(kPhStats, st);
   if ((rc = launch_finish_stats(ws.block_sums, nblocks, sc, st))) return rc;
+  if (d->allreduce) {  // epoch statistics across ranks: sum S^2, sum R^2, usage counts m_k
+    if ((rc = d->allreduce(d->allreduce_ctx, &sc->sq_w, 2, 0, st)) ||
+        (rc = d->allreduce(d->allreduce_ctx, ws.m_count, d->k, 1, st)))
+      { set_error("allreduce callback failed (%d)", rc); return PB_ECUDA; }
+  }
   if (d->rng_mode == PB_RNG_PHILOX)
-    rc = launch_draw_pi_gamma(d->pi, ws.m_count, sc, d->k, d->n, d->n_obs, d->hyper, k0, k1, st);
+    rc = launch_draw_pi_gamma(d->pi, ws.m_count, sc, d->k, n_global, d->n_obs, d->hyper, k0, k1, st);
   phase_mark(kPhEnd, st);
   return rc;
 }
@@ -222,6 +248,16 @@ int pb_extract_patches(const pb_grid_desc* d, const void* tensor, int32_t tensor
                         (cudaStream_t)stream);
 }
 
+int pb_extract_patch_range(const pb_grid_desc* d, const void* tensor, int32_t tensor_f64, const uint8_t* mask,
+                           int32_t mean_subtract, int64_t first_patch, int64_t num_patches, float* values,
+                           uint8_t* observed, float* means, int32_t* counts, void* stream) {
+  Grid g;
+  int rc = make_grid(d, g);
+  if (rc) return rc;
+  return launch_extract(g, tensor, tensor_f64, mask, mean_subtract, values, observed, means, counts,
+                        (cudaStream_t)stream, first_patch, num_patches);
+}
+
 int pb_reconstitute(const pb_grid_desc* d, const float* est, float est_scale, const float* means,
                     const void* original, const uint8_t* mask, int32_t dc, int32_t io_f64, void* out,
                     unsigned long long* uncovered, void* stream) {
@@ -230,6 +266,14 @@ int pb_reconstitute(const pb_grid_desc* d, const float* est, float est_scale, co
   if (rc) return rc;
   return launch_reconstitute(g, est, est_scale, means, original, mask, dc, io_f64, out, uncovered,
                              (cudaStream_t)stream);
+}
+
+int pb_ola_partial(const pb_grid_desc* d, const float* est, float est_scale, const float* means, int64_t first_patch,
+                   int64_t num_patches, double* acc_out, void* stream) {
+  Grid g;
+  int rc = make_grid(d, g);
+  if (rc) return rc;
+  return launch_ola_partial(g, est, est_scale, means, first_patch, num_patches, acc_out, (cudaStream_t)stream);
 }
 
 int pb_coverage_map(const pb_grid_desc* d, int32_t* out, void* stream) {

@@ -198,7 +198,8 @@ __device__ __forceinline__ void code_atoms(const CompactArgs& a, const CodeConst
         s_new = z ? c.geps * proj / alpha + gn / sqrtf(alpha) : gn * c.inv_sqrt_gs;  // bpfa.py:265-269
       } else {
         if ((k & 1) == 0) {
-          t.rnd = philox4x32_10(u32x4{(uint32_t)c.i, (uint32_t)(c.i >> 32), (uint32_t)(k >> 1),
+          const int64_t gi = c.i + a.i_offset;  // global patch index: shards draw the 1-GPU streams
+          t.rnd = philox4x32_10(u32x4{(uint32_t)gi, (uint32_t)(gi >> 32), (uint32_t)(k >> 1),
                                       ((uint32_t)c.epoch & 0xFFFFFFu) | (kDomCode << 24)},
                                 a.key0, a.key1);
           box_muller(t.rnd.z, t.rnd.w, t.nrm0, t.nrm1);
@@ -425,6 +426,42 @@ __device__ __forceinline__ uint64_t gtimer() {
 //   most two) boundary segments go to per-warp slots merged in warp order.
 constexpr int kTbCache = 1024;  // tile bases cached in shared memory per CTA
 
+// The B sequential atom draws of one block from the reduced moments (f64):
+//   C_j += sum_{l<j} G_jl o delta_l;  lambda = P + geps*A_j;  mu = geps*(C_j + d_j*A_j)/lambda;
+//   d_j' = mu + g/sqrt(lambda)  (bpfa.py:161-166, 303-307).  Identical in every CTA/rank.
+template <int B>
+__device__ __forceinline__ void atom_block_update(const double* red, int p, int k0, int nb, double geps, int epoch,
+                                                  const double* draws, uint32_t key0, uint32_t key1,
+                                                  const float* dold, float* dprev, float* atoms_out) {
+  using L = GramLayout<B>;
+  for (int pe = threadIdx.x; pe < p; pe += blockDim.x) {
+    const double* rv = red + (size_t)pe * L::NACC;
+    for (int j = 0; j < nb; ++j) {
+      const int k = k0 + j;
+      double c = rv[j];
+      for (int l = 0; l < j; ++l) c += rv[L::gidx(j, l)] * (double)dprev[l * p + pe];
+      const double am = rv[L::gidx(j, j)];
+      const double d_o = (double)dold[j * p + pe];
+      const double lam = (double)p + geps * am;
+      const double mu = geps * (c + d_o * am) / lam;
+      double gdraw;
+      if (draws) {
+        gdraw = draws[(int64_t)k * p + pe];
+      } else {
+        const u32x4 rr = philox4x32_10(u32x4{(uint32_t)(pe >> 1), (uint32_t)k, (uint32_t)epoch, kDomAtom << 24},
+                                       key0, key1);
+        float n0, n1;
+        box_muller(rr.x, rr.y, n0, n1);
+        gdraw = (pe & 1) ? n1 : n0;
+      }
+      const float dn = (float)(mu + gdraw / sqrt(lam));
+      if (atoms_out) atoms_out[(int64_t)k * p + pe] = dn;
+      dprev[j * p + pe] = dold[j * p + pe] - dn;   // becomes the next pass's shift
+    }
+    for (int j = nb; j < B; ++j) dprev[j * p + pe] = 0.0f;
+  }
+}
+
 template <int B>
 __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
   using L = GramLayout<B>;
@@ -486,7 +523,10 @@ __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
     }
   };
 
-  for (int blk = 0; blk <= nblk; ++blk) {
+  if (a.split && a.blk_begin > 0) {  // split mode: the previous pass's shifts come from global memory
+    for (int t = threadIdx.x; t < B * p; t += blockDim.x) dprev[t] = a.delta_g[t];
+  }
+  for (int blk = a.split ? a.blk_begin : 0; blk <= (a.split ? a.blk_begin : nblk); ++blk) {
     const bool has_cur = blk < nblk, has_prev = blk > 0;
     const int k0 = blk * B;
     const int nb = has_cur ? min(B, a.k - k0) : 0;
@@ -672,43 +712,35 @@ __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
     }
     __threadfence();
     prof(4);
+    if (a.split) return;  // split mode: the caller allreduces `reduced` across ranks, then k_dict_update
     grid_sync(a.bar);
     prof(5);
     for (int t = threadIdx.x; t < nv; t += blockDim.x) red64[t] = __ldcg(a.reduced + t);
     __syncthreads();
     // sequential atom updates inside the block, identical in every CTA
-    for (int pe = threadIdx.x; pe < p; pe += blockDim.x) {
-      const double* rv = red64 + (size_t)pe * L::NACC;
-      float dnew_l[B];
-      for (int j = 0; j < nb; ++j) {
-        const int k = k0 + j;
-        double c = rv[j];
-        for (int l = 0; l < j; ++l) c += rv[L::gidx(j, l)] * (double)dprev[l * p + pe];
-        const double am = rv[L::gidx(j, j)];
-        const double d_o = (double)dold[j * p + pe];
-        const double lam = (double)p + geps * am;
-        const double mu = geps * (c + d_o * am) / lam;
-        double gdraw;
-        if (a.draws) {
-          gdraw = a.draws[(int64_t)k * p + pe];
-        } else {
-          const u32x4 rr = philox4x32_10(u32x4{(uint32_t)(pe >> 1), (uint32_t)k, (uint32_t)epoch, kDomAtom << 24},
-                                         a.key0, a.key1);
-          float n0, n1;
-          box_muller(rr.x, rr.y, n0, n1);
-          gdraw = (pe & 1) ? n1 : n0;
-        }
-        const float dn = (float)(mu + gdraw / sqrt(lam));
-        dnew_l[j] = dn;
-        dprev[j * p + pe] = dold[j * p + pe] - dn;   // becomes the next pass's shift
-      }
-      if (blockIdx.x == 0)
-        for (int j = 0; j < nb; ++j) a.atoms[(int64_t)(k0 + j) * p + pe] = dnew_l[j];
-      for (int j = nb; j < B; ++j) dprev[j * p + pe] = 0.0f;
-    }
+    atom_block_update<B>(red64, p, k0, nb, geps, epoch, a.draws, a.key0, a.key1, dold, dprev,
+                         blockIdx.x == 0 ? a.atoms : nullptr);
     __syncthreads();
     prof(6);
   }
+}
+
+// Split mode, after the cross-rank allreduce of `reduced`: the block's atom draws.
+template <int B>
+__global__ void k_dict_update(DictGramArgs a, int blk) {
+  extern __shared__ float su[];
+  float* dold = su;              // B * p
+  float* dprev = dold + B * a.p; // B * p
+  const int nb = min(B, a.k - blk * B);
+  for (int t = threadIdx.x; t < B * a.p; t += blockDim.x) {
+    const int j = t / a.p, pe = t - j * a.p;
+    dold[t] = j < nb ? a.atoms[(int64_t)(blk * B + j) * a.p + pe] : 0.0f;
+  }
+  __syncthreads();
+  atom_block_update<B>(a.reduced, a.p, blk * B, nb, a.sc->gamma_eps, a.sc->epoch + 1, a.draws, a.key0, a.key1, dold,
+                       dprev, a.atoms);
+  __syncthreads();
+  for (int t = threadIdx.x; t < B * a.p; t += blockDim.x) a.delta_g[t] = dprev[t];
 }
 
 // ---------------------------------------------------------------------------
@@ -815,6 +847,15 @@ static int launch_dict_gram_b(DictGramArgs a, cudaStream_t st) {
 }
 
 int launch_dict_gram(const DictGramArgs& a, cudaStream_t st) { return launch_dict_gram_b<8>(a, st); }
+
+int launch_dict_update(const DictGramArgs& a, int blk, cudaStream_t st) {
+  const size_t smem = (size_t)2 * 8 * a.p * 4;
+  k_dict_update<8><<<1, 256, smem, st>>>(a, blk);
+  PB_LAUNCH_CHECK();
+  return PB_OK;
+}
+
+int dict_gram_blocks(int k) { return (k + 7) / 8; }
 
 size_t dict_gram_partials_bytes(int p, int max_blocks) {
   return (size_t)max_blocks * p * GramLayout<8>::NACC * 4;

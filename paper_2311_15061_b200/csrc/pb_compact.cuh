@@ -35,6 +35,7 @@ struct CompactArgs {
   int64_t ld;           // row pitch of usage/weights (K, ld), ld >= n
   int p, k, kc;
   uint32_t key0, key1;
+  int64_t i_offset;     // global index of local patch 0 (draw counters of a shard)
 };
 
 struct DictGramArgs {
@@ -58,6 +59,11 @@ struct DictGramArgs {
   unsigned* bar;        // 2
   unsigned long long* prof;  // optional [gridDim][8] phase nanoseconds (profiling)
   int dbg;              // profiling-only: 1 skip element math, 2 skip segment reductions
+  // split (multi-rank) mode: run the single pass blk_begin and stop after the
+  // per-GPU reduction; the previous pass's shifts come from delta_g [B][P]
+  int split;
+  int blk_begin;
+  float* delta_g;
   int max_blocks;
   int wbytes;
   int64_t n;
@@ -69,6 +75,8 @@ struct DictGramArgs {
 int launch_resid_compact(const CompactArgs& a, cudaStream_t st);
 int launch_code_compact(const CompactArgs& a, int mode, int& nblocks, cudaStream_t st);
 int launch_dict_gram(const DictGramArgs& a, cudaStream_t st);
+int launch_dict_update(const DictGramArgs& a, int blk, cudaStream_t st);
+int dict_gram_blocks(int k);
 size_t dict_gram_partials_bytes(int p, int max_blocks);
 size_t dict_gram_reduced_bytes(int p);
 

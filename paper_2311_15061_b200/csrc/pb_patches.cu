@@ -52,13 +52,17 @@ static Geo4 make_geo4(const Grid& g) {
   return o;
 }
 
+// Patches [i0, i0 + cnt) of the grid (a shard; i0 = 0, cnt = N for the whole
+// matrix) into a (P, cnt) plane-major patch matrix.
 template <typename T>
 __global__ void __launch_bounds__(256) k_extract(Geo4 g, const T* __restrict__ tensor,
                                                  const uint8_t* __restrict__ mask, int mean_subtract,
                                                  float* __restrict__ values, uint8_t* __restrict__ obs,
-                                                 float* __restrict__ means, int32_t* __restrict__ counts) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n;
-       i += (int64_t)gridDim.x * blockDim.x) {
+                                                 float* __restrict__ means, int32_t* __restrict__ counts, int64_t i0,
+                                                 int64_t cnt_patches) {
+  for (int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; li < cnt_patches;
+       li += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + li;
     int64_t base = 0, rem = i;
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
@@ -78,15 +82,15 @@ __global__ void __launch_bounds__(256) k_extract(Geo4 g, const T* __restrict__ t
       }
     }
     const double mean = (mean_subtract && cnt > 0) ? sum / (double)cnt : 0.0;
-    means[i] = (float)mean;
-    counts[i] = cnt;
+    means[li] = (float)mean;
+    counts[li] = cnt;
     // pass 2: plane-major write
     int q0 = 0, q1 = 0, q2 = 0, q3 = 0;
     for (int p = 0; p < g.p; ++p) {
       const int64_t off = base + q0 * g.tstride[0] + q1 * g.tstride[1] + q2 * g.tstride[2] + q3 * g.tstride[3];
       const uint8_t o = mask[off] ? 1 : 0;
-      values[(int64_t)p * g.n + i] = o ? (float)((double)tensor[off] - mean) : 0.0f;
-      obs[(int64_t)p * g.n + i] = o;
+      values[(int64_t)p * cnt_patches + li] = o ? (float)((double)tensor[off] - mean) : 0.0f;
+      obs[(int64_t)p * cnt_patches + li] = o;
       if (++q3 == g.bshape[3]) { q3 = 0; if (++q2 == g.bshape[2]) { q2 = 0; if (++q1 == g.bshape[1]) { q1 = 0; ++q0; } } }
     }
   }
@@ -136,6 +140,36 @@ __global__ void __launch_bounds__(256) k_reconstitute(Geo4 g, const float* __res
   }
 }
 
+// Shard of the overlap-add: raw sums (no division) of the covering patches in
+// [i0, i0 + cnt), est/means indexed shard-locally; the caller allreduces the
+// sums across ranks and divides by the (analytic, global) coverage.
+__global__ void __launch_bounds__(256) k_ola_partial(Geo4 g, const float* __restrict__ est, float est_scale,
+                                                     const float* __restrict__ means, int64_t i0, int64_t cnt,
+                                                     double* __restrict__ acc_out) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < g.m;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c[4], lo[4], hi[4], rem = x;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      c[d] = rem / g.tstride[d];
+      rem -= c[d] * g.tstride[d];
+      cover_range(c[d], g.bshape[d], g.step[d], g.gcount[d], lo[d], hi[d]);
+    }
+    double acc = 0.0;
+    for (int64_t a0 = lo[0]; a0 <= hi[0]; ++a0)
+      for (int64_t a1 = lo[1]; a1 <= hi[1]; ++a1)
+        for (int64_t a2 = lo[2]; a2 <= hi[2]; ++a2)
+          for (int64_t a3 = lo[3]; a3 <= hi[3]; ++a3) {
+            const int64_t i = a0 * g.gstride[0] + a1 * g.gstride[1] + a2 * g.gstride[2] + a3 * g.gstride[3];
+            if (i < i0 || i >= i0 + cnt) continue;
+            const int64_t p = (c[0] - a0 * g.step[0]) * g.bstride[0] + (c[1] - a1 * g.step[1]) * g.bstride[1] +
+                              (c[2] - a2 * g.step[2]) * g.bstride[2] + (c[3] - a3 * g.step[3]) * g.bstride[3];
+            acc += (double)est[p * cnt + (i - i0)] * (double)est_scale + (double)means[i - i0];
+          }
+    acc_out[x] = acc;
+  }
+}
+
 __global__ void k_coverage(Geo4 g, int32_t* __restrict__ out) {
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < g.m;
        x += (int64_t)gridDim.x * blockDim.x) {
@@ -162,14 +196,19 @@ static int grid_blocks(int64_t work, int threads) {
 }
 
 int launch_extract(const Grid& grid, const void* tensor, int f64, const uint8_t* mask, int mean_subtract,
-                   float* values, uint8_t* obs, float* means, int32_t* counts, cudaStream_t st) {
+                   float* values, uint8_t* obs, float* means, int32_t* counts, cudaStream_t st, int64_t i0,
+                   int64_t cnt) {
   const Geo4 g = make_geo4(grid);
+  if (cnt < 0) cnt = g.n - i0;
+  if (i0 < 0 || i0 + cnt > g.n) { set_error("patch range [%lld, %lld) outside the grid", (long long)i0, (long long)(i0 + cnt)); return PB_ESHAPE; }
   const int th = 256;
-  const int nb = grid_blocks(g.n, th);
+  const int nb = grid_blocks(cnt, th);
   if (f64)
-    k_extract<double><<<nb, th, 0, st>>>(g, (const double*)tensor, mask, mean_subtract, values, obs, means, counts);
+    k_extract<double><<<nb, th, 0, st>>>(g, (const double*)tensor, mask, mean_subtract, values, obs, means, counts, i0,
+                                         cnt);
   else
-    k_extract<float><<<nb, th, 0, st>>>(g, (const float*)tensor, mask, mean_subtract, values, obs, means, counts);
+    k_extract<float><<<nb, th, 0, st>>>(g, (const float*)tensor, mask, mean_subtract, values, obs, means, counts, i0,
+                                        cnt);
   PB_LAUNCH_CHECK();
   return PB_OK;
 }
@@ -186,6 +225,14 @@ int launch_reconstitute(const Grid& grid, const float* est, float est_scale, con
   else
     k_reconstitute<float><<<nb, th, 0, st>>>(g, est, est_scale, means, (const float*)original, mask, dc,
                                              (float*)out, uncovered);
+  PB_LAUNCH_CHECK();
+  return PB_OK;
+}
+
+int launch_ola_partial(const Grid& grid, const float* est, float est_scale, const float* means, int64_t i0,
+                       int64_t cnt, double* acc_out, cudaStream_t st) {
+  const Geo4 g = make_geo4(grid);
+  k_ola_partial<<<grid_blocks(g.m, 256), 256, 0, st>>>(g, est, est_scale, means, i0, cnt, acc_out);
   PB_LAUNCH_CHECK();
   return PB_OK;
 }

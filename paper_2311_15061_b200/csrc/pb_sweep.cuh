@@ -18,10 +18,12 @@ static_assert(sizeof(SweepScalars) == 40, "SweepScalars must match pb_scalars");
 
 // pb_patches.cu
 int launch_extract(const Grid&, const void*, int, const uint8_t*, int, float*, uint8_t*, float*, int32_t*,
-                   cudaStream_t);
+                   cudaStream_t, int64_t i0 = 0, int64_t cnt = -1);
 int launch_reconstitute(const Grid&, const float*, float, const float*, const void*, const uint8_t*, int, int, void*,
                         unsigned long long*, cudaStream_t);
 int launch_coverage(const Grid&, int32_t*, cudaStream_t);
+int launch_ola_partial(const Grid&, const float* est, float est_scale, const float* means, int64_t i0, int64_t cnt,
+                       double* acc_out, cudaStream_t st);
 // pb_sweep.cu
 int launch_accumulate_atoms(bool resid, const float* values, const uint8_t* obs, const uint8_t* usage,
                             const float* weights, const float* atoms, float* out, int64_t n, int p, int k_len,
