@@ -233,13 +233,25 @@ def run_gpu_arm(args):
     world, rank, local = dist_setup(args)
     lib = _lib.load()
     img, mask = workload_inputs(CFG)
-    pm = pp.extract_patches(img, mask, pp.PatchSpec(CFG["patch"]), True)
     hp = gb.Hyperparams(num_atoms=CFG["k"])
+    if world > 1:
+        # one frame sharded across the ranks (strong scaling): contiguous patch
+        # ranges, D replicated, per-atom-block moment allreduce over NCCL
+        from paper_2311_15061_b200 import parallel as par
+
+        comm = par.TorchCollective()
+        pm = par.extract_patch_shard(img, mask, pp.PatchSpec(CFG["patch"]), True, comm)
+        sweep = lambda st: par.gibbs_epoch_sharded(st, pm, hp, comm, check=False)  # noqa: E731
+        n_units = pm.n_global
+    else:
+        pm = pp.extract_patches(img, mask, pp.PatchSpec(CFG["patch"]), True)
+        sweep = lambda st: gb.gibbs_epoch(st, pm, hp, rng="philox", check=False)  # noqa: E731
+        n_units = pm.num_patches
     n, k, p = pm.num_patches, CFG["k"], pm.patch_size
-    st = gb.init_state(pm, hp, CFG["seed"] + rank, "prior")
+    st = gb.init_state(pm, hp, CFG["seed"], "prior")
     clk = ClockSampler(local).__enter__()
     for _ in range(args.warmup):
-        gb.gibbs_epoch(st, pm, hp, rng="philox", check=False)
+        sweep(st)
     torch.cuda.synchronize()
     lib.pb_phase_timing(1)
     stream = torch.cuda.current_stream()
@@ -249,7 +261,7 @@ def run_gpu_arm(args):
     t_start = time.monotonic()
     e0.record(stream)
     for _ in range(args.steps):
-        gb.gibbs_epoch(st, pm, hp, rng="philox", check=False)
+        sweep(st)
     e1.record(stream)
     torch.cuda.synchronize()
     clk.mark(t_start, time.monotonic())
@@ -263,7 +275,7 @@ def run_gpu_arm(args):
     lib.pb_phase_timing(0)
     if st._sc().diverged:
         raise SystemExit("diverged")
-    value = world * n * k * args.steps / (ms * 1e-3)
+    value = n_units * k * args.steps / (ms * 1e-3)   # whole-job updates/s (the frame's N*K per sweep)
 
     # --- roofline of the dominant kernel ------------------------------------
     names = ["k_resid_compact (residual / carry)", "k_dict_gram (dictionary step)", "k_code_compact (code step)",
@@ -295,7 +307,10 @@ def run_gpu_arm(args):
 
     # --- quality of the device result after the timed sweeps ----------------
     est = gb.compose_estimates(st)
-    rec = pp.reconstitute(pm, est, dc_original=img, dc_mask=mask)
+    if world > 1:
+        rec = np.where(mask, img, par.reconstitute_sharded(pm, est, comm))
+    else:
+        rec = pp.reconstitute(pm, est, dc_original=img, dc_mask=mask)
     quality = {"psnr_db": psnr(rec, img), "ssim": ssim(rec, img), "epochs": args.warmup + args.steps}
 
     # --- e2e through the C ABI with host buffers ----------------------------
@@ -303,19 +318,29 @@ def run_gpu_arm(args):
     frame_h = torch.from_numpy(img).pin_memory()
     mask_h = torch.from_numpy(mask.astype(np.uint8)).pin_memory()
     out_h = torch.empty(img.shape, dtype=torch.float64).pin_memory()
-    pr = ctypes.c_void_p()
-    _lib.check(lib.pb_problem_create(ctypes.byref(problem_desc(CFG, CFG["epochs"], warm=False, dc=True)),
-                                     ctypes.byref(pr)))
-    _lib.check(lib.pb_problem_submit_frame(pr, frame_h.data_ptr(), mask_h.data_ptr(), out_h.data_ptr()))  # warm
+    if world == 1:
+        pr = ctypes.c_void_p()
+        _lib.check(lib.pb_problem_create(ctypes.byref(problem_desc(CFG, CFG["epochs"], warm=False, dc=True)),
+                                         ctypes.byref(pr)))
+        run_e2e = lambda: _lib.check(lib.pb_problem_submit_frame(  # noqa: E731
+            pr, frame_h.data_ptr(), mask_h.data_ptr(), out_h.data_ptr()))
+    else:
+        def run_e2e():  # sharded public API: host frame -> shards -> infer -> allreduced OLA -> host
+            pms = par.extract_patch_shard(frame_h, mask_h, pp.PatchSpec(CFG["patch"]), True, comm)
+            _, est_s = par.infer_sharded(pms, hp, CFG["epochs"], CFG["seed"], comm)
+            rec = par.reconstitute_sharded(pms, est_s, comm)
+            out_h.copy_(torch.from_numpy(np.where(mask, img, rec)))
+    run_e2e()  # warm
     barrier(world)
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        _lib.check(lib.pb_problem_submit_frame(pr, frame_h.data_ptr(), mask_h.data_ptr(), out_h.data_ptr()))
+        run_e2e()
     e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps, world)
     barrier(world)
     e2e_psnr = psnr(out_h.numpy(), img)
-    lib.pb_problem_destroy(pr)
-    e2e = {"value": world * n * k * CFG["epochs"] / e2e_s, "unit": "updates/s",
+    if world == 1:
+        lib.pb_problem_destroy(pr)
+    e2e = {"value": n_units * k * CFG["epochs"] / e2e_s, "unit": "updates/s",
            "h2d_bytes_per_step": img.nbytes + mask.size, "d2h_bytes_per_step": img.nbytes,
            "s_per_step": e2e_s, "step": f"one cold inpaint: {CFG['epochs']} epochs, host frame -> host recon",
            "psnr_db": e2e_psnr}
@@ -342,23 +367,27 @@ def run_gpu_arm(args):
     live = {"frames_per_s": 1.0 / live_s, "ms_per_frame": 1e3 * live_s,
             "gpu_ms_per_frame": statistics.median(gpu_ms), "frames": len(fh[2:]),
             "psnr_db_last_frame": psnr(lo.numpy(), frames[-1]),
-            "config": "configs[2]: 512x512 synthetic frames, 25% line-hop, 8x8, K=256, 2 warm-started epochs/frame",
+            "config": "configs[2]: 512x512 synthetic frames, 25% line-hop, 8x8, K=256, 2 warm-started epochs/frame"
+                      + (" (per rank; ranks run independent streams)" if world > 1 else ""),
             "target_fps": 30}
     lib.pb_problem_destroy(lpr)
 
     line = {
         "metric": "BPFA patch-atom updates/sec", "value": value, "unit": "updates/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "configs[1]: 1024x1024 synthetic STEM-like frame, 10% uniform sampling, "
                                "10x10 patches stride 1, K=256; step = one full Gibbs sweep",
-                   "global_batch": world * n, "seq_len": 1, "parallelism": f"replicas{world}",
+                   "global_batch": n_units, "seq_len": 1,
+                   "parallelism": f"patch-shards{world} (NCCL allreduce per 8-atom block)" if world > 1 else "single",
                    "patches": n, "atoms": k, "patch_size": p, "observed_per_patch": obs_per_patch,
                    "rng": "philox (device)",
                    "l2": f"inputs larger than L2: values {n * p * 4 / 1e6:.0f} MB + Z/S state "
                          f"{n * k * 5 / 1e6:.0f} MB per rank"},
         "clocks": clk.summary(),
-        "gpu_launches": 5 * args.steps,
+        # per sweep: k_dict_gram, k_code_compact, k_finish_stats, k_draw_pi_gamma (residual carried);
+        # sharded: k_dict_gram per atom block + 1, k_dict_update per block
+        "gpu_launches": (4 if world == 1 else 2 * ((k + 7) // 8) + 4) * args.steps,
         "e2e": e2e, "live": live, "quality": quality, "roofline": roofline,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
