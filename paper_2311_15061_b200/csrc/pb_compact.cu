@@ -130,16 +130,14 @@ __global__ void __launch_bounds__(256) k_resid_compact(CompactArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Code step.  Per-thread loop state kept in registers across the atom loop.
-struct CodeThread {
-  double sq_w;
-  u32x4 rnd;
-  float nrm0, nrm1;
-  float sn;
-  uint8_t zn;
-  double un, gnx;
-};
-
+// Code step (bpfa.py:240-275, atoms k = 0..K-1 in order, one patch per G-lane
+// group).  D is staged in shared memory TRANSPOSED, DT[p][k] with row pitch KP =
+// kc + 2 floats (KP/2 odd, so 8-byte loads from random rows spread over the
+// banks; row P is all zero and backs the padded register slots).  One 8-byte load
+// per slot then serves an atom PAIR, and one Philox4x32-10 block per pair gives
+// both uniforms (x, y) and a Box-Muller normal pair (z, w); counter = (global
+// patch, k/2, epoch | domain).  The kernel is persistent: D is staged once per
+// CTA and the CTA walks patch blocks of blockDim/G.
 struct CodeConst {
   int64_t i, ic;
   bool live;
@@ -147,109 +145,206 @@ struct CodeConst {
   float geps, gs, inv_sqrt_gs;
   const float* logit;
   int* mcnt;
-  float* wwin;
+  float* wrow;  // this patch's 8-atom window of w (pitch 9, lane g == 0 only)
 };
 
-// Atoms [k0, k0+kn) for one patch with W live register slots (slots >= W are
-// padding for the whole warp; padded slots inside W read the zero column).
+struct CodeThread {
+  double sq_w;
+  float sq_w8;  // philox mode: sum S^2 over the current 8-atom group
+};
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// Box-Muller pair with the MUFU approximations (|err| ~ 1e-6, far below the
+// sampler's statistical resolution).
+__device__ __forceinline__ void box_muller_fast(uint32_t a, uint32_t b, float& n0, float& n1) {
+  const float u1 = fmaf((float)a, 2.3283064365386963e-10f, 1.1641532182693481e-10f);
+  const float rr = sqrt_approx(-1.3862943611198906f * lg2_approx(u1));  // sqrt(-2 ln u1)
+  const float th = 6.283185307179586f * u01_24(b);
+  float s, c;
+  asm("sin.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(th));
+  asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(th));
+  n0 = rr * c;
+  n1 = rr * s;
+}
+
+// One atom of the code step for this patch: moments u = |d|^2_obs, v = <d, r>_obs
+// (_kernels.code_moments), the z/s draw (_code_params, bpfa.py:169-178 and
+// 262-269), the residual shift (_kernels.shift_codes) and the state write.
 template <int CMAX, int W, int G, int MODE>
-__device__ __forceinline__ void code_atoms(const CompactArgs& a, const CodeConst& c, int k0, int kn, const float* ds,
-                                           int pp, float (&r)[CMAX], const int (&off)[CMAX], CodeThread& t) {
-  for (int kk = 0; kk < kn; ++kk) {
-    const int k = k0 + kk;
-    const float* d = ds + kk * pp;
-    const bool z_old = t.zn != 0;
-    const float s_old = t.sn;
-    const double ud = t.un, gd = t.gnx;
-    if (k + 1 < a.k) {  // 1-deep prefetch of the next atom's code and replay draws
-      const int64_t zn_i = (int64_t)(k + 1) * a.ld + c.ic;
-      t.zn = a.usage[zn_i];
-      t.sn = a.weights[zn_i];
-      if (MODE == kRngReplay) {
-        const int64_t dn_i = (int64_t)(k + 1) * a.n + c.ic;
-        t.un = a.u_draw[dn_i];
-        t.gnx = a.g_draw[dn_i];
-      }
-    }
-    float dj[W];
-    float u = 0.0f, v = 0.0f;
+__device__ __forceinline__ void code_one(const CompactArgs& a, const CodeConst& c, CodeThread& t, int k, int64_t zo,
+                                         const float (&d)[W], float (&r)[CMAX], uint8_t z_old8, float s_old, float uu,
+                                         float gn, double ud, double gd) {
+  float u = 0.0f, v = 0.0f;
 #pragma unroll
-    for (int j = 0; j < W; ++j) {
-      dj[j] = d[off[j]];
-      u = fmaf(dj[j], dj[j], u);
-      v = fmaf(dj[j], r[j], v);
-    }
-    if (G > 1) {
-      u = gsum<G>(u);
-      v = gsum<G>(v);
-    }
-    bool z = false;
-    if (c.live) {
-      const int64_t zi = (int64_t)k * a.ld + c.i;
-      const float w_old = z_old ? s_old : 0.0f;
-      // _code_params (bpfa.py:169-178)
-      const float proj = fmaf(w_old, u, v);
-      const float log_rho = c.logit[k] - 0.5f * c.geps * (s_old * s_old * u - 2.0f * s_old * proj);
-      const float alpha = fmaf(c.geps, u, c.gs);
-      float s_new;
+  for (int j = 0; j < W; ++j) {
+    u = fmaf(d[j], d[j], u);
+    v = fmaf(d[j], r[j], v);
+  }
+  if (G > 1) {
+    u = gsum<G>(u);
+    v = gsum<G>(v);
+  }
+  const float w_old = z_old8 ? s_old : 0.0f;
+  const float proj = fmaf(w_old, u, v);
+  const float log_rho = c.logit[k] - 0.5f * c.geps * (s_old * s_old * u - 2.0f * s_old * proj);
+  const float alpha = fmaf(c.geps, u, c.gs);
+  bool z;
+  float s_new;
+  if (MODE == kRngReplay) {
+    z = (log(ud) - log1p(-ud)) < (double)log_rho;  // bpfa.py:262-263
+    const float g = (float)gd;
+    s_new = z ? c.geps * proj / alpha + g / sqrtf(alpha) : g * c.inv_sqrt_gs;  // bpfa.py:265-269
+  } else {
+    z = uu * (1.0f + ex2_approx(-1.4426950408889634f * log_rho)) < 1.0f;  // U < sigmoid(log_rho)
+    const float ra = rsqrt_approx(alpha);
+    s_new = z ? fmaf(c.geps * proj, ra * ra, gn * ra) : gn * c.inv_sqrt_gs;
+  }
+  const float w_new = z ? s_new : 0.0f;
+  const float dw = w_old - w_new;
+#pragma unroll
+  for (int j = 0; j < W; ++j) r[j] = fmaf(dw, d[j], r[j]);
+  const bool own = c.live && c.g == 0;
+  if (own) {
+    a.usage[zo] = z ? 1 : 0;
+    a.weights[zo] = s_new;
+    if (MODE == kRngReplay) t.sq_w += (double)s_new * (double)s_new;
+    else t.sq_w8 = fmaf(s_new, s_new, t.sq_w8);
+    c.wrow[k & 7] = w_new;
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, z && own);
+  if (c.lane == 0 && bal) atomicAdd(&c.mcnt[k], __popc(bal));
+}
+
+// Atoms [k0, k1) (k0 a multiple of 8) against the staged DT whose column 0 is
+// atom kc0.  W = live register slots of this warp (compile time).
+template <int CMAX, int W, int G, int MODE>
+__device__ __forceinline__ void code_atoms(const CompactArgs& a, const CodeConst& c, CodeThread& t, int k0, int k1,
+                                           int kc0, const float* dt, float (&r)[CMAX], const int (&addr)[CMAX]) {
+  constexpr bool kPair = W <= 16;  // register budget: 2W values of D per pair
+  int64_t zo = (int64_t)k0 * a.ld + c.ic;
+  uint8_t za = a.usage[zo], zb = 0;
+  float sa = a.weights[zo], sb = 0.0f;
+  if (k0 + 1 < a.k) { zb = a.usage[zo + a.ld]; sb = a.weights[zo + a.ld]; }
+  for (int kg = k0; kg < k1; kg += 8) {
+#pragma unroll 1
+    for (int q = 0; q < 8; q += 2) {
+      const int k = kg + q;
+      if (k >= k1) break;
+      // prefetch the next pair's state
+      uint8_t zna = 0, znb = 0;
+      float sna = 0.0f, snb = 0.0f;
+      if (k + 2 < a.k) { zna = a.usage[zo + 2 * a.ld]; sna = a.weights[zo + 2 * a.ld]; }
+      if (k + 3 < a.k) { znb = a.usage[zo + 3 * a.ld]; snb = a.weights[zo + 3 * a.ld]; }
+      float uu0 = 0.f, uu1 = 0.f, g0 = 0.f, g1 = 0.f;
+      double ud0 = 0.0, ud1 = 0.0, gd0 = 0.0, gd1 = 0.0;
       if (MODE == kRngReplay) {
-        z = (log(ud) - log1p(-ud)) < (double)log_rho;  // bpfa.py:262-263
-        const float gn = (float)gd;
-        s_new = z ? c.geps * proj / alpha + gn / sqrtf(alpha) : gn * c.inv_sqrt_gs;  // bpfa.py:265-269
+        const int64_t di = (int64_t)k * a.n + c.ic;
+        ud0 = a.u_draw[di];
+        gd0 = a.g_draw[di];
+        if (k + 1 < k1) { ud1 = a.u_draw[di + a.n]; gd1 = a.g_draw[di + a.n]; }
       } else {
-        if ((k & 1) == 0) {
-          const int64_t gi = c.i + a.i_offset;  // global patch index: shards draw the 1-GPU streams
-          t.rnd = philox4x32_10(u32x4{(uint32_t)gi, (uint32_t)(gi >> 32), (uint32_t)(k >> 1),
-                                      ((uint32_t)c.epoch & 0xFFFFFFu) | (kDomCode << 24)},
-                                a.key0, a.key1);
-          box_muller(t.rnd.z, t.rnd.w, t.nrm0, t.nrm1);
-        }
-        const float uu = u01_24((k & 1) ? t.rnd.y : t.rnd.x);
-        const float gn = (k & 1) ? t.nrm1 : t.nrm0;
-        z = uu * (1.0f + __expf(-log_rho)) < 1.0f;  // U < sigmoid(log_rho)
-        const float ra = rsqrtf(alpha);
-        s_new = z ? fmaf(c.geps * proj, ra * ra, gn * ra) : gn * c.inv_sqrt_gs;
+        const int64_t gi = c.i + a.i_offset;  // global patch index: shards draw the 1-GPU streams
+        const u32x4 rnd = philox4x32_10(u32x4{(uint32_t)gi, (uint32_t)(gi >> 32), (uint32_t)(k >> 1),
+                                              ((uint32_t)c.epoch & 0xFFFFFFu) | (kDomCode << 24)},
+                                        a.key0, a.key1);
+        box_muller_fast(rnd.z, rnd.w, g0, g1);
+        uu0 = u01_24(rnd.x);
+        uu1 = u01_24(rnd.y);
       }
-      const float w_new = z ? s_new : 0.0f;
-      const float dw = w_old - w_new;
+      const char* col = (const char*)dt + (size_t)(k - kc0) * 4;
+      if (kPair) {
+        float d0[W], d1[W];
 #pragma unroll
-      for (int j = 0; j < W; ++j) r[j] = fmaf(dw, dj[j], r[j]);
-      if (c.g == 0) {
-        a.usage[zi] = z ? 1 : 0;
-        a.weights[zi] = s_new;
-        t.sq_w += (double)s_new * (double)s_new;
-        // 8-atom window of w (shared memory, pitch 9: conflict-free) for the
-        // tile-blocked copy the dictionary step bulk-loads
-        float* wrow = c.wwin + (threadIdx.x / G) * 9;
-        wrow[k & 7] = w_new;
-        if ((k & 7) == 7 || k == a.k - 1) {
-          for (int q = (k & 7) + 1; q < 8; ++q) wrow[q] = 0.0f;  // partial last block
-          float* blk = a.wt + ((c.i / kTile) * a.nblk8 + (k >> 3)) * kTile * kWB;
-          const int il = (int)(c.i % kTile);
-          *(float4*)(blk + wsw(il, 0)) = make_float4(wrow[0], wrow[1], wrow[2], wrow[3]);
-          *(float4*)(blk + wsw(il, 1)) = make_float4(wrow[4], wrow[5], wrow[6], wrow[7]);
+        for (int j = 0; j < W; ++j) {
+          const float2 dd = *(const float2*)(col + addr[j]);
+          d0[j] = dd.x;
+          d1[j] = dd.y;
+        }
+        code_one<CMAX, W, G, MODE>(a, c, t, k, zo, d0, r, za, sa, uu0, g0, ud0, gd0);
+        if (k + 1 < k1) code_one<CMAX, W, G, MODE>(a, c, t, k + 1, zo + a.ld, d1, r, zb, sb, uu1, g1, ud1, gd1);
+      } else {
+        float d0[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) d0[j] = *(const float*)(col + addr[j]);
+        code_one<CMAX, W, G, MODE>(a, c, t, k, zo, d0, r, za, sa, uu0, g0, ud0, gd0);
+        if (k + 1 < k1) {
+#pragma unroll
+          for (int j = 0; j < W; ++j) d0[j] = *(const float*)(col + 4 + addr[j]);
+          code_one<CMAX, W, G, MODE>(a, c, t, k + 1, zo + a.ld, d0, r, zb, sb, uu1, g1, ud1, gd1);
         }
       }
+      za = zna; zb = znb; sa = sna; sb = snb;
+      zo += 2 * a.ld;
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, z && c.g == 0);
-    if (c.lane == 0 && bal) atomicAdd(&c.mcnt[k], __popc(bal));
+    // group done: the tile-blocked copy of w for the dictionary step, sum S^2
+    if (c.live && c.g == 0) {
+      if (MODE != kRngReplay) { t.sq_w += (double)t.sq_w8; t.sq_w8 = 0.0f; }
+      float* wrow = c.wrow;
+      for (int q = k1 - kg; q < 8; ++q) wrow[q] = 0.0f;  // partial last group
+      float* blk = a.wt + ((c.i / kTile) * a.nblk8 + (kg >> 3)) * kTile * kWB;
+      const int il = (int)(c.i % kTile);
+      *(float4*)(blk + wsw(il, 0)) = make_float4(wrow[0], wrow[1], wrow[2], wrow[3]);
+      *(float4*)(blk + wsw(il, 1)) = make_float4(wrow[4], wrow[5], wrow[6], wrow[7]);
+    }
+  }
+}
+
+// Stage atoms [k0, k0+kn) transposed into DT (pitch kp, P+1 rows, zero row P and
+// zero pad columns).  Coalesced global reads along p.
+__device__ __forceinline__ void stage_atoms_t(float* dt, const float* __restrict__ atoms, int k0, int kn, int p,
+                                              int kp) {
+  for (int t = threadIdx.x; t < (p + 1) * kp; t += blockDim.x) {
+    const int kk = t / (p + 1), pe = t - kk * (p + 1);
+    dt[pe * kp + kk] = (pe < p && kk < kn) ? atoms[(int64_t)(k0 + kk) * p + pe] : 0.0f;
+  }
+}
+
+template <int CMAX, int W, int G, int MODE>
+__device__ __forceinline__ void code_patch_range(const CompactArgs& a, const CodeConst& c, CodeThread& t, float* dt,
+                                                 int kp, float (&r)[CMAX], const int (&addr)[CMAX]) {
+  if (a.kc >= a.k) {
+    code_atoms<CMAX, W, G, MODE>(a, c, t, 0, a.k, 0, dt, r, addr);
+  } else {
+    for (int k0 = 0; k0 < a.k; k0 += a.kc) {
+      const int kn = min(a.kc, a.k - k0);
+      __syncthreads();
+      stage_atoms_t(dt, a.atoms, k0, kn, a.p, kp);
+      __syncthreads();
+      code_atoms<CMAX, W, G, MODE>(a, c, t, k0, k0 + kn, k0, dt, r, addr);
+    }
   }
 }
 
 template <int CMAX, int G, int MODE>
 __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
-  extern __shared__ float sm[];
-  const int pp = a.p + 1;
-  float* logit = sm;                     // K
-  int* mcnt = (int*)(logit + a.k);       // K
-  float* wwin = (float*)(mcnt + a.k);    // (blockDim / G) * 9
-  float* ds = wwin + (blockDim.x / G) * 9;  // kc * pp
+  extern __shared__ __align__(16) float sm[];
+  const int kp = a.kc + 2;                     // DT row pitch (kc % 8 == 0  =>  kp/2 odd)
+  float* dt = sm;                              // (P+1) * kp
+  float* logit = dt + (size_t)(a.p + 1) * kp;  // K
+  int* mcnt = (int*)(logit + a.k);             // K
+  float* wwin = (float*)(mcnt + a.k);          // (blockDim / G) * 9
   __shared__ double red[32];
   CodeConst c;
   c.g = threadIdx.x % G;
-  c.i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
-  c.live = c.i < a.n;
-  c.ic = c.live ? c.i : 0;
   c.lane = threadIdx.x & 31;
   c.epoch = a.sc->epoch + 1;
   c.geps = (float)a.sc->gamma_eps;
@@ -257,66 +352,56 @@ __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
   c.inv_sqrt_gs = (float)(1.0 / sqrt(a.sc->gamma_s));
   c.logit = logit;
   c.mcnt = mcnt;
-  c.wwin = wwin;
-
+  c.wrow = wwin + (threadIdx.x / G) * 9;
   for (int k = threadIdx.x; k < a.k; k += blockDim.x) {
     const double pk = fmin(fmax(a.pi[k], 1e-15), 1.0 - 1e-15);  // bpfa.py:173
     logit[k] = (float)(log(pk) - log1p(-pk));
     mcnt[k] = 0;
   }
-  float r[CMAX];
-  int off[CMAX];
-  int cnt = 0;
-  int64_t r0 = 0;
-  if (c.live) { cnt = a.counts[c.i]; r0 = a.rowptr[c.i]; }
-  const int wmax = __reduce_max_sync(0xffffffffu, lane_slots<G>(cnt, c.g));
-#pragma unroll
-  for (int j = 0; j < CMAX; ++j) {
-    off[j] = a.p;
-    r[j] = 0.0f;
-    if (j < wmax) {
-      const int s = j * G + c.g;
-      if (s < cnt) {
-        off[j] = a.csr_p[r0 + s];
-        r[j] = a.r_csc[a.csr_pos[r0 + s]];
-      }
-    }
-  }
+  if (a.kc >= a.k) stage_atoms_t(dt, a.atoms, 0, a.k, a.p, kp);
+  __syncthreads();
+  const int row_bytes = kp * 4;
   CodeThread t;
   t.sq_w = 0.0;
-  t.rnd = u32x4{0, 0, 0, 0};
-  t.nrm0 = t.nrm1 = 0.f;
-  t.zn = a.usage[c.ic];
-  t.sn = a.weights[c.ic];
-  t.un = t.gnx = 0.0;
-  if (MODE == kRngReplay) { t.un = a.u_draw[c.ic]; t.gnx = a.g_draw[c.ic]; }
-  if (a.kc >= a.k) {
-    // whole dictionary resident: stage once, then run the atom loop with the
-    // warp's live slot count as a compile-time constant (no padded-slot work)
-    __syncthreads();
-    stage_atoms(ds, a.atoms, 0, a.k, a.p, pp);
-    __syncthreads();
-    const int wc = (wmax + 7) & ~7;
-    if (wc <= 8 || CMAX == 8) code_atoms<CMAX, (CMAX < 8 ? CMAX : 8), G, MODE>(a, c, 0, a.k, ds, pp, r, off, t);
-    else if (wc <= 16 || CMAX == 16) code_atoms<CMAX, (CMAX < 16 ? CMAX : 16), G, MODE>(a, c, 0, a.k, ds, pp, r, off, t);
-    else if (wc <= 24 || CMAX == 24) code_atoms<CMAX, (CMAX < 24 ? CMAX : 24), G, MODE>(a, c, 0, a.k, ds, pp, r, off, t);
-    else code_atoms<CMAX, CMAX, G, MODE>(a, c, 0, a.k, ds, pp, r, off, t);
-  } else {
-    for (int k0 = 0; k0 < a.k; k0 += a.kc) {
-      const int kn = min(a.kc, a.k - k0);
-      __syncthreads();
-      stage_atoms(ds, a.atoms, k0, kn, a.p, pp);
-      __syncthreads();
-      code_atoms<CMAX, CMAX, G, MODE>(a, c, k0, kn, ds, pp, r, off, t);
-    }
-  }
+  t.sq_w8 = 0.0f;
   double sq_r = 0.0;
+  const int per_blk = blockDim.x / G;
+  const int64_t nblk = ceil_div(a.n, per_blk);
+  for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
+    c.i = b * per_blk + threadIdx.x / G;
+    c.live = c.i < a.n;
+    c.ic = c.live ? c.i : 0;
+    float r[CMAX];
+    int addr[CMAX];
+    int cnt = 0;
+    int64_t r0 = 0;
+    if (c.live) { cnt = a.counts[c.i]; r0 = a.rowptr[c.i]; }
+    const int wmax = __reduce_max_sync(0xffffffffu, lane_slots<G>(cnt, c.g));
 #pragma unroll
-  for (int j = 0; j < CMAX; ++j) {
-    sq_r += (double)r[j] * (double)r[j];
-    // the end-of-sweep residual is the next epoch's starting residual (carry mode)
-    const int s = j * G + c.g;
-    if (c.live && j < wmax && s < cnt) a.r_csc[a.csr_pos[r0 + s]] = r[j];
+    for (int j = 0; j < CMAX; ++j) {
+      addr[j] = a.p * row_bytes;
+      r[j] = 0.0f;
+      if (j < wmax) {
+        const int s = j * G + c.g;
+        if (s < cnt) {
+          addr[j] = (int)a.csr_p[r0 + s] * row_bytes;
+          r[j] = a.r_csc[a.csr_pos[r0 + s]];
+        }
+      }
+    }
+    // the warp's live slot count as a compile-time constant (no padded-slot work)
+    const int wc = (wmax + 7) & ~7;
+    if (wc <= 8 || CMAX == 8) code_patch_range<CMAX, (CMAX < 8 ? CMAX : 8), G, MODE>(a, c, t, dt, kp, r, addr);
+    else if (wc <= 16 || CMAX == 16) code_patch_range<CMAX, (CMAX < 16 ? CMAX : 16), G, MODE>(a, c, t, dt, kp, r, addr);
+    else if (wc <= 24 || CMAX == 24) code_patch_range<CMAX, (CMAX < 24 ? CMAX : 24), G, MODE>(a, c, t, dt, kp, r, addr);
+    else code_patch_range<CMAX, CMAX, G, MODE>(a, c, t, dt, kp, r, addr);
+#pragma unroll
+    for (int j = 0; j < CMAX; ++j) {
+      sq_r += (double)r[j] * (double)r[j];
+      // the end-of-sweep residual is the next epoch's starting residual (carry mode)
+      const int s = j * G + c.g;
+      if (c.live && j < wmax && s < cnt) a.r_csc[a.csr_pos[r0 + s]] = r[j];
+    }
   }
   const double bw = block_sum_d(t.sq_w, red);
   __syncthreads();
@@ -763,15 +848,14 @@ static bool pick_compact(int cmax, int& c, int& g) {
 
 #define PB_DISPATCH_CG(c, g, MACRO)                                                                 \
   switch (c * 100 + g) {                                                                            \
-    MACRO(8, 1) MACRO(16, 1) MACRO(24, 1) MACRO(32, 1) MACRO(24, 2) MACRO(32, 2) MACRO(24, 4)       \
-    MACRO(32, 4) MACRO(24, 8) MACRO(32, 8) MACRO(32, 16) MACRO(32, 32)                              \
+    MACRO(8, 1) MACRO(16, 1) MACRO(24, 1) MACRO(32, 1) MACRO(32, 2) MACRO(32, 4) MACRO(32, 8)      \
+    MACRO(32, 16) MACRO(32, 32)                                                                     \
     default: set_error("unsupported compact layout c=%d g=%d", c, g); return PB_EUNSUPPORTED;       \
   }
 
 static void normalize_cg(int& c, int& g) {
   // collapse to the instantiated set
-  if (g >= 2 && c < 24) c = 24;
-  if (g >= 16) c = 32;
+  if (g >= 2) c = 32;
 }
 
 int launch_resid_compact(const CompactArgs& a_in, cudaStream_t st) {
@@ -803,19 +887,26 @@ int launch_code_compact(const CompactArgs& a_in, int mode, int& nblocks, cudaStr
   if (!pick_compact(a.cmax, c, g)) { set_error("patch has too many observed elements (%d)", a.cmax); return PB_EUNSUPPORTED; }
   normalize_cg(c, g);
   const int th = 256;
-  a.kc = (int)((100 * 1024) / ((size_t)(a.p + 1) * 4));
-  if (a.kc < 1) a.kc = 1;
-  if (a.kc > a.k) a.kc = a.k;
-  const size_t smem = (size_t)a.kc * (a.p + 1) * 4 + (size_t)a.k * 8 + (size_t)(th / g) * 9 * 4;
+  // DT chunk: kc atoms (a multiple of 8) x (P+1) rows of pitch kc+2 within ~100 KB
+  // (two CTAs per SM); the whole dictionary when it fits
+  const size_t fixed = (size_t)a.k * 8 + (size_t)(th / g) * 9 * 4;
+  const int k8 = (int)ceil_div(a.k, 8) * 8;
+  int kc = (int)(((100 * 1024) / ((size_t)(a.p + 1) * 4) - 2) & ~(size_t)7);
+  if (kc < 8) kc = 8;
+  a.kc = kc >= k8 ? k8 : kc;
+  const size_t smem = (size_t)(a.kc + 2) * (a.p + 1) * 4 + fixed;
   if (smem > 220 * 1024) { set_error("too many atoms for the code step (K=%d)", a.k); return PB_EUNSUPPORTED; }
-  const unsigned nb = (unsigned)ceil_div(a.n * g, th);
-  nblocks = (int)nb;
+  const int64_t nb = ceil_div(a.n * g, th);
   PB_CUDA_TRY(cudaMemsetAsync(a.m_count, 0, (size_t)a.k * sizeof(int32_t), st));
 #define PB_C(C, GG)                                                                                  \
   case C * 100 + GG: {                                                                               \
     auto kern = mode == kRngReplay ? k_code_compact<C, GG, kRngReplay> : k_code_compact<C, GG, kRngPhilox>; \
     PB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    kern<<<nb, th, smem, st>>>(a);                                                                   \
+    int per_sm = 0;                                                                                  \
+    PB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, th, smem));             \
+    const int64_t grid = std::min<int64_t>(nb, (int64_t)std::max(per_sm, 1) * sm_count_c());         \
+    nblocks = (int)grid;                                                                             \
+    kern<<<(unsigned)grid, th, smem, st>>>(a);                                                       \
     break;                                                                                           \
   }
   PB_DISPATCH_CG(c, g, PB_C)
