@@ -238,7 +238,9 @@ __device__ __forceinline__ void code_one(const CompactArgs& a, const CodeConst& 
 // atom kc0.  W = live register slots of this warp (compile time).
 template <int CMAX, int W, int G, int MODE>
 __device__ __forceinline__ void code_atoms(const CompactArgs& a, const CodeConst& c, CodeThread& t, int k0, int k1,
-                                           int kc0, const float* dt, float (&r)[CMAX], const int (&addr)[CMAX]) {
+                                           const float* dt, float (&r)[CMAX], int (&addr)[CMAX]) {
+  // addr[j]: byte offset of slot j's DT row + the current pair's column; it
+  // advances by 8 per pair (no per-slot address arithmetic beyond that)
   constexpr bool kPair = W <= 16;  // register budget: 2W values of D per pair
   int64_t zo = (int64_t)k0 * a.ld + c.ic;
   uint8_t za = a.usage[zo], zb = 0;
@@ -270,7 +272,7 @@ __device__ __forceinline__ void code_atoms(const CompactArgs& a, const CodeConst
         uu0 = u01_24(rnd.x);
         uu1 = u01_24(rnd.y);
       }
-      const char* col = (const char*)dt + (size_t)(k - kc0) * 4;
+      const char* col = (const char*)dt;
       if (kPair) {
         float d0[W], d1[W];
 #pragma unroll
@@ -292,6 +294,8 @@ __device__ __forceinline__ void code_atoms(const CompactArgs& a, const CodeConst
           code_one<CMAX, W, G, MODE>(a, c, t, k + 1, zo + a.ld, d0, r, zb, sb, uu1, g1, ud1, gd1);
         }
       }
+#pragma unroll
+      for (int j = 0; j < W; ++j) addr[j] += 8;
       za = zna; zb = znb; sa = sna; sb = snb;
       zo += 2 * a.ld;
     }
@@ -320,16 +324,18 @@ __device__ __forceinline__ void stage_atoms_t(float* dt, const float* __restrict
 
 template <int CMAX, int W, int G, int MODE>
 __device__ __forceinline__ void code_patch_range(const CompactArgs& a, const CodeConst& c, CodeThread& t, float* dt,
-                                                 int kp, float (&r)[CMAX], const int (&addr)[CMAX]) {
+                                                 int kp, float (&r)[CMAX], int (&addr)[CMAX]) {
   if (a.kc >= a.k) {
-    code_atoms<CMAX, W, G, MODE>(a, c, t, 0, a.k, 0, dt, r, addr);
+    code_atoms<CMAX, W, G, MODE>(a, c, t, 0, a.k, dt, r, addr);
   } else {
     for (int k0 = 0; k0 < a.k; k0 += a.kc) {
       const int kn = min(a.kc, a.k - k0);
       __syncthreads();
       stage_atoms_t(dt, a.atoms, k0, kn, a.p, kp);
       __syncthreads();
-      code_atoms<CMAX, W, G, MODE>(a, c, t, k0, k0 + kn, k0, dt, r, addr);
+      code_atoms<CMAX, W, G, MODE>(a, c, t, k0, k0 + kn, dt, r, addr);
+#pragma unroll
+      for (int j = 0; j < W; ++j) addr[j] -= 4 * ((kn + 1) & ~1);  // back to column 0
     }
   }
 }
