@@ -209,10 +209,12 @@ int pb_gibbs_epoch(const pb_epoch_desc* d, int32_t* m_counts_out, void* stream);
  * the epochs since enabling (single host thread use). */
 int pb_phase_timing(int32_t enable);
 int pb_phase_read(double* ms_out /* [4] */, int64_t* epochs_out);
-/* Profiling only: in-kernel globaltimer phases of the dictionary step, max over
- * CTAs, accumulated since enabling: [staging, last-tile elements, pass-end
- * reduce, grid sync 1, cross-CTA reduce, grid sync 2, atom update, elements]. */
-int pb_dict_profile(int32_t enable, double* slots_ns_out /* [8] or NULL */);
+/* Profiling only: in-kernel globaltimer phases of the dictionary step as seen by
+ * thread 0 of each CTA, mean over CTAs, accumulated since enabling:
+ * [tile-top barrier, W/colptr copy wait, element work, tile-end barrier,
+ *  boundary merge, pass-end partials, grid sync 1, cross-CTA reduce,
+ *  grid sync 2, atom update, -, -]. */
+int pb_dict_profile(int32_t enable, double* slots_ns_out /* [12] or NULL */);
 
 /* ---- stateful problem (C-ABI with HOST buffers; the live submit_frame slice,
  *      pipeline.py:217-251).  Owns all device buffers. ---- */

@@ -356,15 +356,22 @@ int pb_index_refresh_values(const pb_patch_index* pi, const float* values, const
 }
 
 int pb_dict_profile(int32_t enable, double* slots_ns_out) {
-  const size_t bytes = (size_t)kMaxDictBlocks * 8 * sizeof(unsigned long long);
+  const size_t bytes = (size_t)kMaxDictBlocks * kProfSlots * sizeof(unsigned long long);
   if (slots_ns_out) {
-    for (int i = 0; i < 8; ++i) slots_ns_out[i] = 0.0;
+    for (int i = 0; i < kProfSlots; ++i) slots_ns_out[i] = 0.0;
     if (g_dict_prof) {
-      std::vector<unsigned long long> h(kMaxDictBlocks * 8);
+      std::vector<unsigned long long> h(kMaxDictBlocks * kProfSlots);
       PB_CUDA_TRY(cudaDeviceSynchronize());
       PB_CUDA_TRY(cudaMemcpy(h.data(), g_dict_prof, bytes, cudaMemcpyDeviceToHost));
-      for (int b = 0; b < kMaxDictBlocks; ++b)
-        for (int i = 0; i < 8; ++i) slots_ns_out[i] = std::max(slots_ns_out[i], (double)h[b * 8 + i]);
+      int nb = 0;  // CTAs that recorded anything; report the mean over them
+      for (int b = 0; b < kMaxDictBlocks; ++b) {
+        unsigned long long tot = 0;
+        for (int i = 0; i < kProfSlots; ++i) tot += h[b * kProfSlots + i];
+        if (!tot) continue;
+        ++nb;
+        for (int i = 0; i < kProfSlots; ++i) slots_ns_out[i] += (double)h[b * kProfSlots + i];
+      }
+      for (int i = 0; i < kProfSlots; ++i) slots_ns_out[i] /= nb ? nb : 1;
     }
   }
   if (enable && !g_dict_prof) PB_CUDA_TRY(cudaMalloc(&g_dict_prof, bytes));

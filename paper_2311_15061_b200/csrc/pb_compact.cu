@@ -469,6 +469,27 @@ __device__ __forceinline__ void warp_transpose_reduce(float (&v)[NP], int lane) 
   for (int q = 0; q < NP / 16; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], 1);
 }
 
+// Transpose reduction of NP per-lane values inside groups of S lanes (S | 32):
+// afterwards lane `sub` of a group holds the group sums of values
+// [base, base + NP/S) with base = sum over levels o = S/2..1 of (sub & o ? half : 0).
+template <int NP, int S>
+__device__ __forceinline__ void group_transpose_reduce(float (&v)[NP], int sub) {
+  constexpr int LV = S == 2 ? 1 : S == 4 ? 2 : S == 8 ? 3 : S == 16 ? 4 : 5;
+  static_assert(NP % S == 0, "NP must be a multiple of the group size");
+#pragma unroll
+  for (int lvl = 0; lvl < LV; ++lvl) {
+    const int o = (S / 2) >> lvl;
+    const int half = NP >> (lvl + 1);
+    const bool lo = (sub & o) == 0;
+#pragma unroll
+    for (int q = 0; q < half; ++q) {
+      const float send = lo ? v[half + q] : v[q];
+      const float keep = lo ? v[q] : v[half + q];
+      v[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+}
+
 template <int B>
 struct GramLayout {
   static constexpr int NACC = B + B * (B + 1) / 2;      // C_j, then G_jl (l <= j), G_jj = A_j
@@ -490,6 +511,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// 16-byte shared load from a precomputed shared-window address (volatile: the
+// staged tile is produced by the async proxy, keep it behind the mbarrier wait)
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 // global -> shared bulk copy completing on an mbarrier (size and addresses 16-byte aligned)
@@ -516,6 +544,8 @@ __device__ __forceinline__ uint64_t gtimer() {
 //   wholly owned by one warp add straight into the CTA accumulator; the (at
 //   most two) boundary segments go to per-warp slots merged in warp order.
 constexpr int kTbCache = 1024;  // tile bases cached in shared memory per CTA
+constexpr int kGroupLanes = 8;  // lanes per segment group in the element phase
+constexpr int kSegLen = 128;    // max elements of one segment (a multiple of kGroupLanes)
 
 // The B sequential atom draws of one block from the reduced moments (f64):
 //   C_j += sum_{l<j} G_jl o delta_l;  lambda = P + geps*A_j;  mu = geps*(C_j + d_j*A_j)/lambda;
@@ -609,7 +639,7 @@ __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
   auto prof = [&](int slot) {
     if (a.prof && threadIdx.x == 0) {
       const uint64_t now = gtimer();
-      a.prof[blockIdx.x * 8 + slot] += now - t_mark;
+      a.prof[blockIdx.x * kProfSlots + slot] += now - t_mark;
       t_mark = now;
     }
   };
@@ -645,9 +675,9 @@ __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
       if (threadIdx.x == 0 && !(a.dbg & 4)) issue(t_lo, seq & 1);
     }
     for (int tile = t_lo; tile < t_hi; ++tile, ++seq) {
-      prof(7);
       const uint32_t st = seq & 1;
       __syncthreads();   // previous tile fully consumed: its stage and cps buffer are free
+      prof(0);
       if (tile + 1 < t_hi) {
         if (threadIdx.x == 0 && !(a.dbg & 4)) issue(tile + 1, st ^ 1);
       }
@@ -655,109 +685,106 @@ __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
       const int64_t tb = tile_start(tile);
       const int64_t rs = max(tb, e_lo), re = min(tile_start(tile + 1), e_hi);
       const float* wcur = wbuf + (size_t)st * 2 * kTile * B;
-      const float* wprev = wcur + kTile * B;
+      const uint32_t wcur_s = smem_u32(wcur), wprev_s = wcur_s + kTile * B * 4u;
       const int* cpt = cps + st * cpp;
       if (!(a.dbg & 4)) mbar_wait(&mbar[st], (phase_bits >> st) & 1u);
       phase_bits ^= 1u << st;
-      prof(0);
+      prof(1);
       const int m = (int)(re - rs);
       const int ws = (int)(rs - tb) + (int)((int64_t)m * wid / NW), we = (int)(rs - tb) + (int)((int64_t)m * (wid + 1) / NW);
       if (ws < we && !(a.dbg & 8)) {
-        // Stream the warp's slice [ws, we) in 128-element chunks with the next
-        // chunk's loads in flight, independent of column boundaries; the
-        // per-column sums are flushed (transpose-reduced) where a column ends.
-        int c = 0;
+        // Element phase of this warp's slice [ws, we).  The slice is cut into
+        // segments that never cross a column end and hold at most kSegLen
+        // elements; a ROUND gives one segment to each of the kGroups lane
+        // groups (kGroupLanes lanes each, striding the segment).  The Gram /
+        // moment sums of a round are reduced inside each lane group (3 shuffle
+        // levels instead of 5 per column), groups that share a column are
+        // combined in group order, and the head group adds the totals to the
+        // CTA accumulator (or the warp's boundary slot) — fixed order, so
+        // deterministic.
+        constexpr int S = kGroupLanes, NG = 32 / kGroupLanes;
+        const int grp = lane / S, sub = lane % S;
+        int col = 0;
         {
           int lo = 0, hi = p - 1;
           while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (cpt[mid] <= ws) lo = mid; else hi = mid - 1; }
-          c = lo;
+          col = lo;
         }
-        const int c_first = c;
-        int cend = min(we, cpt[c + 1]);
-        const int64_t ebase = tb;
-        float dl[B];
+        const int c_first = col;
+        int pos = ws;
+        for (int q = lane; q < 2 * L::NACC; q += 32) slots[wid * 2 * L::NACC + q] = 0.0f;
+        __syncwarp();
+        // carve the next NG segments (warp-uniform) and put the first kPf
+        // elements of this lane's segment in flight
+        constexpr int kPf = 4;
+        const uint16_t* eloc_t = a.e_loc + tb;
+        float* r_t = a.r_csc + tb;
+        int ms = 0, mt = 0, mc = -1, its = 0;
+        int ilb[kPf];
+        float rb[kPf];
+        auto carve = [&]() {
+          int max_len = 0;
+          ms = 0; mt = 0; mc = -1;
 #pragma unroll
-        for (int j = 0; j < B; ++j) dl[j] = has_prev ? dprev[j * p + c] : 0.0f;
-        float v[L::NP];
-#pragma unroll
-        for (int q = 0; q < L::NP; ++q) v[q] = 0.0f;
-        auto flush = [&]() {  // column c's segment of this slice is complete
-          const int cs = max(ws, cpt[c]);
-          if (has_cur && cs < cend) {
-            if (!(a.dbg & 2)) warp_transpose_reduce<L::NP>(v, lane);
-            const bool exclusive = cpt[c] >= ws && cpt[c + 1] <= we;
-            const int slot = c == c_first ? 0 : 1;
-            if ((lane & 1) == 0) {
-              constexpr int R = L::NP / 16;
-              const int base = R * (((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
-                                    ((lane >> 1) & 1));
-#pragma unroll
-              for (int q = 0; q < R; ++q) {
-                if (base + q < L::NACC) {
-                  if (exclusive) acc[c * L::NACC + base + q] += v[q];
-                  else slots[(wid * 2 + slot) * L::NACC + base + q] = v[q];
-                }
-              }
+          for (int g = 0; g < NG; ++g) {
+            int s = we, t = we, cg = -1;
+            if (pos < we) {
+              while (cpt[col + 1] <= pos) ++col;  // skip empty columns
+              s = pos;
+              t = min(min(we, cpt[col + 1]), pos + kSegLen);
+              cg = col;
+              pos = t;
             }
-            if (!exclusive && lane == 0) slot_col[wid * 2 + slot] = c;
-#pragma unroll
-            for (int q = 0; q < L::NP; ++q) v[q] = 0.0f;
+            max_len = max(max_len, t - s);
+            if (g == grp) { ms = s; mt = t; mc = cg; }
           }
-          ++c;
-          if (c < p) {
-            cend = min(we, cpt[c + 1]);
+          its = (max_len + S - 1) / S;
 #pragma unroll
-            for (int j = 0; j < B; ++j) dl[j] = has_prev ? dprev[j * p + c] : 0.0f;
+          for (int d = 0; d < kPf; ++d) {
+            const int e = ms + sub + d * S;
+            ilb[d] = 0;
+            rb[d] = 0.0f;
+            if (e < mt) { ilb[d] = eloc_t[e]; rb[d] = r_t[e]; }
           }
         };
-        int iln[4];
-        float rn[4];
+        carve();
+        while (true) {
+          float dl[B];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int e = ws + q * 32 + lane;
-          iln[q] = e < we ? (int)a.e_loc[ebase + e] : -1;
-          rn[q] = e < we ? a.r_csc[ebase + e] : 0.0f;
-        }
-        for (int eb = ws; eb < we; eb += 128) {
-          int ilq[4];
-          float rq[4];
+          for (int j = 0; j < B; ++j) dl[j] = (has_prev && mc >= 0) ? dprev[j * p + mc] : 0.0f;
+          float v[L::NP];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            ilq[q] = iln[q];
-            rq[q] = rn[q];
-            const int e = eb + 128 + q * 32 + lane;
-            iln[q] = e < we ? (int)a.e_loc[ebase + e] : -1;
-            rn[q] = e < we ? a.r_csc[ebase + e] : 0.0f;
-          }
+          for (int q = 0; q < L::NP; ++q) v[q] = 0.0f;
+          // lane-private cursors: element ec, its residual slot rc, kPf*S ahead in flight
+          int ec = ms + sub;
+          float* rc = r_t + ec;
+          const uint16_t* ecp = eloc_t + ec;
+          for (int it = 0; it < its; it += kPf) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int s0 = eb + q * 32;
-            if (s0 >= we) break;
-            const int s1 = min(s0 + 32, we);
-            const int e = s0 + lane;
-            int lo = s0;
-            while (lo < s1) {  // warp-uniform: split the 32 elements at column ends
-              const int hi = min(s1, cend);
-              if (e >= lo && e < hi && !(a.dbg & 1)) {
-                const int il = ilq[q];
-                float r = rq[q];
+            for (int d = 0; d < kPf; ++d) {
+              if (it + d >= its) break;
+              const int il = ilb[d];
+              float r = rb[d];
+              if (ec + kPf * S < mt) { ilb[d] = ecp[kPf * S]; rb[d] = rc[kPf * S]; }
+              if (ec < mt) {
+                const uint32_t wo[2] = {(uint32_t)wsw(il, 0) * 4u, (uint32_t)wsw(il, 1) * 4u};
                 if (has_prev) {
                   float sh[B / 4];
 #pragma unroll
                   for (int h = 0; h < B / 4; ++h) {  // independent partial sums: short FMA chains
-                    const float4 w4 = *(const float4*)(wprev + wsw(il, h));
+                    const float4 w4 = lds128(wprev_s + wo[h]);
                     sh[h] = fmaf(w4.w, dl[4 * h + 3],
                                  fmaf(w4.z, dl[4 * h + 2], fmaf(w4.y, dl[4 * h + 1], w4.x * dl[4 * h])));
                   }
 #pragma unroll
                   for (int h = 0; h < B / 4; ++h) r += sh[h];
-                  a.r_csc[ebase + e] = r;
+                  *rc = r;
                 }
                 if (has_cur) {
                   float wc[B];
 #pragma unroll
                   for (int h = 0; h < B / 4; ++h) {
-                    const float4 w4 = *(const float4*)(wcur + wsw(il, h));
+                    const float4 w4 = lds128(wcur_s + wo[h]);
                     wc[4 * h + 0] = w4.x; wc[4 * h + 1] = w4.y; wc[4 * h + 2] = w4.z; wc[4 * h + 3] = w4.w;
                   }
 #pragma unroll
@@ -768,30 +795,95 @@ __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
                   }
                 }
               }
-              if (hi == cend) flush();
-              lo = hi;
+              ec += S;
+              rc += S;
+              ecp += S;
             }
+          }
+          const int mc_done = mc;
+          const bool more = pos < we;
+          if (more) carve();  // next round's loads overlap this round's reduction
+          if (has_cur) {
+            // reduce inside the lane group: lane `sub` ends with values [base, base + NP/S)
+            group_transpose_reduce<L::NP, S>(v, sub);
+            constexpr int R = L::NP / S;
+            int base = 0;
+            {
+              int cnt = L::NP;
+#pragma unroll
+              for (int o = S / 2; o >= 1; o >>= 1) { cnt >>= 1; if (sub & o) base += cnt; }
+            }
+            // combine groups of the same column (segmented, in group order)
+            const int c_next1 = __shfl_down_sync(0xffffffffu, mc_done, S);
+            const int c_next2 = __shfl_down_sync(0xffffffffu, mc_done, 2 * S);
+            const bool j1 = grp + 1 < NG && c_next1 == mc_done && mc_done >= 0;
+            const bool j2 = grp + 2 < NG && j1 && c_next2 == mc_done;
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+              const float o1 = __shfl_down_sync(0xffffffffu, v[q], S);
+              v[q] += j1 ? o1 : 0.0f;
+            }
+            if (NG > 2) {
+#pragma unroll
+              for (int q = 0; q < R; ++q) {
+                const float o2 = __shfl_down_sync(0xffffffffu, v[q], 2 * S);
+                v[q] += j2 ? o2 : 0.0f;
+              }
+            }
+            const int c_prev = __shfl_up_sync(0xffffffffu, mc_done, S);
+            const bool head = mc_done >= 0 && (grp == 0 || c_prev != mc_done);
+            if (head) {
+              const bool exclusive = cpt[mc_done] >= ws && cpt[mc_done + 1] <= we;
+              const int slot = wid * 2 + (mc_done == c_first ? 0 : 1);
+              float* dst = exclusive ? acc + mc_done * L::NACC : slots + slot * L::NACC;
+#pragma unroll
+              for (int q = 0; q < R; ++q)
+                if (base + q < L::NACC) dst[base + q] += v[q];
+              if (!exclusive && sub == 0) slot_col[slot] = mc_done;
+            }
+          }
+          if (!more) break;
+        }
+      }
+      prof(2);
+      __syncthreads();
+      prof(3);
+      // merge the boundary segments in warp order (deterministic): the valid
+      // slots have non-decreasing columns, so each column is a run of slots;
+      // warp h merges the h-th run (every warp derives the runs by ballot)
+      static_assert(NW * 2 == 32, "one boundary slot per lane");
+      if (has_cur) {
+        const int col = slot_col[lane];
+        const unsigned vm = __ballot_sync(0xffffffffu, col >= 0);
+        const unsigned before = vm & ((1u << lane) - 1u);
+        const int prev_col = __shfl_sync(0xffffffffu, col, before ? 31 - __clz(before) : 0);
+        const unsigned hm = __ballot_sync(0xffffffffu, col >= 0 && (!before || prev_col != col));
+        if (wid < __popc(hm)) {
+          unsigned m = hm;
+          for (int i = 0; i < wid; ++i) m &= m - 1u;
+          const int hs = __ffs(m) - 1;
+          const int c = __shfl_sync(0xffffffffu, col, hs);
+          for (int q = lane; q < L::NACC; q += 32) {
+            float sum = acc[c * L::NACC + q];
+            for (int s2 = hs; s2 < NW * 2; ++s2) {
+              const int c2 = slot_col[s2];
+              if (c2 == c) sum += slots[s2 * L::NACC + q];
+              else if (c2 > c) break;
+            }
+            acc[c * L::NACC + q] = sum;
           }
         }
       }
-      __syncthreads();
-      // merge the boundary segments in warp order (deterministic)
-      if (has_cur && threadIdx.x < L::NACC) {
-        for (int s2 = 0; s2 < NW * 2; ++s2) {
-          const int c = slot_col[s2];
-          if (c >= 0) acc[c * L::NACC + threadIdx.x] += slots[s2 * L::NACC + threadIdx.x];
-        }
-      }
+      prof(4);
     }
-    prof(1);
     if (!has_cur) break;
     __syncthreads();
     float* mine = a.partials + (size_t)blockIdx.x * p * L::NACC;
     for (int t = threadIdx.x; t < p * L::NACC; t += blockDim.x) mine[t] = acc[t];
     __threadfence();
-    prof(2);
+    prof(5);
     grid_sync(a.bar);
-    prof(3);
+    prof(6);
     // cross-CTA reduction, one warp per value, fixed order (lane-strided, then a fixed shuffle tree)
     const int nv = p * L::NACC;
     const int gw = blockIdx.x * NW + wid, nwarps = gridDim.x * NW;
@@ -802,17 +894,17 @@ __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
       if (lane == 0) a.reduced[t] = s;
     }
     __threadfence();
-    prof(4);
+    prof(7);
     if (a.split) return;  // split mode: the caller allreduces `reduced` across ranks, then k_dict_update
     grid_sync(a.bar);
-    prof(5);
+    prof(8);
     for (int t = threadIdx.x; t < nv; t += blockDim.x) red64[t] = __ldcg(a.reduced + t);
     __syncthreads();
     // sequential atom updates inside the block, identical in every CTA
     atom_block_update<B>(red64, p, k0, nb, geps, epoch, a.draws, a.key0, a.key1, dold, dprev,
                          blockIdx.x == 0 ? a.atoms : nullptr);
     __syncthreads();
-    prof(6);
+    prof(9);
   }
 }
 

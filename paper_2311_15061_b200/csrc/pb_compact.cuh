@@ -7,6 +7,8 @@
 
 namespace pb {
 
+constexpr int kProfSlots = 12;  // in-kernel dictionary-step profile slots per CTA
+
 struct CompactArgs {
   // index (CSR view) + residual in CSC order
   const int32_t* counts;
@@ -57,8 +59,8 @@ struct DictGramArgs {
   float* partials;      // max_blocks * P * NACC
   double* reduced;      // P * NACC
   unsigned* bar;        // 2
-  unsigned long long* prof;  // optional [gridDim][8] phase nanoseconds (profiling)
-  int dbg;              // profiling-only: 1 skip element math, 2 skip segment reductions
+  unsigned long long* prof;  // optional [gridDim][kProfSlots] phase nanoseconds (profiling)
+  int dbg;              // profiling-only: 4 skip the W/colptr bulk copies, 8 skip the element phase
   // split (multi-rank) mode: run the single pass blk_begin and stop after the
   // per-GPU reduction; the previous pass's shifts come from delta_g [B][P]
   int split;

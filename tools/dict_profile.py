@@ -11,8 +11,8 @@ from paper_2311_15061_b200 import inputs  # noqa: E402
 from paper_2311_15061_b200 import patches as pp  # noqa: E402
 from tools.prof_epoch import CFGS  # noqa: E402
 
-NAMES = ["staging", "elems(last tile)", "pass-end reduce", "grid sync 1", "cross-CTA reduce", "grid sync 2",
-         "atom update", "elems(other tiles)"]
+NAMES = ["tile-top barrier", "W copy wait", "elements (warp 0)", "tile-end barrier", "boundary merge",
+         "pass-end partials", "grid sync 1", "cross-CTA reduce", "grid sync 2", "atom update", "-", "-"]
 for cid in [int(x) for x in sys.argv[1:]] or [3, 2]:
     c = CFGS[cid]
     img = inputs.synthetic_texture(c["shape"], seed=0) if len(c["shape"]) == 2 else \
@@ -28,11 +28,11 @@ for cid in [int(x) for x in sys.argv[1:]] or [3, 2]:
     E = 3
     for _ in range(E):
         gb.gibbs_epoch(st, pm, hp, rng="philox", check=False)
-    out = (ctypes.c_double * 8)()
+    out = (ctypes.c_double * 12)()
     lib.pb_dict_profile(0, out)
     ph = (ctypes.c_double * 4)()
     ne = ctypes.c_int64()
     lib.pb_phase_read(ph, ctypes.byref(ne))
-    print(f"cfg{cid}: N={pm.num_patches} nnz={pm.n_obs} dict {ph[1] / E:.3f} ms/epoch; in-kernel (max over CTAs, ms/epoch):")
+    print(f"cfg{cid}: N={pm.num_patches} nnz={pm.n_obs} dict {ph[1] / E:.3f} ms/epoch; in-kernel (thread 0, mean over CTAs, ms/epoch):")
     for nm, v in zip(NAMES, out):
         print(f"   {nm:20s} {v / 1e6 / E:8.3f}")
