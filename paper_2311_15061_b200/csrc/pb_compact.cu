@@ -544,8 +544,6 @@ __device__ __forceinline__ uint64_t gtimer() {
 //   wholly owned by one warp add straight into the CTA accumulator; the (at
 //   most two) boundary segments go to per-warp slots merged in warp order.
 constexpr int kTbCache = 1024;  // tile bases cached in shared memory per CTA
-constexpr int kGroupLanes = 8;  // lanes per segment group in the element phase
-constexpr int kSegLen = 128;    // max elements of one segment (a multiple of kGroupLanes)
 
 // The B sequential atom draws of one block from the reduced moments (f64):
 //   C_j += sum_{l<j} G_jl o delta_l;  lambda = P + geps*A_j;  mu = geps*(C_j + d_j*A_j)/lambda;
@@ -583,7 +581,10 @@ __device__ __forceinline__ void atom_block_update(const double* red, int p, int 
   }
 }
 
-template <int B>
+constexpr int kDictGroupLanes = 8;  // lanes per segment group in the element phase
+constexpr int kDictSegLen = 256;   // max elements of one segment (a multiple of the group size)
+
+template <int B, int kGroupLanes, int kSegLen>
 __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
   using L = GramLayout<B>;
   constexpr int NW = 16;
@@ -712,6 +713,20 @@ __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
         }
         const int c_first = col;
         int pos = ws;
+        // segment length: when the slice spans fewer columns than groups, cut it
+        // into whole rounds of NG equal segments (<= kSegLen); otherwise the
+        // column ends already give enough segments
+        int c_last = 0;
+        {
+          int lo = c_first, hi = p - 1;
+          while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (cpt[mid] <= we - 1) lo = mid; else hi = mid - 1; }
+          c_last = lo;
+        }
+        int seg_len = kSegLen;
+        if (c_last - c_first + 1 < NG) {
+          const int n_rounds = (we - ws + NG * kSegLen - 1) / (NG * kSegLen);
+          seg_len = ((we - ws + NG * n_rounds - 1) / (NG * n_rounds) + S - 1) / S * S;
+        }
         for (int q = lane; q < 2 * L::NACC; q += 32) slots[wid * 2 * L::NACC + q] = 0.0f;
         __syncwarp();
         // carve the next NG segments (warp-uniform) and put the first kPf
@@ -731,7 +746,7 @@ __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
             if (pos < we) {
               while (cpt[col + 1] <= pos) ++col;  // skip empty columns
               s = pos;
-              t = min(min(we, cpt[col + 1]), pos + kSegLen);
+              t = min(min(we, cpt[col + 1]), pos + seg_len);
               cg = col;
               pos = t;
             }
@@ -813,21 +828,16 @@ __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
 #pragma unroll
               for (int o = S / 2; o >= 1; o >>= 1) { cnt >>= 1; if (sub & o) base += cnt; }
             }
-            // combine groups of the same column (segmented, in group order)
-            const int c_next1 = __shfl_down_sync(0xffffffffu, mc_done, S);
-            const int c_next2 = __shfl_down_sync(0xffffffffu, mc_done, 2 * S);
-            const bool j1 = grp + 1 < NG && c_next1 == mc_done && mc_done >= 0;
-            const bool j2 = grp + 2 < NG && j1 && c_next2 == mc_done;
+            // combine groups of the same column: segmented doubling sum toward
+            // the run's first group (columns are non-decreasing across groups)
 #pragma unroll
-            for (int q = 0; q < R; ++q) {
-              const float o1 = __shfl_down_sync(0xffffffffu, v[q], S);
-              v[q] += j1 ? o1 : 0.0f;
-            }
-            if (NG > 2) {
+            for (int k = 1; k < NG; k <<= 1) {
+              const int cn = __shfl_down_sync(0xffffffffu, mc_done, k * S);
+              const bool join = grp + k < NG && cn == mc_done && mc_done >= 0;
 #pragma unroll
               for (int q = 0; q < R; ++q) {
-                const float o2 = __shfl_down_sync(0xffffffffu, v[q], 2 * S);
-                v[q] += j2 ? o2 : 0.0f;
+                const float o = __shfl_down_sync(0xffffffffu, v[q], k * S);
+                v[q] += join ? o : 0.0f;
               }
             }
             const int c_prev = __shfl_up_sync(0xffffffffu, mc_done, S);
@@ -1013,7 +1023,7 @@ int launch_code_compact(const CompactArgs& a_in, int mode, int& nblocks, cudaStr
   return PB_OK;
 }
 
-template <int B>
+template <int B, int GL, int SL>
 static int launch_dict_gram_b(DictGramArgs a, cudaStream_t st) {
   using L = GramLayout<B>;
   const int th = 512;
@@ -1023,19 +1033,21 @@ static int launch_dict_gram_b(DictGramArgs a, cudaStream_t st) {
   const size_t smem = wbytes + (size_t)a.p * L::NACC * 4 + (size_t)16 * 2 * L::NACC * 4 + 16 * 2 * 4 +
                       (size_t)2 * colptr_pitch(a.p) * 4 + (size_t)kTbCache * 8 + (size_t)2 * B * a.p * 4;
   if (smem > 225 * 1024) { set_error("patch size %d too large for the dictionary step", a.p); return PB_EUNSUPPORTED; }
-  PB_CUDA_TRY(cudaFuncSetAttribute(k_dict_gram<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  PB_CUDA_TRY(cudaFuncSetAttribute(k_dict_gram<B, GL, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  PB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dict_gram<B>, th, smem));
+  PB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dict_gram<B, GL, SL>, th, smem));
   if (per_sm < 1) { set_error("dictionary step cannot be resident"); return PB_EUNSUPPORTED; }
   int blocks = sm_count_c() * per_sm;
   if (blocks > a.max_blocks) blocks = a.max_blocks;
   PB_CUDA_TRY(cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned), st));
   void* args[] = {&a};
-  PB_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_dict_gram<B>, dim3(blocks), dim3(th), args, smem, st));
+  PB_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_dict_gram<B, GL, SL>, dim3(blocks), dim3(th), args, smem, st));
   return PB_OK;
 }
 
-int launch_dict_gram(const DictGramArgs& a, cudaStream_t st) { return launch_dict_gram_b<8>(a, st); }
+int launch_dict_gram(const DictGramArgs& a, cudaStream_t st) {
+  return launch_dict_gram_b<8, kDictGroupLanes, kDictSegLen>(a, st);
+}
 
 int launch_dict_update(const DictGramArgs& a, int blk, cudaStream_t st) {
   const size_t smem = (size_t)2 * 8 * a.p * 4;
