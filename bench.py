@@ -26,6 +26,7 @@ Metric: patch-atom updates/s (higher is better).
 from __future__ import annotations
 
 import argparse
+import glob
 import ctypes
 import json
 import os
@@ -297,8 +298,19 @@ def run_gpu_arm(args):
         alg_flops = n * k * 2.0 * p
     dur_s = per[dom] * 1e-3
     achieved = alg_bytes / dur_s / 1e9
+    # DRAM traffic per launch of the same kernel from the committed `ncu --set full`
+    # capture (profiles/rNN/ncu_traffic.json, configs[1] sizes); null if absent
+    traffic, traffic_src = None, None
+    kname = names[dom].split()[0]
+    for tf in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_traffic.json")), reverse=True):
+        tj = json.load(open(tf))
+        if kname in tj:
+            traffic = tj[kname]["traffic_bytes"]
+            traffic_src = os.path.relpath(tf, ROOT) + " @ " + tj.get("_capture", {}).get("commit", "?")
+            break
     roofline = {"bound": "hbm", "kernel": names[dom], "achieved": achieved, "peak": peaks["hbm_gbs"],
-                "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                "traffic_source": traffic_src,
                 "peak_source": "fallback" if peaks.get("_fallback") else "MEASURED_PEAKS.json hbm_gbs",
                 "alg_bytes_per_launch": alg_bytes, "launch_ms": per[dom],
                 "fp32": {"achieved_tflops": alg_flops / dur_s / 1e12, "peak_tflops_derived": 74.45,

@@ -179,6 +179,7 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
     { const char* e = getenv("PB_DICT_DEBUG"); g.dbg = e ? atoi(e) : 0; }
     g.n = d->n; g.p = d->p; g.k = d->k; g.key0 = k0; g.key1 = k1;
     g.ld = c.ld;
+    g.nnz = d->index->nnz;
     if (!d->allreduce) {
       if ((rc = launch_dict_gram(g, st))) return rc;   // fused: all passes in one persistent launch
     } else {

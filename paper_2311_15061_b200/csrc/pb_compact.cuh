@@ -70,6 +70,7 @@ struct DictGramArgs {
   int wbytes;
   int64_t n;
   int64_t ld;           // row pitch of usage/weights (K, ld), ld >= n
+  int64_t nnz;          // observed elements (host copy of tile_base[ntiles])
   int p, k;
   uint32_t key0, key1;
 };
