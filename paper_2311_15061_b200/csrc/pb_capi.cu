@@ -5,6 +5,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "../../include/pb200.h"
@@ -373,6 +374,18 @@ int pb_dict_profile(int32_t enable, double* slots_ns_out) {
         for (int i = 0; i < kProfSlots; ++i) slots_ns_out[i] += (double)h[b * kProfSlots + i];
       }
       for (int i = 0; i < kProfSlots; ++i) slots_ns_out[i] /= nb ? nb : 1;
+      if (getenv("PB_DICT_PROF_DUMP")) {  // per-CTA spread of each slot (profiling aid)
+        for (int i = 0; i < kProfSlots; ++i) {
+          std::vector<double> v;
+          for (int b = 0; b < kMaxDictBlocks; ++b)
+            if (h[b * kProfSlots + i] || h[b * kProfSlots + 2]) v.push_back((double)h[b * kProfSlots + i]);
+          if (v.empty()) continue;
+          std::sort(v.begin(), v.end());
+          fprintf(stderr, "pb_dict_profile slot %2d: min %.3f p10 %.3f median %.3f p90 %.3f max %.3f ms (n=%zu)\n", i,
+                  v.front() / 1e6, v[v.size() / 10] / 1e6, v[v.size() / 2] / 1e6, v[v.size() * 9 / 10] / 1e6,
+                  v.back() / 1e6, v.size());
+        }
+      }
     }
   }
   if (enable && !g_dict_prof) PB_CUDA_TRY(cudaMalloc(&g_dict_prof, bytes));

@@ -38,13 +38,8 @@ __device__ __forceinline__ void stage_atoms(float* ds, const float* __restrict__
 }
 
 // Float offset of 16-byte chunk h (0/1) of patch row il inside a tile block of
-// the code copy W ([kTile][8] floats).  Chunks are XOR-swizzled across each
-// 128-byte line so the dictionary step's row gathers spread over all banks.
-__device__ __forceinline__ int wsw(int il, int h) {
-  const int line = il >> 2;
-  const int cw = ((il & 3) << 1) | h;
-  return line * 32 + ((cw ^ (line & 7)) << 2);
-}
+// the code copy W ([kTile][8] floats); see w_row_off (pb_index.cuh).
+__device__ __forceinline__ int wsw(int il, int h) { return (int)((w_row_off(il) ^ (h << 4)) >> 2); }
 
 template <int G>
 __device__ __forceinline__ float gsum(float v) {
@@ -581,6 +576,7 @@ __device__ __forceinline__ void atom_block_update(const double* red, int p, int 
   }
 }
 
+constexpr double kTileVisitCost = 3000.0;  // element-equivalents of one tile visit (work split)
 constexpr int kDictGroupLanes = 8;  // lanes per segment group in the element phase
 constexpr int kDictSegLen = 256;   // max elements of one segment (a multiple of the group size)
 
@@ -617,7 +613,25 @@ __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
   const int epoch = a.sc->epoch + 1;
   const int nblk = (a.k + B - 1) / B;
   const int64_t nnz = a.tile_base[a.ntiles];
-  const int64_t e_lo = nnz * blockIdx.x / gridDim.x, e_hi = nnz * (blockIdx.x + 1) / gridDim.x;
+  // CTA element ranges balance elements + kTileVisitCost per tile visited (each
+  // visit pays the staging, barriers and boundary merge): boundary c sits where
+  // the prefix cost C(e) = e + kTileVisitCost * (tiles started up to e) reaches
+  // c/G of the total; a boundary falling in a tile's visit cost snaps to the
+  // tile start.  Static and deterministic.
+  auto boundary = [&](int c) -> int64_t {
+    if (c <= 0) return 0;
+    if (c >= (int)gridDim.x) return nnz;
+    const double target = ((double)nnz + kTileVisitCost * a.ntiles) * c / gridDim.x;
+    int lo = 0, hi = a.ntiles - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if ((double)a.tile_base[mid] + kTileVisitCost * mid <= target) lo = mid; else hi = mid - 1;
+    }
+    const double over = target - ((double)a.tile_base[lo] + kTileVisitCost * lo) - kTileVisitCost;
+    const int64_t e = a.tile_base[lo] + (over > 0.0 ? (int64_t)over : 0);
+    return min(e, a.tile_base[lo + 1]);
+  };
+  const int64_t e_lo = boundary(blockIdx.x), e_hi = boundary(blockIdx.x + 1);
   // tiles overlapping [e_lo, e_hi): t_lo = last tile starting <= e_lo
   int t_lo = 0, t_hi = 0;
   {
@@ -782,7 +796,7 @@ __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
               float r = rb[d];
               if (ec + kPf * S < mt) { ilb[d] = ecp[kPf * S]; rb[d] = rc[kPf * S]; }
               if (ec < mt) {
-                const uint32_t wo[2] = {(uint32_t)wsw(il, 0) * 4u, (uint32_t)wsw(il, 1) * 4u};
+                const uint32_t wo[2] = {(uint32_t)il, (uint32_t)il ^ 16u};  // e_loc holds w_row_off
                 if (has_prev) {
                   float sh[B / 4];
 #pragma unroll

@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kFillThreads) k_tile_fill(
     if (threadIdx.x == 0) colptr[(int64_t)t * colptr_pitch(p) + pe] = (int32_t)(col - tb);
     if (o0) {
       const int64_t pos = col + rank;
-      e_loc[pos] = (uint16_t)l0;
+      e_loc[pos] = (uint16_t)w_row_off(l0);
       x_csc[pos] = values[(int64_t)pe * n + g0];
       csr_p[row0 + j0] = (uint16_t)pe;
       csr_pos[row0 + j0] = (uint32_t)pos;
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kFillThreads) k_tile_fill(
     }
     if (o1) {
       const int64_t pos = col + rank + o0;
-      e_loc[pos] = (uint16_t)(l0 + 1);
+      e_loc[pos] = (uint16_t)w_row_off(l0 + 1);
       x_csc[pos] = values[(int64_t)pe * n + g1];
       csr_p[row1 + j1] = (uint16_t)pe;
       csr_pos[row1 + j1] = (uint32_t)pos;

@@ -10,6 +10,14 @@ constexpr int kWB = 8;             // atoms per block of the tile-blocked code c
 
 __host__ __device__ constexpr int colptr_pitch(int p) { return (p + 1 + 3) & ~3; }
 
+// Byte offset of patch row il's first 16-byte chunk inside a tile block of the
+// code copy W ([kTile][kWB] floats); the second chunk is at (offset ^ 16).
+// Chunks are XOR-swizzled across each 128-byte line (4 rows) so gathers of
+// nearby rows spread over the shared-memory banks.
+__host__ __device__ constexpr uint32_t w_row_off(int il) {
+  return ((uint32_t)(il >> 2) << 7) | ((uint32_t)(((il & 3) << 1) ^ ((il >> 2) & 7)) << 4);
+}
+
 struct PatchIndex {
   int64_t n;
   int p;
@@ -18,7 +26,7 @@ struct PatchIndex {
   int64_t* tile_base;   // [ntiles + 1] first element of each tile; tile_base[ntiles] = nnz
   int32_t* colptr;      // [ntiles][colptr_pitch(p)] tile-relative first element of each column (p+1 used)
   int64_t* rowptr;      // [n + 1] first CSR slot of each patch
-  uint16_t* e_loc;      // [nnz] CSC: patch index inside its tile
+  uint16_t* e_loc;      // [nnz] CSC: w_row_off(patch index inside its tile) — the W row of the element
   float* x_csc;         // [nnz] CSC: observed (mean-subtracted) value
   uint16_t* csr_p;      // [nnz] CSR: patch offset p of each slot
   uint32_t* csr_pos;    // [nnz] CSR: CSC position of each slot

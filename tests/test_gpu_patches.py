@@ -128,6 +128,25 @@ def test_large_frame_indices_exact(cuda_device):
     assert np.array_equal(pp.coverage_map(pm), op.coverage((512, 512), (8, 8), (1, 1)))
 
 
+def _w_row_off(il):
+    """Byte offset of row il's first chunk in a W tile block (pb_index.cuh w_row_off)."""
+    il = np.asarray(il, dtype=np.int64)
+    return ((il >> 2) << 7) | ((((il & 3) << 1) ^ ((il >> 2) & 7)) << 4)
+
+
+def _w_row_index(off):
+    """Inverse of _w_row_off."""
+    line = off >> 7
+    return line * 4 + ((((off >> 4) & 7) ^ (line & 7)) >> 1)
+
+
+def test_w_row_offset_is_a_bijection():
+    il = np.arange(1024)
+    off = _w_row_off(il)
+    assert len(np.unique(off)) == 1024 and off.max() < 2 ** 15 and np.all(off % 16 == 0)
+    assert np.array_equal(_w_row_index(off), il)
+
+
 def _carve(buf, n, p, nnz):
     """Mirror of carve_index (pb_index.cu) to read the index back for checking."""
     kt = 1024
@@ -166,7 +185,7 @@ def test_observed_element_index_exact(cuda_device, shape, patch, ratio, kind):
     pos = b["csr_pos"].astype(np.int64)
     assert np.array_equal(np.sort(pos), np.arange(ix.nnz))
     tile = rows // 1024
-    assert np.array_equal(b["e_loc"][pos].astype(np.int64), rows - tile * 1024)
+    assert np.array_equal(b["e_loc"][pos].astype(np.int64), _w_row_off(rows - tile * 1024))
     assert np.array_equal(b["x_csc"][pos], vals[rows, cols].astype(np.float32))
     tb = b["tile_base"].astype(np.int64)
     cp = b["colptr"].reshape(-1, (p + 1 + 3) & ~3)[:, :p + 1].astype(np.int64) + tb[:-1, None]  # tile-relative
@@ -174,5 +193,5 @@ def test_observed_element_index_exact(cuda_device, shape, patch, ratio, kind):
     # CSC order inside a column: ascending patch
     for t in range(cp.shape[0]):
         for pe in range(p):
-            seg = b["e_loc"][cp[t, pe]:cp[t, pe + 1]]
-            assert np.all(np.diff(seg.astype(np.int64)) > 0)
+            seg = _w_row_index(b["e_loc"][cp[t, pe]:cp[t, pe + 1]].astype(np.int64))
+            assert np.all(np.diff(seg) > 0)
