@@ -212,8 +212,8 @@ int pb_phase_read(double* ms_out /* [4] */, int64_t* epochs_out);
 /* Profiling only: in-kernel globaltimer phases of the dictionary step as seen by
  * thread 0 of each CTA, mean over CTAs, accumulated since enabling:
  * [tile-top barrier, W/colptr copy wait, element work, tile-end barrier,
- *  boundary merge, pass-end partials, grid sync 1, cross-CTA reduce,
- *  grid sync 2, atom update, -, -]. */
+ *  boundary merge, pass-end partials, grid sync 1, per-pixel reduce,
+ *  grid sync 2, shift load, owner atom update, -]. */
 int pb_dict_profile(int32_t enable, double* slots_ns_out /* [12] or NULL */);
 
 /* ---- stateful problem (C-ABI with HOST buffers; the live submit_frame slice,

@@ -55,7 +55,7 @@ struct EpochWs {
   unsigned* bar;
   double* block_sums;
   int32_t* m_count;
-  float* delta_g;   // split-mode atom shifts of the previous block [8][P]
+  float* delta_g;   // atom shifts of the last updated block [8][P] (dictionary step exchange)
 };
 static const int kMaxDictBlocks = 148 * 8;
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -181,13 +181,13 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
     g.n = d->n; g.p = d->p; g.k = d->k; g.key0 = k0; g.key1 = k1;
     g.ld = c.ld;
     g.nnz = d->index->nnz;
+    g.delta_g = ws.delta_g;   // atom shifts of the last updated block [8][P]
     if (!d->allreduce) {
       if ((rc = launch_dict_gram(g, st))) return rc;   // fused: all passes in one persistent launch
     } else {
       // split (sharded) mode: per atom block, local pass -> allreduce of the
       // 44*P moment sums across ranks -> identical atom draws on every rank
       g.split = 1;
-      g.delta_g = ws.delta_g;
       const int nblk = dict_gram_blocks(d->k);
       for (int b = 0; b <= nblk; ++b) {
         g.blk_begin = b;

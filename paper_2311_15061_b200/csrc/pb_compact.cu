@@ -543,47 +543,71 @@ constexpr int kTbCache = 1024;  // tile bases cached in shared memory per CTA
 // The B sequential atom draws of one block from the reduced moments (f64):
 //   C_j += sum_{l<j} G_jl o delta_l;  lambda = P + geps*A_j;  mu = geps*(C_j + d_j*A_j)/lambda;
 //   d_j' = mu + g/sqrt(lambda)  (bpfa.py:161-166, 303-307).  Identical in every CTA/rank.
+// The B sequential atom draws of one block at ONE pixel pe from its reduced
+// moments rv[NACC] (f64):
+//   C_j += sum_{l<j} G_jl delta_l;  lambda = P + geps*A_j;  mu = geps*(C_j + d_j*A_j)/lambda;
+//   d_j' = mu + g/sqrt(lambda)  (bpfa.py:161-166, 303-307);  delta_j = d_j - d_j' (f32).
+template <int B>
+__device__ __forceinline__ double atom_draw(const double* draws, int pe, int p, int k, int epoch, uint32_t key0,
+                                            uint32_t key1) {
+  if (draws) return draws[(int64_t)k * p + pe];
+  const u32x4 rr = philox4x32_10(u32x4{(uint32_t)(pe >> 1), (uint32_t)k, (uint32_t)epoch, kDomAtom << 24}, key0, key1);
+  float n0, n1;
+  box_muller(rr.x, rr.y, n0, n1);
+  return (pe & 1) ? n1 : n0;
+}
+
+template <int B>
+__device__ __forceinline__ void atom_pixel_update(const double* rv, int pe, int p, int k0, int nb, double geps,
+                                                  int epoch, const double* draws, uint32_t key0, uint32_t key1,
+                                                  const float* dold, float* atoms_out, float* dsh, float* delta_out,
+                                                  const double* gpre = nullptr) {
+  // dsh: [B][p] shifts of this block (read back for the C corrections), delta_out: optional global copy,
+  // gpre: optional precomputed normals [B] of this pixel
+  using L = GramLayout<B>;
+  for (int j = 0; j < nb; ++j) {
+    const int k = k0 + j;
+    double c = rv[j];
+    for (int l = 0; l < j; ++l) c += rv[L::gidx(j, l)] * (double)dsh[l * p + pe];
+    const double am = rv[L::gidx(j, j)];
+    const double d_o = (double)dold[j * p + pe];
+    const double lam = (double)p + geps * am;
+    const double rs = rsqrt(lam);   // 1/sqrt(lambda); 1/lambda = rs^2
+    const double mu = geps * (c + d_o * am) * (rs * rs);
+    const double gdraw = gpre ? gpre[j] : atom_draw<B>(draws, pe, p, k, epoch, key0, key1);
+    const float dn = (float)(mu + gdraw * rs);
+    if (atoms_out) atoms_out[(int64_t)k * p + pe] = dn;
+    const float dd = dold[j * p + pe] - dn;   // the next pass's shift
+    dsh[j * p + pe] = dd;
+    if (delta_out) delta_out[j * p + pe] = dd;
+  }
+  for (int j = nb; j < B; ++j) {
+    dsh[j * p + pe] = 0.0f;
+    if (delta_out) delta_out[j * p + pe] = 0.0f;
+  }
+}
+
 template <int B>
 __device__ __forceinline__ void atom_block_update(const double* red, int p, int k0, int nb, double geps, int epoch,
                                                   const double* draws, uint32_t key0, uint32_t key1,
                                                   const float* dold, float* dprev, float* atoms_out) {
   using L = GramLayout<B>;
-  for (int pe = threadIdx.x; pe < p; pe += blockDim.x) {
-    const double* rv = red + (size_t)pe * L::NACC;
-    for (int j = 0; j < nb; ++j) {
-      const int k = k0 + j;
-      double c = rv[j];
-      for (int l = 0; l < j; ++l) c += rv[L::gidx(j, l)] * (double)dprev[l * p + pe];
-      const double am = rv[L::gidx(j, j)];
-      const double d_o = (double)dold[j * p + pe];
-      const double lam = (double)p + geps * am;
-      const double mu = geps * (c + d_o * am) / lam;
-      double gdraw;
-      if (draws) {
-        gdraw = draws[(int64_t)k * p + pe];
-      } else {
-        const u32x4 rr = philox4x32_10(u32x4{(uint32_t)(pe >> 1), (uint32_t)k, (uint32_t)epoch, kDomAtom << 24},
-                                       key0, key1);
-        float n0, n1;
-        box_muller(rr.x, rr.y, n0, n1);
-        gdraw = (pe & 1) ? n1 : n0;
-      }
-      const float dn = (float)(mu + gdraw / sqrt(lam));
-      if (atoms_out) atoms_out[(int64_t)k * p + pe] = dn;
-      dprev[j * p + pe] = dold[j * p + pe] - dn;   // becomes the next pass's shift
-    }
-    for (int j = nb; j < B; ++j) dprev[j * p + pe] = 0.0f;
-  }
+  for (int pe = threadIdx.x; pe < p; pe += blockDim.x)
+    atom_pixel_update<B>(red + (size_t)pe * L::NACC, pe, p, k0, nb, geps, epoch, draws, key0, key1, dold, atoms_out,
+                         dprev, nullptr);
 }
 
 constexpr double kTileVisitCost = 3000.0;  // element-equivalents of one tile visit (work split)
 constexpr int kDictGroupLanes = 8;  // lanes per segment group in the element phase
 constexpr int kDictSegLen = 256;   // max elements of one segment (a multiple of the group size)
 
-template <int B, int kGroupLanes, int kSegLen>
-__global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
+// NW warps per CTA, NSTAGE staging buffers (2: the next tile is bulk-copied
+// while this one is processed; 1: two CTAs share an SM and cover each other's
+// copy and barrier waits).
+template <int B, int kGroupLanes, int kSegLen, int NW, int NSTAGE>
+__global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) {
   using L = GramLayout<B>;
-  constexpr int NW = 16;
+  static_assert(NW * 2 <= 32, "at most one boundary slot per lane");
   extern __shared__ __align__(16) unsigned char smraw[];
   const int p = a.p;
   static_assert(B == kWB, "the tile-blocked code copy W holds blocks of kWB atoms");
@@ -594,8 +618,8 @@ __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
   float* slots = acc + (size_t)p * L::NACC;              // NW * 2 * NACC
   int* slot_col = (int*)(slots + NW * 2 * L::NACC);      // NW * 2
   const int cpp = colptr_pitch(p);
-  int* cps = slot_col + NW * 2;                          // 2 * cpp (double-buffered tile colptr, bulk-copied)
-  int64_t* tbs = (int64_t*)(cps + 2 * cpp);             // kTbCache tile bases of this CTA
+  int* cps = slot_col + NW * 2;                          // NSTAGE * cpp (tile colptr, bulk-copied)
+  int64_t* tbs = (int64_t*)(cps + NSTAGE * cpp);        // kTbCache tile bases of this CTA
   float* dold = (float*)(tbs + kTbCache);                // B * p
   float* dprev = dold + B * p;                           // B * p
   double* red64 = (double*)smraw;                        // p * NACC (aliases the staging)
@@ -686,15 +710,16 @@ __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
                       &mbar[stage]);
     };
     __syncthreads();
-    if (t_lo < t_hi) {
+    if (NSTAGE == 2 && t_lo < t_hi) {
       if (threadIdx.x == 0 && !(a.dbg & 4)) issue(t_lo, seq & 1);
     }
     for (int tile = t_lo; tile < t_hi; ++tile, ++seq) {
-      const uint32_t st = seq & 1;
+      const uint32_t st = NSTAGE == 2 ? (seq & 1) : 0;
       __syncthreads();   // previous tile fully consumed: its stage and cps buffer are free
       prof(0);
-      if (tile + 1 < t_hi) {
-        if (threadIdx.x == 0 && !(a.dbg & 4)) issue(tile + 1, st ^ 1);
+      if (threadIdx.x == 0 && !(a.dbg & 4)) {
+        if (NSTAGE == 1) issue(tile, 0);
+        else if (tile + 1 < t_hi) issue(tile + 1, st ^ 1);
       }
       if (lane == 0) { slot_col[wid * 2] = -1; slot_col[wid * 2 + 1] = -1; }
       const int64_t tb = tile_start(tile);
@@ -875,16 +900,15 @@ __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
       // merge the boundary segments in warp order (deterministic): the valid
       // slots have non-decreasing columns, so each column is a run of slots;
       // warp h merges the h-th run (every warp derives the runs by ballot)
-      static_assert(NW * 2 == 32, "one boundary slot per lane");
       if (has_cur) {
-        const int col = slot_col[lane];
+        const int col = lane < NW * 2 ? slot_col[lane] : -1;
         const unsigned vm = __ballot_sync(0xffffffffu, col >= 0);
         const unsigned before = vm & ((1u << lane) - 1u);
         const int prev_col = __shfl_sync(0xffffffffu, col, before ? 31 - __clz(before) : 0);
         const unsigned hm = __ballot_sync(0xffffffffu, col >= 0 && (!before || prev_col != col));
-        if (wid < __popc(hm)) {
+        for (int h = wid; h < __popc(hm); h += NW) {
           unsigned m = hm;
-          for (int i = 0; i < wid; ++i) m &= m - 1u;
+          for (int i = 0; i < h; ++i) m &= m - 1u;
           const int hs = __ffs(m) - 1;
           const int c = __shfl_sync(0xffffffffu, col, hs);
           for (int q = lane; q < L::NACC; q += 32) {
@@ -908,25 +932,56 @@ __global__ void __launch_bounds__(512, 1) k_dict_gram(DictGramArgs a) {
     prof(5);
     grid_sync(a.bar);
     prof(6);
-    // cross-CTA reduction, one warp per value, fixed order (lane-strided, then a fixed shuffle tree)
+    // Cross-CTA reduction distributed by PIXEL: CTA c owns pixels c, c+G, ...;
+    // one warp per (pixel, value) sums the G partials lane-strided then by a
+    // fixed shuffle tree (f64, deterministic), and the owner performs that
+    // pixel's B sequential atom draws right away (pixels are independent).
     const int nv = p * L::NACC;
-    const int gw = blockIdx.x * NW + wid, nwarps = gridDim.x * NW;
-    for (int t = gw; t < nv; t += nwarps) {
-      double s = 0.0;
-      for (int b = lane; b < (int)gridDim.x; b += 32) s += (double)__ldcg(a.partials + (size_t)b * nv + t);
-      s = warp_sum_d(s);
-      if (lane == 0) a.reduced[t] = s;
+    const int npl = blockIdx.x < (unsigned)p ? (p - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    constexpr int NPART = (NW * 32) / L::NACC;   // threads per value
+    double* part64 = red64 + (size_t)((p + gridDim.x - 1) / gridDim.x) * L::NACC;  // [NPART][NACC] scratch
+    double* gpre = part64 + NPART * L::NACC;     // [B] normals of the pixel
+    for (int i = 0; i < npl; ++i) {
+      const int pe = blockIdx.x + i * gridDim.x;
+      if (threadIdx.x < NPART * L::NACC) {
+        // value q over partials b = part, part + NPART, ...: 8 independent loads in flight
+        const int q = threadIdx.x % L::NACC, part = threadIdx.x / L::NACC;
+        const float* src = a.partials + (size_t)pe * L::NACC + q;
+        double acc8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc8[u] = 0.0;
+        int b = part;
+        for (; b + 7 * NPART < (int)gridDim.x; b += 8 * NPART) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc8[u] += (double)__ldcg(src + (size_t)(b + u * NPART) * nv);
+        }
+        for (; b < (int)gridDim.x; b += NPART) acc8[0] += (double)__ldcg(src + (size_t)b * nv);
+        part64[part * L::NACC + q] =
+            ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
+      } else if (!a.split && (int)threadIdx.x - NPART * L::NACC < nb) {
+        const int j = threadIdx.x - NPART * L::NACC;   // the pixel's B atom normals, in parallel
+        gpre[j] = atom_draw<B>(a.draws, pe, p, k0 + j, epoch, a.key0, a.key1);
+      }
+      __syncthreads();
+      if (threadIdx.x < L::NACC) {
+        double sum = 0.0;
+        for (int u = 0; u < NPART; ++u) sum += part64[u * L::NACC + threadIdx.x];
+        red64[(size_t)i * L::NACC + threadIdx.x] = sum;
+        if (a.split) a.reduced[(size_t)pe * L::NACC + threadIdx.x] = sum;
+      }
+      __syncthreads();
+      if (!a.split && threadIdx.x == 0)
+        atom_pixel_update<B>(red64 + (size_t)i * L::NACC, pe, p, k0, nb, geps, epoch, a.draws, a.key0, a.key1, dold,
+                             a.atoms, dprev, a.delta_g, gpre);
+      __syncthreads();
     }
-    __threadfence();
     prof(7);
     if (a.split) return;  // split mode: the caller allreduces `reduced` across ranks, then k_dict_update
+    __threadfence();
+    prof(10);
     grid_sync(a.bar);
     prof(8);
-    for (int t = threadIdx.x; t < nv; t += blockDim.x) red64[t] = __ldcg(a.reduced + t);
-    __syncthreads();
-    // sequential atom updates inside the block, identical in every CTA
-    atom_block_update<B>(red64, p, k0, nb, geps, epoch, a.draws, a.key0, a.key1, dold, dprev,
-                         blockIdx.x == 0 ? a.atoms : nullptr);
+    for (int t = threadIdx.x; t < B * p; t += blockDim.x) dprev[t] = __ldcg(a.delta_g + t);
     __syncthreads();
     prof(9);
   }
@@ -1037,30 +1092,44 @@ int launch_code_compact(const CompactArgs& a_in, int mode, int& nblocks, cudaStr
   return PB_OK;
 }
 
-template <int B, int GL, int SL>
-static int launch_dict_gram_b(DictGramArgs a, cudaStream_t st) {
+template <int B, int GL, int SL, int NW, int NSTAGE>
+static size_t dict_gram_smem(int p, size_t* wbytes_out) {
   using L = GramLayout<B>;
-  const int th = 512;
+  const size_t wbytes = std::max((size_t)NSTAGE * 2 * kTile * B * 4, (size_t)p * L::NACC * 8);
+  if (wbytes_out) *wbytes_out = wbytes;
+  return wbytes + (size_t)p * L::NACC * 4 + (size_t)NW * 2 * L::NACC * 4 + NW * 2 * 4 +
+         (size_t)NSTAGE * colptr_pitch(p) * 4 + (size_t)kTbCache * 8 + (size_t)2 * B * p * 4;
+}
+
+template <int B, int GL, int SL, int NW, int NSTAGE>
+static int launch_dict_gram_b(DictGramArgs a, cudaStream_t st) {
+  const int th = NW * 32;
   if (a.ld % 4) { set_error("usage/weights row pitch must be a multiple of 4 (got %lld)", (long long)a.ld); return PB_EVALUE; }
-  const size_t wbytes = std::max((size_t)2 * 2 * kTile * B * 4, (size_t)a.p * L::NACC * 8);
+  size_t wbytes = 0;
+  const size_t smem = dict_gram_smem<B, GL, SL, NW, NSTAGE>(a.p, &wbytes);
   a.wbytes = (int)wbytes;
-  const size_t smem = wbytes + (size_t)a.p * L::NACC * 4 + (size_t)16 * 2 * L::NACC * 4 + 16 * 2 * 4 +
-                      (size_t)2 * colptr_pitch(a.p) * 4 + (size_t)kTbCache * 8 + (size_t)2 * B * a.p * 4;
   if (smem > 225 * 1024) { set_error("patch size %d too large for the dictionary step", a.p); return PB_EUNSUPPORTED; }
-  PB_CUDA_TRY(cudaFuncSetAttribute(k_dict_gram<B, GL, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  auto kern = k_dict_gram<B, GL, SL, NW, NSTAGE>;
+  PB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  PB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dict_gram<B, GL, SL>, th, smem));
+  PB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, th, smem));
   if (per_sm < 1) { set_error("dictionary step cannot be resident"); return PB_EUNSUPPORTED; }
   int blocks = sm_count_c() * per_sm;
   if (blocks > a.max_blocks) blocks = a.max_blocks;
   PB_CUDA_TRY(cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned), st));
   void* args[] = {&a};
-  PB_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_dict_gram<B, GL, SL>, dim3(blocks), dim3(th), args, smem, st));
+  PB_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(blocks), dim3(th), args, smem, st));
   return PB_OK;
 }
 
 int launch_dict_gram(const DictGramArgs& a, cudaStream_t st) {
-  return launch_dict_gram_b<8, kDictGroupLanes, kDictSegLen>(a, st);
+  // two 8-warp CTAs per SM (single-buffered staging) when they fit in shared
+  // memory, else one 16-warp CTA with double-buffered staging
+  static int variant = -1;
+  if (variant < 0) { const char* e = getenv("PB_DICT_VARIANT"); variant = e ? atoi(e) : 0; }
+  if (variant != 1 && 2 * dict_gram_smem<8, kDictGroupLanes, kDictSegLen, 8, 1>(a.p, nullptr) <= 226 * 1024)
+    return launch_dict_gram_b<8, kDictGroupLanes, kDictSegLen, 8, 1>(a, st);
+  return launch_dict_gram_b<8, kDictGroupLanes, kDictSegLen, 16, 2>(a, st);
 }
 
 int launch_dict_update(const DictGramArgs& a, int blk, cudaStream_t st) {
