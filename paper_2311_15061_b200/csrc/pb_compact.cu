@@ -557,33 +557,63 @@ __device__ __forceinline__ double atom_draw(const double* draws, int pe, int p, 
   return (pe & 1) ? n1 : n0;
 }
 
+// Per-atom quantities of the draw that do not depend on the earlier atoms'
+// shifts (computable in parallel): 1/lambda, 1/sqrt(lambda), A_j, d_j(old), g.
+struct AtomPre {
+  double inv, rs, am, d_o, g;
+};
+
+template <int B>
+__device__ __forceinline__ AtomPre atom_pre(const double* rv, int j, int pe, int p, int k0, double geps, int epoch,
+                                            const double* draws, uint32_t key0, uint32_t key1, const float* dold) {
+  using L = GramLayout<B>;
+  AtomPre r;
+  r.am = rv[L::gidx(j, j)];
+  const double lam = (double)p + geps * r.am;
+  r.rs = rsqrt(lam);   // 1/sqrt(lambda); 1/lambda = rs^2
+  r.inv = r.rs * r.rs;
+  r.d_o = (double)dold[j * p + pe];
+  r.g = atom_draw<B>(draws, pe, p, k0 + j, epoch, key0, key1);
+  return r;
+}
+
+// The sequential part: C_j corrected by the shifts of atoms < j, the posterior
+// mean and the draw d_j' = mu + g/sqrt(lambda).
+template <int B>
+__device__ __forceinline__ float atom_chain_step(const double* rv, int j, const AtomPre& pr, const double (&dl)[B],
+                                                 double geps) {
+  using L = GramLayout<B>;
+  double c = rv[j];
+#pragma unroll
+  for (int l = 0; l < B; ++l)
+    if (l < j) c += rv[L::gidx(j, l)] * dl[l];
+  const double mu = geps * (c + pr.d_o * pr.am) * pr.inv;
+  return (float)(mu + pr.g * pr.rs);
+}
+
+// One thread: the B sequential atom draws of one block at pixel pe.
 template <int B>
 __device__ __forceinline__ void atom_pixel_update(const double* rv, int pe, int p, int k0, int nb, double geps,
                                                   int epoch, const double* draws, uint32_t key0, uint32_t key1,
                                                   const float* dold, float* atoms_out, float* dsh, float* delta_out,
-                                                  const double* gpre = nullptr) {
-  // dsh: [B][p] shifts of this block (read back for the C corrections), delta_out: optional global copy,
-  // gpre: optional precomputed normals [B] of this pixel
-  using L = GramLayout<B>;
-  for (int j = 0; j < nb; ++j) {
-    const int k = k0 + j;
-    double c = rv[j];
-    for (int l = 0; l < j; ++l) c += rv[L::gidx(j, l)] * (double)dsh[l * p + pe];
-    const double am = rv[L::gidx(j, j)];
-    const double d_o = (double)dold[j * p + pe];
-    const double lam = (double)p + geps * am;
-    const double rs = rsqrt(lam);   // 1/sqrt(lambda); 1/lambda = rs^2
-    const double mu = geps * (c + d_o * am) * (rs * rs);
-    const double gdraw = gpre ? gpre[j] : atom_draw<B>(draws, pe, p, k, epoch, key0, key1);
-    const float dn = (float)(mu + gdraw * rs);
-    if (atoms_out) atoms_out[(int64_t)k * p + pe] = dn;
+                                                  const AtomPre* pre = nullptr) {
+  // dsh: [B][p] shifts of this block, delta_out: optional global copy, pre: optional precomputed [B]
+  double dl[B];
+#pragma unroll
+  for (int j = 0; j < B; ++j) {
+    dl[j] = 0.0;
+    if (j >= nb) {
+      dsh[j * p + pe] = 0.0f;
+      if (delta_out) delta_out[j * p + pe] = 0.0f;
+      continue;
+    }
+    const AtomPre pr = pre ? pre[j] : atom_pre<B>(rv, j, pe, p, k0, geps, epoch, draws, key0, key1, dold);
+    const float dn = atom_chain_step<B>(rv, j, pr, dl, geps);
+    if (atoms_out) atoms_out[(int64_t)(k0 + j) * p + pe] = dn;
     const float dd = dold[j * p + pe] - dn;   // the next pass's shift
     dsh[j * p + pe] = dd;
     if (delta_out) delta_out[j * p + pe] = dd;
-  }
-  for (int j = nb; j < B; ++j) {
-    dsh[j * p + pe] = 0.0f;
-    if (delta_out) delta_out[j * p + pe] = 0.0f;
+    dl[j] = (double)dd;
   }
 }
 
@@ -940,27 +970,29 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
     const int npl = blockIdx.x < (unsigned)p ? (p - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     constexpr int NPART = (NW * 32) / L::NACC;   // threads per value
     double* part64 = red64 + (size_t)((p + gridDim.x - 1) / gridDim.x) * L::NACC;  // [NPART][NACC] scratch
-    double* gpre = part64 + NPART * L::NACC;     // [B] normals of the pixel
+    AtomPre* pre = (AtomPre*)(part64 + NPART * L::NACC);                          // [B]
     for (int i = 0; i < npl; ++i) {
       const int pe = blockIdx.x + i * gridDim.x;
       if (threadIdx.x < NPART * L::NACC) {
-        // value q over partials b = part, part + NPART, ...: 8 independent loads in flight
+        // value q over partials b = part, part + NPART, ...: 16 independent loads in flight
         const int q = threadIdx.x % L::NACC, part = threadIdx.x / L::NACC;
         const float* src = a.partials + (size_t)pe * L::NACC + q;
-        double acc8[8];
+        double acc16[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) acc8[u] = 0.0;
+        for (int u = 0; u < 16; ++u) acc16[u] = 0.0;
         int b = part;
-        for (; b + 7 * NPART < (int)gridDim.x; b += 8 * NPART) {
+        for (; b + 15 * NPART < (int)gridDim.x; b += 16 * NPART) {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) acc8[u] += (double)__ldcg(src + (size_t)(b + u * NPART) * nv);
+          for (int u = 0; u < 16; ++u) acc16[u] += (double)__ldcg(src + (size_t)(b + u * NPART) * nv);
         }
-        for (; b < (int)gridDim.x; b += NPART) acc8[0] += (double)__ldcg(src + (size_t)b * nv);
-        part64[part * L::NACC + q] =
-            ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
-      } else if (!a.split && (int)threadIdx.x - NPART * L::NACC < nb) {
-        const int j = threadIdx.x - NPART * L::NACC;   // the pixel's B atom normals, in parallel
-        gpre[j] = atom_draw<B>(a.draws, pe, p, k0 + j, epoch, a.key0, a.key1);
+#pragma unroll
+        for (int u = 0; u < 16; ++u)  // tail: at most 15 more partials, still independent
+          if (b + u * NPART < (int)gridDim.x) acc16[u] += (double)__ldcg(src + (size_t)(b + u * NPART) * nv);
+#pragma unroll
+        for (int h = 8; h >= 1; h >>= 1)
+#pragma unroll
+          for (int u = 0; u < h; ++u) acc16[u] += acc16[u + h];
+        part64[part * L::NACC + q] = acc16[0];
       }
       __syncthreads();
       if (threadIdx.x < L::NACC) {
@@ -970,9 +1002,15 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
         if (a.split) a.reduced[(size_t)pe * L::NACC + threadIdx.x] = sum;
       }
       __syncthreads();
-      if (!a.split && threadIdx.x == 0)
+      if (a.split) continue;
+      prof(11);
+      if ((int)threadIdx.x < nb)   // the parallel part of the B draws
+        pre[threadIdx.x] = atom_pre<B>(red64 + (size_t)i * L::NACC, threadIdx.x, pe, p, k0, geps, epoch, a.draws,
+                                       a.key0, a.key1, dold);
+      __syncthreads();
+      if (threadIdx.x == 0)
         atom_pixel_update<B>(red64 + (size_t)i * L::NACC, pe, p, k0, nb, geps, epoch, a.draws, a.key0, a.key1, dold,
-                             a.atoms, dprev, a.delta_g, gpre);
+                             a.atoms, dprev, a.delta_g, pre);
       __syncthreads();
     }
     prof(7);
