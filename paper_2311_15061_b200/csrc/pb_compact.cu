@@ -464,6 +464,14 @@ __device__ __forceinline__ void warp_transpose_reduce(float (&v)[NP], int lane) 
   for (int q = 0; q < NP / 16; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], 1);
 }
 
+// Packed FMA on the aligned accumulator pair (v[2i], v[2i+1]) += a * b (FFMA2).
+template <int NP>
+__device__ __forceinline__ void pfma(float (&v)[NP], int i, float2 a, float2 b) {
+  const float2 c = __ffma2_rn(a, b, make_float2(v[2 * i], v[2 * i + 1]));
+  v[2 * i] = c.x;
+  v[2 * i + 1] = c.y;
+}
+
 // Transpose reduction of NP per-lane values inside groups of S lanes (S | 32):
 // afterwards lane `sub` of a group holds the group sums of values
 // [base, base + NP/S) with base = sum over levels o = S/2..1 of (sub & o ? half : 0).
@@ -485,11 +493,20 @@ __device__ __forceinline__ void group_transpose_reduce(float (&v)[NP], int sub) 
   }
 }
 
+// Accumulator layout of one atom block (B even): C_0..C_{B-1}, then per row j
+// of the Gram triangle the PAIRS (G_j,2m, G_j,2m+1) for 2m+1 <= j, then the
+// even-row diagonals G_00, G_22, ... — every update is a packed f32x2 FMA
+// (FFMA2) on an aligned pair; G_jj = A_j.
 template <int B>
 struct GramLayout {
-  static constexpr int NACC = B + B * (B + 1) / 2;      // C_j, then G_jl (l <= j), G_jj = A_j
+  static_assert(B % 2 == 0, "pair layout needs an even block");
+  static constexpr int NACC = B + B * (B + 1) / 2;
   static constexpr int NP = ((NACC + 15) / 16) * 16;    // padded for the transpose reduce
-  __device__ static constexpr int gidx(int j, int l) { return B + j * (j + 1) / 2 + l; }
+  __host__ __device__ static constexpr int pairbase(int j) { return (j / 2) * ((j + 1) / 2); }
+  static constexpr int DIAG = B + 2 * pairbase(B);     // first even-row diagonal
+  __host__ __device__ static constexpr int gidx(int j, int l) {
+    return ((j & 1) == 0 && l == j) ? DIAG + j / 2 : B + 2 * (pairbase(j) + l / 2) + (l & 1);
+  }
 };
 
 // --- mbarrier + 1-D bulk async copy (TMA engine) helpers --------------------
@@ -833,9 +850,11 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
         };
         carve();
         while (true) {
-          float dl[B];
+          float2 dl2[B / 2];
 #pragma unroll
-          for (int j = 0; j < B; ++j) dl[j] = (has_prev && mc >= 0) ? dprev[j * p + mc] : 0.0f;
+          for (int j = 0; j < B / 2; ++j)
+            dl2[j] = (has_prev && mc >= 0) ? make_float2(dprev[2 * j * p + mc], dprev[(2 * j + 1) * p + mc])
+                                           : make_float2(0.0f, 0.0f);
           float v[L::NP];
 #pragma unroll
           for (int q = 0; q < L::NP; ++q) v[q] = 0.0f;
@@ -852,16 +871,16 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
               if (ec + kPf * S < mt) { ilb[d] = ecp[kPf * S]; rb[d] = rc[kPf * S]; }
               if (ec < mt) {
                 const uint32_t wo[2] = {(uint32_t)il, (uint32_t)il ^ 16u};  // e_loc holds w_row_off
-                if (has_prev) {
-                  float sh[B / 4];
+                if (has_prev) {  // r += w_prev . delta  (packed pairs, two independent chains)
+                  float2 sh[B / 4];
 #pragma unroll
-                  for (int h = 0; h < B / 4; ++h) {  // independent partial sums: short FMA chains
+                  for (int h = 0; h < B / 4; ++h) {
                     const float4 w4 = lds128(wprev_s + wo[h]);
-                    sh[h] = fmaf(w4.w, dl[4 * h + 3],
-                                 fmaf(w4.z, dl[4 * h + 2], fmaf(w4.y, dl[4 * h + 1], w4.x * dl[4 * h])));
+                    sh[h] = __fmul2_rn(make_float2(w4.x, w4.y), dl2[2 * h]);
+                    sh[h] = __ffma2_rn(make_float2(w4.z, w4.w), dl2[2 * h + 1], sh[h]);
                   }
 #pragma unroll
-                  for (int h = 0; h < B / 4; ++h) r += sh[h];
+                  for (int h = 0; h < B / 4; ++h) r += sh[h].x + sh[h].y;
                   *rc = r;
                 }
                 if (has_cur) {
@@ -871,11 +890,20 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
                     const float4 w4 = lds128(wcur_s + wo[h]);
                     wc[4 * h + 0] = w4.x; wc[4 * h + 1] = w4.y; wc[4 * h + 2] = w4.z; wc[4 * h + 3] = w4.w;
                   }
+                  const float2 rr2 = make_float2(r, r);
 #pragma unroll
-                  for (int j = 0; j < B; ++j) {
-                    v[j] = fmaf(wc[j], r, v[j]);
+                  for (int h = 0; h < B / 2; ++h) pfma(v, h, make_float2(wc[2 * h], wc[2 * h + 1]), rr2);  // C
 #pragma unroll
-                    for (int l = 0; l <= j; ++l) v[L::gidx(j, l)] = fmaf(wc[j], wc[l], v[L::gidx(j, l)]);
+                  for (int j = 1; j < B; ++j) {   // Gram pairs (G_j,2m, G_j,2m+1)
+                    const float2 wj = make_float2(wc[j], wc[j]);
+#pragma unroll
+                    for (int m = 0; 2 * m + 1 <= j; ++m)
+                      pfma(v, L::gidx(j, 2 * m) / 2, wj, make_float2(wc[2 * m], wc[2 * m + 1]));
+                  }
+#pragma unroll
+                  for (int j = 0; j < B; j += 4) {   // even-row diagonals, two per pair
+                    const float2 d2 = make_float2(wc[j], wc[j + 2]);
+                    pfma(v, L::DIAG / 2 + j / 4, d2, d2);
                   }
                 }
               }
