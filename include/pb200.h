@@ -216,6 +216,17 @@ int pb_phase_read(double* ms_out /* [4] */, int64_t* epochs_out);
  *  grid sync 2, shift load, owner atom update, -]. */
 int pb_dict_profile(int32_t enable, double* slots_ns_out /* [12] or NULL */);
 
+/* ---- adaptive-residual sampling mask on device (sampling.py:184-207) ----
+ * Budget round(ratio*M); exploit = the round(exploit_fraction*budget) largest
+ * residuals, ties by lowest flat index (bit-exact with the reference's stable
+ * argsort); explore = the rest of the budget drawn uniformly without
+ * replacement from the unexploited elements with a device Philox stream keyed by
+ * (seed, frame_index) — NOT numpy's Generator.choice stream.  An all-zero map
+ * draws the whole budget uniformly (status 1).  Negative / NaN residuals:
+ * PB_EVALUE.  residual and mask_out are device pointers. */
+int pb_adaptive_mask(const double* residual, int64_t m, double ratio, double exploit_fraction, uint64_t seed,
+                     int64_t frame_index, uint8_t* mask_out, int32_t* status_out, void* stream);
+
 /* ---- stateful problem (C-ABI with HOST buffers; the live submit_frame slice,
  *      pipeline.py:217-251).  Owns all device buffers. ---- */
 typedef struct pb_problem pb_problem;
@@ -241,6 +252,22 @@ int pb_problem_destroy(pb_problem* pr);
  * hot slice (pipeline.py:224-251). */
 int pb_problem_submit_frame(pb_problem* pr, const double* frame_host, const uint8_t* mask_host,
                             double* recon_host);
+/* submit_frame plus the device-resident tail: any output may be
+ * NULL.  recon_host f64 (M) after data consistency; panel_host / masked_host
+ * uint8 wire panels of the reconstruction and of frame*mask,
+ * round(clip(x,0,1)*255) (server.py:46-53; rank-3 tensors show slice 0, other
+ * ranks refuse).  Every frame also updates the device residual map
+ * (recon - previous recon)^2 of the pre-consistency reconstruction
+ * (pipeline.py:265-269). */
+int pb_problem_submit_frame_ex(pb_problem* pr, const double* frame_host, const uint8_t* mask_host,
+                               double* recon_host, uint8_t* panel_host, uint8_t* masked_host);
+/* The residual map of the last frame (f64, M), copied to host. */
+int pb_problem_residual_map(pb_problem* pr, double* host_out);
+/* The adaptive-residual sampler (sampling.py:184-207) on the problem's residual
+ * map: writes the next mask (uint8, M) to host and keeps it as the cached
+ * device mask.  status 1 = all-zero map (uniform device draw). */
+int pb_problem_adaptive_mask(pb_problem* pr, double ratio, double exploit_fraction, uint64_t seed,
+                             int64_t frame_index, uint8_t* mask_host, int32_t* status_out);
 /* Device-side timing of the last submit_frame's GPU work (ms). */
 float pb_problem_last_gpu_ms(pb_problem* pr);
 /* Current dictionary (K,P) f32 and scalars, copied to host. */

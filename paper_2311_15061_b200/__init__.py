@@ -18,6 +18,7 @@ from .bpfa import (  # noqa: F401
     install_dictionary,
     transfer_dictionary,
 )
+from .live import LiveFrame, LiveProblem, adaptive_mask  # noqa: F401
 from .patches import (  # noqa: F401
     CoverageError,
     PatchMatrix,

@@ -99,6 +99,12 @@ SIGNATURES = {
     "pb_problem_create": (c_i32, [ctypes.POINTER(ProblemDesc), ctypes.POINTER(c_vp)]),
     "pb_problem_destroy": (c_i32, [c_vp]),
     "pb_problem_submit_frame": (c_i32, [c_vp, c_vp, c_vp, c_vp]),
+    "pb_problem_submit_frame_ex": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "pb_problem_residual_map": (c_i32, [c_vp, c_vp]),
+    "pb_problem_adaptive_mask": (c_i32, [c_vp, ctypes.c_double, ctypes.c_double, ctypes.c_uint64, c_i64, c_vp,
+                                         ctypes.POINTER(c_i32)]),
+    "pb_adaptive_mask": (c_i32, [c_vp, c_i64, ctypes.c_double, ctypes.c_double, ctypes.c_uint64, c_i64, c_vp,
+                                 ctypes.POINTER(c_i32), c_vp]),
     "pb_problem_last_gpu_ms": (c_f32, [c_vp]),
     "pb_problem_get_dictionary": (c_i32, [c_vp, c_vp, c_vp, ctypes.POINTER(Scalars)]),
 }

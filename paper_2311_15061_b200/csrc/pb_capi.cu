@@ -10,6 +10,7 @@
 
 #include "../../include/pb200.h"
 #include "pb_compact.cuh"
+#include "pb_live.cuh"
 
 namespace pb {
 
@@ -439,7 +440,11 @@ struct pb_problem {
   float *values = nullptr, *means = nullptr, *atoms = nullptr, *weights = nullptr, *est = nullptr;
   uint8_t *obs = nullptr, *usage = nullptr;
   int32_t *counts = nullptr, *m_count = nullptr;
-  double *pi = nullptr, *recon = nullptr;
+  double *pi = nullptr, *recon = nullptr, *out = nullptr, *prev = nullptr, *resid = nullptr;
+  uint8_t *panel = nullptr, *masked = nullptr;
+  int64_t panel_px = 0, panel_stride = 1;  // wire panel: rank 2, or slice 0 of rank 3
+  bool have_prev = false;
+  bool index_valid = false;  // the observed-element index matches the device mask
   pb_scalars* scalars = nullptr;
   unsigned long long* nobs_dev = nullptr;
   void* ws = nullptr;
@@ -465,7 +470,8 @@ extern "C" {
 int pb_problem_destroy(pb_problem* pr) {
   if (!pr) return PB_OK;
   void* bufs[] = {pr->frame, pr->mask, pr->values, pr->means, pr->atoms, pr->weights, pr->est, pr->obs, pr->usage,
-                  pr->counts, pr->m_count, pr->pi, pr->recon, pr->scalars, pr->nobs_dev, pr->ws, pr->index.buffer};
+                  pr->counts, pr->m_count, pr->pi, pr->recon, pr->scalars, pr->nobs_dev, pr->ws, pr->index.buffer,
+                  pr->out, pr->prev, pr->resid, pr->panel, pr->masked};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (pr->ev0) cudaEventDestroy(pr->ev0);
@@ -491,7 +497,12 @@ int pb_problem_create(const pb_problem_desc* desc, pb_problem** out) {
 #define PB_A(ptr, cnt) if ((rc = dalloc(&pr->ptr, (size_t)(cnt)))) { pb_problem_destroy(pr); return rc; }
   PB_A(frame, m) PB_A(mask, m) PB_A(values, p * n) PB_A(obs, p * n) PB_A(means, n) PB_A(counts, n)
   PB_A(atoms, k * p) PB_A(pi, k) PB_A(usage, k * ld) PB_A(weights, k * ld) PB_A(est, p * n) PB_A(recon, m)
-  PB_A(m_count, k) PB_A(scalars, 1) PB_A(nobs_dev, 1)
+  PB_A(m_count, k) PB_A(scalars, 1) PB_A(nobs_dev, 1) PB_A(out, m) PB_A(prev, m) PB_A(resid, m)
+  if (pr->grid.rank == 2 || pr->grid.rank == 3) {
+    pr->panel_stride = pr->grid.rank == 3 ? pr->grid.tshape[2] : 1;
+    pr->panel_px = m / pr->panel_stride;
+    PB_A(panel, pr->panel_px) PB_A(masked, pr->panel_px)
+  }
 #undef PB_A
   if (cudaStreamCreateWithFlags(&pr->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&pr->ev0) != cudaSuccess || cudaEventCreate(&pr->ev1) != cudaSuccess) {
@@ -524,16 +535,29 @@ static int problem_cold_init(pb_problem* pr) {
 
 int pb_problem_submit_frame(pb_problem* pr, const double* frame_host, const uint8_t* mask_host,
                             double* recon_host) {
-  if (!pr || !frame_host || !mask_host || !recon_host) { set_error("null argument"); return PB_EVALUE; }
+  if (!recon_host) { set_error("null argument"); return PB_EVALUE; }
+  return pb_problem_submit_frame_ex(pr, frame_host, mask_host, recon_host, nullptr, nullptr);
+}
+
+int pb_problem_submit_frame_ex(pb_problem* pr, const double* frame_host, const uint8_t* mask_host,
+                               double* recon_host, uint8_t* panel_host, uint8_t* masked_host) {
+  if (!pr || !frame_host || !mask_host) { set_error("null argument"); return PB_EVALUE; }
+  if ((panel_host || masked_host) && !pr->panel) {
+    set_error("wire panels need a rank-2 or rank-3 tensor (got rank %d)", pr->grid.rank);
+    return PB_EVALUE;
+  }
   const int64_t m = pr->grid.m, n = pr->n;
   cudaStream_t st = pr->stream;
   PB_CUDA_TRY(cudaEventRecord(pr->ev0, st));
   PB_CUDA_TRY(cudaMemcpyAsync(pr->frame, frame_host, m * sizeof(double), cudaMemcpyHostToDevice, st));
-  const bool new_mask = pr->mask_cache.size() != (size_t)m || memcmp(pr->mask_cache.data(), mask_host, m) != 0;
-  if (new_mask) {
+  const bool mask_changed = pr->mask_cache.size() != (size_t)m || memcmp(pr->mask_cache.data(), mask_host, m) != 0;
+  if (mask_changed) {
     pr->mask_cache.assign(mask_host, mask_host + m);
     PB_CUDA_TRY(cudaMemcpyAsync(pr->mask, pr->mask_cache.data(), m, cudaMemcpyHostToDevice, st));
   }
+  // the observed-element index follows the mask (a device-generated mask is
+  // already resident but still needs its index)
+  const bool new_mask = mask_changed || !pr->index_valid;
   int rc = launch_extract(pr->grid, pr->frame, 1, pr->mask, pr->desc.mean_subtract, pr->values, pr->obs, pr->means,
                           pr->counts, st);
   if (rc) return rc;
@@ -560,6 +584,7 @@ int pb_problem_submit_frame(pb_problem* pr, const double* frame_host, const uint
     }
     pr->index.n = n; pr->index.p = pr->p; pr->index.nnz = pr->n_obs;
     if ((rc = pb_build_index(&pr->index, pr->obs, pr->values, pr->counts, st))) return rc;
+    pr->index_valid = true;
   } else {
     if ((rc = pb_index_refresh_values(&pr->index, pr->values, pr->counts, st))) return rc;
   }
@@ -589,10 +614,22 @@ int pb_problem_submit_frame(pb_problem* pr, const double* frame_host, const uint
       if (rc) return rc;
     }
   }
-  rc = launch_reconstitute(pr->grid, pr->est, 1.0f / (float)tail, pr->means, pr->frame, pr->mask,
-                           pr->desc.data_consistency, 1, pr->recon, nullptr, st);
+  // overlap-add (before data consistency), then the fused tail: consistency,
+  // residual map, previous-reconstruction update, uint8 wire panels
+  rc = launch_reconstitute(pr->grid, pr->est, 1.0f / (float)tail, pr->means, pr->frame, pr->mask, 0, 1, pr->recon,
+                           nullptr, st);
   if (rc) return rc;
-  PB_CUDA_TRY(cudaMemcpyAsync(recon_host, pr->recon, m * sizeof(double), cudaMemcpyDeviceToHost, st));
+  LiveFinishArgs lf{};
+  lf.recon = pr->recon; lf.frame = pr->frame; lf.mask = pr->mask; lf.out = pr->out;
+  lf.prev = pr->prev; lf.resid = pr->resid;
+  lf.panel = panel_host ? pr->panel : nullptr;
+  lf.masked = masked_host ? pr->masked : nullptr;
+  lf.m = m; lf.panel_stride = pr->panel_stride; lf.dc = pr->desc.data_consistency; lf.have_prev = pr->have_prev;
+  if ((rc = launch_live_finish(lf, st))) return rc;
+  pr->have_prev = true;
+  if (recon_host) PB_CUDA_TRY(cudaMemcpyAsync(recon_host, pr->out, m * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (panel_host) PB_CUDA_TRY(cudaMemcpyAsync(panel_host, pr->panel, pr->panel_px, cudaMemcpyDeviceToHost, st));
+  if (masked_host) PB_CUDA_TRY(cudaMemcpyAsync(masked_host, pr->masked, pr->panel_px, cudaMemcpyDeviceToHost, st));
   pb_scalars s;
   PB_CUDA_TRY(cudaMemcpyAsync(&s, pr->scalars, sizeof(s), cudaMemcpyDeviceToHost, st));
   PB_CUDA_TRY(cudaEventRecord(pr->ev1, st));
@@ -607,6 +644,56 @@ int pb_problem_submit_frame(pb_problem* pr, const double* frame_host, const uint
 }
 
 float pb_problem_last_gpu_ms(pb_problem* pr) { return pr ? pr->last_ms : 0.f; }
+
+int pb_problem_residual_map(pb_problem* pr, double* host_out) {
+  if (!pr || !host_out) { set_error("null argument"); return PB_EVALUE; }
+  if (!pr->have_prev) { set_error("no frame submitted yet"); return PB_EVALUE; }
+  PB_CUDA_TRY(cudaMemcpyAsync(host_out, pr->resid, (size_t)pr->grid.m * 8, cudaMemcpyDeviceToHost, pr->stream));
+  PB_CUDA_TRY(cudaStreamSynchronize(pr->stream));
+  return PB_OK;
+}
+
+static int adaptive_counts(double ratio, double exploit_fraction, int64_t total, int64_t& budget, int64_t& n_exploit) {
+  if (!(ratio >= 0.0 && ratio <= 1.0)) { set_error("sampling ratio must be in [0, 1], got %g", ratio); return PB_EVALUE; }
+  budget = (int64_t)floor(ratio * (double)total + 0.5);                 // sampling.py:53-56
+  n_exploit = (int64_t)floor(exploit_fraction * (double)budget + 0.5);  // sampling.py:195-197
+  if (n_exploit < 0) n_exploit = 0;
+  if (n_exploit > budget) n_exploit = budget;
+  return PB_OK;
+}
+
+int pb_adaptive_mask(const double* residual, int64_t m, double ratio, double exploit_fraction, uint64_t seed,
+                     int64_t frame_index, uint8_t* mask_out, int32_t* status_out, void* stream) {
+  if (!residual || !mask_out || m < 0) { set_error("bad argument"); return PB_EVALUE; }
+  int64_t budget = 0, n_exploit = 0;
+  int rc = adaptive_counts(ratio, exploit_fraction, m, budget, n_exploit);
+  if (rc) return rc;
+  uint32_t k0, k1;
+  device_key(seed, k0, k1);
+  int status = 0;
+  rc = adaptive_mask(residual, m, budget, n_exploit, k0, k1, (uint64_t)frame_index, mask_out, &status,
+                     (cudaStream_t)stream);
+  if (status_out) *status_out = status;
+  return rc;
+}
+
+int pb_problem_adaptive_mask(pb_problem* pr, double ratio, double exploit_fraction, uint64_t seed,
+                             int64_t frame_index, uint8_t* mask_host, int32_t* status_out) {
+  if (!pr || !mask_host) { set_error("null argument"); return PB_EVALUE; }
+  const int64_t m = pr->grid.m;
+  int status = 1;
+  if (!pr->have_prev) {  // no residual yet (pipeline.py:266-269): all-zero map
+    PB_CUDA_TRY(cudaMemsetAsync(pr->resid, 0, (size_t)m * 8, pr->stream));
+  }
+  int rc = pb_adaptive_mask(pr->resid, m, ratio, exploit_fraction, seed, frame_index, pr->mask, &status, pr->stream);
+  if (rc) return rc;
+  PB_CUDA_TRY(cudaMemcpyAsync(mask_host, pr->mask, (size_t)m, cudaMemcpyDeviceToHost, pr->stream));
+  PB_CUDA_TRY(cudaStreamSynchronize(pr->stream));
+  pr->mask_cache.assign(mask_host, mask_host + m);  // the device copy is current: no re-upload
+  pr->index_valid = false;                           // ... but its index is not built yet
+  if (status_out) *status_out = status;
+  return PB_OK;
+}
 
 int pb_problem_get_dictionary(pb_problem* pr, float* atoms_host, double* pi_host, pb_scalars* scalars_host) {
   if (!pr) { set_error("null problem"); return PB_EVALUE; }

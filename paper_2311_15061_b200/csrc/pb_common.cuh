@@ -79,7 +79,7 @@ __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& n0, fl
 }
 
 // Domains for the device counters (mirror rng.py:14-20).
-enum : uint32_t { kDomInit = 1, kDomAtom = 2, kDomCode = 3, kDomPi = 4, kDomGamma = 5 };
+enum : uint32_t { kDomInit = 1, kDomAtom = 2, kDomCode = 3, kDomPi = 4, kDomGamma = 5, kDomMask = 6 };
 
 // ---------------------------------------------------------------------------
 // Reductions

@@ -1,0 +1,164 @@
+// pb200 — device-resident live-path tail:
+//
+//  k_live_finish     after the overlap-add of a live frame: data consistency
+//                    (patches.py:218-229), the residual map (recon − prev)²
+//                    that drives adaptive sampling (pipeline.py:265-269, on the
+//                    pre-consistency reconstruction), the previous-reconstruction
+//                    update, and the uint8 wire panels of the reconstruction and
+//                    of the masked input (server.py:46-53: round(clip(x,0,1)·255),
+//                    rank-3 tensors show slice 0) — one pass over the frame.
+//  adaptive mask     sampling.py:184-207 on device: the exploit set is the top
+//                    round(f·budget) residuals, ties by lowest flat index (a
+//                    stable descending radix sort of (residual, index) pairs —
+//                    the reference's argsort(-r, kind="stable")); the explore
+//                    set is drawn uniformly without replacement from the rest
+//                    by sorting Philox keys (device stream, keyed by seed and
+//                    frame index; not numpy's Generator.choice stream).
+#include <cub/cub.cuh>
+
+#include "pb_live.cuh"
+
+namespace pb {
+
+__device__ __forceinline__ uint8_t quantize_u8(double x) {
+  // np.round(np.clip(x, 0, 1) * 255): round half to even
+  return (uint8_t)rint(fmin(fmax(x, 0.0), 1.0) * 255.0);
+}
+
+__global__ void __launch_bounds__(256) k_live_finish(LiveFinishArgs a) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < a.m; x += (int64_t)gridDim.x * blockDim.x) {
+    const double r = a.recon[x];
+    const bool obs = a.mask[x] != 0;
+    const double f = a.frame[x];
+    const double out = (a.dc && obs) ? f : r;
+    a.out[x] = out;
+    if (a.resid) {
+      const double dlt = a.have_prev ? r - a.prev[x] : 0.0;
+      a.resid[x] = dlt * dlt;
+      a.prev[x] = r;
+    }
+    if (a.panel || a.masked) {
+      // panel pixel (y, x) of a rank-3 (H, W, C) tensor is element (y, x, 0)
+      if (a.panel_stride == 1 || x % a.panel_stride == 0) {
+        const int64_t px = x / a.panel_stride;
+        if (a.panel) a.panel[px] = quantize_u8(out);
+        if (a.masked) a.masked[px] = quantize_u8(obs ? f : 0.0);
+      }
+    }
+  }
+}
+
+int launch_live_finish(const LiveFinishArgs& a, cudaStream_t st) {
+  const int th = 256;
+  int64_t nb = (a.m + th - 1) / th;
+  if (nb > 148 * 16) nb = 148 * 16;
+  if (nb < 1) nb = 1;
+  k_live_finish<<<(unsigned)nb, th, 0, st>>>(a);
+  PB_LAUNCH_CHECK();
+  return PB_OK;
+}
+
+// --- adaptive-residual mask ------------------------------------------------
+__global__ void k_adaptive_check(const double* __restrict__ r, int64_t m, unsigned* __restrict__ flags) {
+  // flags[0]: any residual > 0, flags[1]: any residual < 0 or NaN
+  unsigned any_pos = 0, bad = 0;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < m; x += (int64_t)gridDim.x * blockDim.x) {
+    const double v = r[x];
+    any_pos |= v > 0.0;
+    bad |= !(v >= 0.0);
+  }
+  any_pos = __any_sync(0xffffffffu, any_pos);
+  bad = __any_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0) {
+    if (any_pos) atomicOr(flags, 1u);
+    if (bad) atomicOr(flags + 1, 1u);
+  }
+}
+
+__global__ void k_iota(int64_t* __restrict__ idx, int64_t m) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < m; x += (int64_t)gridDim.x * blockDim.x)
+    idx[x] = x;
+}
+
+__global__ void k_mark(const int64_t* __restrict__ idx, int64_t cnt, uint8_t* __restrict__ mask) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < cnt; t += (int64_t)gridDim.x * blockDim.x)
+    mask[idx[t]] = 1;
+}
+
+// 64-bit uniform sort key per element; taken elements sort last.
+__global__ void k_explore_keys(const uint8_t* __restrict__ taken, int64_t m, uint32_t k0, uint32_t k1,
+                               uint64_t frame_index, uint64_t* __restrict__ keys) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < m; x += (int64_t)gridDim.x * blockDim.x) {
+    if (taken[x]) {
+      keys[x] = ~0ull;
+    } else {
+      const u32x4 rr = philox4x32_10(u32x4{(uint32_t)x, (uint32_t)(x >> 32), (uint32_t)frame_index,
+                                           ((uint32_t)(frame_index >> 32) & 0xFFFFFFu) | (kDomMask << 24)},
+                                     k0, k1);
+      keys[x] = ((uint64_t)(rr.x >> 1) << 32) | rr.y;  // < 2^63: always below a taken element
+    }
+  }
+}
+
+static unsigned grid_for(int64_t m) {
+  int64_t nb = (m + 255) / 256;
+  if (nb > 148 * 16) nb = 148 * 16;
+  return (unsigned)(nb < 1 ? 1 : nb);
+}
+
+int adaptive_mask(const double* resid, int64_t m, int64_t budget, int64_t n_exploit, uint32_t k0, uint32_t k1,
+                  uint64_t frame_index, uint8_t* mask, int* status, cudaStream_t st) {
+  *status = 0;
+  if (m <= 0) return PB_OK;
+  // scratch: flags, (keys, idx) in/out pairs
+  unsigned* flags = nullptr;
+  double *kd_in = nullptr, *kd_out = nullptr;
+  uint64_t *ku_in = nullptr, *ku_out = nullptr;
+  int64_t *iv_in = nullptr, *iv_out = nullptr;
+  void* temp = nullptr;
+  size_t tb_d = 0, tb_u = 0;
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, tb_d, kd_in, kd_out, iv_in, iv_out, m, 0, 64, st);
+  cub::DeviceRadixSort::SortPairs(nullptr, tb_u, ku_in, ku_out, iv_in, iv_out, m, 0, 64, st);
+  const size_t tb = tb_d > tb_u ? tb_d : tb_u;
+  int rc = PB_OK;
+#define PB_M(ptr, bytes)                                                                   \
+  if (cudaMallocAsync((void**)&ptr, (bytes), st) != cudaSuccess) {                          \
+    set_error("adaptive mask: scratch allocation failed");                                  \
+    rc = PB_ECUDA;                                                                           \
+  }
+  PB_M(flags, 8) if (!rc) PB_M(ku_in, (size_t)m * 8) if (!rc) PB_M(ku_out, (size_t)m * 8)
+  if (!rc) PB_M(iv_in, (size_t)m * 8) if (!rc) PB_M(iv_out, (size_t)m * 8) if (!rc) PB_M(temp, tb ? tb : 16)
+#undef PB_M
+  if (!rc) {
+    kd_out = (double*)ku_out;  // reuse: the double keys are only an output of the first sort
+    unsigned hflags[2] = {0, 0};
+    cudaMemsetAsync(flags, 0, 8, st);
+    k_adaptive_check<<<grid_for(m), 256, 0, st>>>(resid, m, flags);
+    cudaMemcpyAsync(hflags, flags, 8, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) { set_error("adaptive mask: check failed"); rc = PB_ECUDA; }
+    else if (hflags[1]) { set_error("residual map must be non-negative and finite"); rc = PB_EVALUE; }
+    if (!rc) {
+      cudaMemsetAsync(mask, 0, (size_t)m, st);
+      k_iota<<<grid_for(m), 256, 0, st>>>(iv_in, m);
+      if (!hflags[0]) n_exploit = 0;  // all-zero residual: uniform sampling (status 1)
+      *status = hflags[0] ? 0 : 1;
+      if (n_exploit > 0) {
+        cub::DeviceRadixSort::SortPairsDescending(temp, tb_d, resid, kd_out, iv_in, iv_out, m, 0, 64, st);
+        k_mark<<<grid_for(n_exploit), 256, 0, st>>>(iv_out, n_exploit, mask);
+      }
+      const int64_t n_explore = budget - n_exploit;
+      if (n_explore > 0) {
+        k_explore_keys<<<grid_for(m), 256, 0, st>>>(mask, m, k0, k1, frame_index, ku_in);
+        cub::DeviceRadixSort::SortPairs(temp, tb_u, ku_in, ku_out, iv_in, iv_out, m, 0, 64, st);
+        k_mark<<<grid_for(n_explore), 256, 0, st>>>(iv_out, n_explore, mask);
+      }
+      if (cudaGetLastError() != cudaSuccess) { set_error("adaptive mask: kernel launch failed"); rc = PB_ECUDA; }
+    }
+  }
+  void* bufs[] = {flags, ku_in, ku_out, iv_in, iv_out, temp};
+  for (void* b : bufs)
+    if (b) cudaFreeAsync(b, st);
+  return rc;
+}
+
+}  // namespace pb

@@ -1,0 +1,27 @@
+// pb200 — live-path tail kernels (pb_live.cu).
+#pragma once
+#include "pb_common.cuh"
+
+namespace pb {
+
+struct LiveFinishArgs {
+  const double* recon;   // overlap-add reconstruction before data consistency (M)
+  const double* frame;   // the frame (M)
+  const uint8_t* mask;   // sampling mask (M)
+  double* out;           // reconstruction after data consistency (M)
+  double* prev;          // previous frame's reconstruction (M), updated; null: no residual map
+  double* resid;         // (recon - prev)^2 (M) or 0 without a previous frame
+  uint8_t* panel;        // optional uint8 panel of `out` (2-D, or slice 0 of a rank-3 tensor)
+  uint8_t* masked;       // optional uint8 panel of frame * mask
+  int64_t m;
+  int64_t panel_stride;  // 1 for rank 2; C for (H, W, C)
+  int dc;
+  int have_prev;
+};
+
+int launch_live_finish(const LiveFinishArgs& a, cudaStream_t st);
+// sampling.py:184-207 on device; status 1 = all-zero residual (uniform draw)
+int adaptive_mask(const double* resid, int64_t m, int64_t budget, int64_t n_exploit, uint32_t k0, uint32_t k1,
+                  uint64_t frame_index, uint8_t* mask, int* status, cudaStream_t st);
+
+}  // namespace pb

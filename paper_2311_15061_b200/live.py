@@ -1,0 +1,140 @@
+"""Live inpainting of one problem on the device: the hot slice of
+``Pipeline.submit_frame`` (pipeline.py:217-276) behind the C ABI's stateful
+problem (``pb_problem_*``), with the device-resident tail of SURVEY §8f:
+
+* warm start (codes re-burn each frame; dictionary, pi and the precisions carry
+  over, pipeline.py:230-238), device Philox draws;
+* overlap-add, optional data consistency, uint8 wire panels of the
+  reconstruction and of the masked input (server.py:46-53), all on device;
+* the residual map (recon − previous recon)² kept on device (pipeline.py:265-269)
+  and the adaptive-residual sampler on it (sampling.py:184-207: exact exploit
+  set, device-stream explore set).
+
+Inputs and outputs are host NumPy arrays (the C ABI copies them).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .bpfa import Hyperparams
+from .patches import PatchSpec, ShapeError
+
+_VALUE = {_lib.PB_EVALUE: ValueError}
+
+
+@dataclass
+class LiveFrame:
+    reconstruction: np.ndarray           # f64, after data consistency when enabled
+    panel: np.ndarray | None             # uint8 wire panel of the reconstruction
+    masked_panel: np.ndarray | None      # uint8 wire panel of frame * mask
+    gpu_ms: float                        # device time of the frame's GPU work
+
+
+class LiveProblem:
+    """One live problem (ProblemConfig + ProblemHandle of pipeline.py:36-110)."""
+
+    def __init__(self, shape, patch_spec: PatchSpec, hyperparams: Hyperparams | None = None, seed: int = 0,
+                 epochs_per_frame: int = 2, freeze_dict: bool = False, data_consistency: bool = False,
+                 warm_start: bool = True, average_last: int = 1, mean_subtract: bool | None = None):
+        self.shape = tuple(int(m) for m in shape)
+        patch_spec.validate_for(self.shape)
+        hp = hyperparams or Hyperparams()
+        if mean_subtract is None:  # pipeline.py:60-64: on for 2-D patches only
+            mean_subtract = len(patch_spec.patch_shape) == 2
+        d = _lib.ProblemDesc()
+        d.grid = patch_spec.desc(self.shape)
+        d.num_atoms = hp.num_atoms
+        for j, v in enumerate((hp.concentration_a, hp.concentration_b, hp.weight_shape, hp.weight_rate,
+                               hp.noise_shape, hp.noise_rate)):
+            d.hyper[j] = v
+        d.seed = int(seed)
+        d.mean_subtract = int(bool(mean_subtract))
+        d.epochs_per_frame = int(epochs_per_frame)
+        d.freeze_dict = int(bool(freeze_dict))
+        d.data_consistency = int(bool(data_consistency))
+        d.warm_start = int(bool(warm_start))
+        d.average_last = int(average_last)
+        self._lib = _lib.load()
+        self._h = ctypes.c_void_p()
+        _lib.check(self._lib.pb_problem_create(ctypes.byref(d), ctypes.byref(self._h)))
+        self.num_atoms, self.patch_size = hp.num_atoms, patch_spec.patch_size
+        rank = len(self.shape)
+        self.panel_shape = self.shape[:2] if rank in (2, 3) else None
+        self.frames_processed = 0
+
+    def close(self):
+        if self._h:
+            self._lib.pb_problem_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def submit_frame(self, frame, mask, panels: bool = False) -> LiveFrame:
+        frame = np.ascontiguousarray(frame, dtype=np.float64)
+        mask = np.ascontiguousarray(mask, dtype=np.uint8)
+        if frame.shape != self.shape or mask.shape != self.shape:
+            raise ShapeError(f"frame {frame.shape} / mask {mask.shape} do not match the problem shape {self.shape}")
+        out = np.empty(self.shape, dtype=np.float64)
+        pnl = msk = None
+        if panels:
+            if self.panel_shape is None:
+                raise ValueError(f"wire panels must be 2D, got rank {len(self.shape)}")
+            pnl = np.empty(self.panel_shape, dtype=np.uint8)
+            msk = np.empty(self.panel_shape, dtype=np.uint8)
+        _lib.check(self._lib.pb_problem_submit_frame_ex(
+            self._h, frame.ctypes.data, mask.ctypes.data, out.ctypes.data,
+            pnl.ctypes.data if pnl is not None else None, msk.ctypes.data if msk is not None else None), _VALUE)
+        self.frames_processed += 1
+        return LiveFrame(out, pnl, msk, float(self._lib.pb_problem_last_gpu_ms(self._h)))
+
+    def residual_map(self) -> np.ndarray:
+        out = np.empty(self.shape, dtype=np.float64)
+        _lib.check(self._lib.pb_problem_residual_map(self._h, out.ctypes.data))
+        return out
+
+    def adaptive_mask(self, ratio: float, exploit_fraction: float = 0.5, seed: int = 0,
+                      frame_index: int | None = None) -> np.ndarray:
+        """The next mask from the device residual map (sampling.py:184-207)."""
+        fi = self.frames_processed if frame_index is None else int(frame_index)
+        out = np.empty(self.shape, dtype=np.uint8)
+        status = ctypes.c_int32(0)
+        _lib.check(self._lib.pb_problem_adaptive_mask(self._h, float(ratio), float(exploit_fraction), int(seed), fi,
+                                                      out.ctypes.data, ctypes.byref(status)), _VALUE)
+        return out.astype(bool)
+
+    def dictionary(self):
+        atoms = np.empty((self.num_atoms, self.patch_size), dtype=np.float32)
+        pi = np.empty(self.num_atoms, dtype=np.float64)
+        sc = _lib.Scalars()
+        _lib.check(self._lib.pb_problem_get_dictionary(self._h, atoms.ctypes.data, pi.ctypes.data, ctypes.byref(sc)))
+        return atoms, pi, sc
+
+
+def adaptive_mask(residual, ratio: float, exploit_fraction: float = 0.5, seed: int = 0, frame_index: int = 0):
+    """sampling.py:184-207 on device for a residual map (host or CUDA tensor);
+    returns (mask bool ndarray, all_zero flag)."""
+    import torch
+
+    r = torch.as_tensor(np.asarray(residual, dtype=np.float64) if not isinstance(residual, torch.Tensor)
+                        else residual, dtype=torch.float64).to("cuda").contiguous()
+    out = torch.empty(r.shape, dtype=torch.uint8, device="cuda")
+    status = ctypes.c_int32(0)
+    _lib.check(_lib.load().pb_adaptive_mask(r.data_ptr(), r.numel(), float(ratio), float(exploit_fraction), int(seed),
+                                            int(frame_index), out.data_ptr(), ctypes.byref(status),
+                                            torch.cuda.current_stream().cuda_stream), _VALUE)
+    return out.cpu().numpy().astype(bool), bool(status.value)

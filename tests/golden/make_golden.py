@@ -205,15 +205,56 @@ def posterior(pb):
     np.savez_compressed(os.path.join(OUT, "posterior.npz"), **out)
 
 
+def live_tail(pb):
+    """The live path's tail: uint8 wire panels (server.py:46-53), the residual
+    map of consecutive reconstructions (pipeline.py:265-269) and the
+    adaptive-residual sampler (sampling.py:184-207)."""
+    from patchbeam import bpfa
+    from patchbeam.patches import PatchSpec
+    from patchbeam.pipeline import Pipeline, ProblemConfig
+    from patchbeam.sampling import SamplerSpec, run_strategy
+    from patchbeam.server import quantize_panel
+    from patchbeam.sources import SyntheticSource
+
+    rng = np.random.default_rng(515)
+    out = {}
+    # panels: out-of-range values, exact half-steps (round half to even), rank 3
+    p2 = rng.uniform(-0.2, 1.2, size=(9, 13))
+    p2[0, :6] = (np.arange(6) + 0.5) / 255.0
+    p3 = rng.uniform(0, 1, size=(7, 5, 3))
+    for name, pnl in (("q2", p2), ("q3", p3)):
+        out[f"{name}_in"] = pnl
+        out[f"{name}_out"] = quantize_panel(pnl)
+    # adaptive sampler on maps with ties (integer-valued residuals)
+    cases = [((24, 20), 0.25, 0.5, 0), ((16, 16), 0.1, 0.75, 3), ((12, 10, 3), 0.3, 0.4, 1), ((30, 30), 0.2, 1.0, 2)]
+    for i, (shape, ratio, ef, seed) in enumerate(cases):
+        res = rng.integers(0, 6, size=shape).astype(np.float64) * 0.25
+        spec = SamplerSpec(kind="adaptive-residual", ratio=ratio, seed=seed, parameters={"exploit_fraction": ef})
+        out[f"a{i}_res"] = res
+        out[f"a{i}_mask"] = run_strategy(spec, shape, prev_mask=None, residual_map=res, frame_index=i)
+        out[f"a{i}_spec"] = np.array([ratio, ef, seed, i], dtype=np.float64)
+    # residual maps of a 3-frame live run (DC off: the recon is pre-consistency)
+    pipe = Pipeline()
+    cfg = ProblemConfig(name="r", patch_spec=PatchSpec((6, 6)), hyperparams=bpfa.Hyperparams(num_atoms=8),
+                        sampler_spec=SamplerSpec(kind="uniform-random", ratio=0.3, seed=0),
+                        epochs_per_frame=2, seed=0, data_consistency=False)
+    h = pipe.create_problem(cfg)
+    for t, frame in enumerate(SyntheticSource((24, 24), num_frames=3, seed=0).frames()):
+        res = pipe.submit_frame(h, frame)
+        out[f"r{t}_recon"] = res.reconstruction
+        out[f"r{t}_resid"] = h.residual_map.copy()
+    np.savez_compressed(os.path.join(OUT, "live_tail.npz"), **out)
+
+
 def main():
     pb = _import_reference()
     import numba
 
-    extraction_cases(pb)
-    trajectories(pb)
-    masks(pb)
-    live(pb)
-    posterior(pb)
+    only = sys.argv[1:]
+    for name, fn in (("extract", extraction_cases), ("traj", trajectories), ("masks", masks), ("live", live),
+                     ("posterior", posterior), ("live_tail", live_tail)):
+        if not only or name in only:
+            fn(pb)
     meta = {"python": platform.python_version(), "numpy": np.__version__,
             "numba": numba.__version__, "reference": REF,
             "note": "generated by running the reference patchbeam package itself"}

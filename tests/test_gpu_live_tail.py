@@ -1,0 +1,112 @@
+"""Device-resident live tail against the oracle restatement
+(oracle/sampling.py, pinned to the reference by tests/golden/live_tail.npz):
+
+* uint8 wire panels: bit-exact with round(clip(x,0,1)*255) of the returned
+  reconstruction / of frame*mask (rank 2 and slice 0 of rank 3);
+* residual map: bit-exact (recon_t - recon_{t-1})^2, zeros on the first frame;
+* adaptive sampler: budget exact; exploit set bit-exact with the reference's
+  stable argsort (with exploit_fraction = 1 the mask equals the reference's
+  mask); the explore part is a device stream — checked for disjointness,
+  count and uniformity (each candidate's hit rate within 5 sigma);
+* errors: negative residuals and non-2D/3D panels refuse.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import sampling as osm
+from paper_2311_15061_b200 import _lib
+from paper_2311_15061_b200 import inputs
+from paper_2311_15061_b200.bpfa import Hyperparams
+from paper_2311_15061_b200.live import LiveProblem, adaptive_mask
+from paper_2311_15061_b200.patches import PatchSpec
+
+pytestmark = pytest.mark.gpu
+
+
+def test_panels_and_residual_map(cuda_device):
+    frames = inputs.synthetic_frames((24, 24), 3, seed=0)
+    mask = inputs.make_mask((24, 24), 0.3, "uniform-random", 0)
+    with LiveProblem((24, 24), PatchSpec((6, 6)), Hyperparams(num_atoms=8), epochs_per_frame=2) as lp:
+        prev = None
+        for f in frames:
+            fr = lp.submit_frame(f, mask, panels=True)
+            assert np.array_equal(fr.panel, osm.quantize_panel(fr.reconstruction))
+            assert np.array_equal(fr.masked_panel, osm.quantize_panel(f * mask))
+            assert np.array_equal(lp.residual_map(), osm.residual_map(fr.reconstruction, prev))
+            prev = fr.reconstruction
+            assert fr.gpu_ms > 0
+
+
+def test_data_consistency_and_rank3_panel(cuda_device):
+    rng = np.random.default_rng(3)
+    cube = rng.random((12, 10, 3))
+    mask = rng.random(cube.shape) < 0.4
+    with LiveProblem(cube.shape, PatchSpec((4, 4, 3)), Hyperparams(num_atoms=6), data_consistency=True) as lp:
+        fr = lp.submit_frame(cube, mask, panels=True)
+        assert np.array_equal(fr.reconstruction[mask], cube[mask])
+        assert fr.panel.shape == (12, 10)
+        assert np.array_equal(fr.panel, osm.quantize_panel(fr.reconstruction))
+    with LiveProblem((40,), PatchSpec((5,)), Hyperparams(num_atoms=4)) as lp:
+        with pytest.raises(ValueError):
+            lp.submit_frame(np.zeros(40), np.ones(40, bool), panels=True)
+
+
+@pytest.mark.parametrize("case", [0, 1, 2, 3])
+def test_adaptive_exploit_matches_reference(golden, cuda_device, case):
+    g = golden("live_tail.npz")
+    ratio, ef, seed, fi = g[f"a{case}_spec"]
+    res, ref_mask = g[f"a{case}_res"], g[f"a{case}_mask"]
+    mask, all_zero = adaptive_mask(res, ratio, ef, int(seed), int(fi))
+    budget, n_exploit = osm.adaptive_split(ratio, ef, res.size)
+    assert not all_zero and mask.sum() == budget == ref_mask.sum()
+    ex = osm.adaptive_exploit(res, ratio, ef)
+    assert mask.ravel()[ex].all()
+    if n_exploit == budget:            # pure exploit: the whole mask is reference-exact
+        assert np.array_equal(mask, ref_mask)
+
+
+def test_adaptive_explore_is_uniform_and_keyed(cuda_device):
+    rng = np.random.default_rng(11)
+    res = rng.random((20, 20)) * (rng.random((20, 20)) < 0.5)
+    ex = set(osm.adaptive_exploit(res, 0.2, 0.5).tolist())
+    budget, n_exploit = osm.adaptive_split(0.2, 0.5, res.size)
+    hits = np.zeros(res.size)
+    trials = 300
+    for t in range(trials):
+        m, _ = adaptive_mask(res, 0.2, 0.5, seed=7, frame_index=t)
+        flat = np.flatnonzero(m.ravel())
+        assert len(flat) == budget and ex <= set(flat.tolist())
+        hits[flat] += 1
+    free = np.array([i for i in range(res.size) if i not in ex])
+    p = (budget - n_exploit) / len(free)
+    rate = hits[free] / trials
+    assert np.all(np.abs(rate - p) <= 5 * np.sqrt(p * (1 - p) / trials))
+    a, _ = adaptive_mask(res, 0.2, 0.5, seed=7, frame_index=3)
+    b, _ = adaptive_mask(res, 0.2, 0.5, seed=7, frame_index=3)
+    c, _ = adaptive_mask(res, 0.2, 0.5, seed=8, frame_index=3)
+    assert np.array_equal(a, b) and not np.array_equal(a, c)
+
+
+def test_adaptive_zero_and_invalid(cuda_device):
+    m, all_zero = adaptive_mask(np.zeros((16, 16)), 0.25, 0.5, seed=1)
+    assert all_zero and m.sum() == osm.sample_budget(0.25, 256)
+    with pytest.raises(ValueError):
+        adaptive_mask(-np.ones((4, 4)), 0.25)
+    with pytest.raises(ValueError):
+        adaptive_mask(np.ones((4, 4)), 1.5)
+
+
+def test_problem_adaptive_loop(cuda_device):
+    """Frame t's mask comes from frame t-1's residual map, on device."""
+    frames = inputs.synthetic_frames((32, 32), 4, seed=2)
+    with LiveProblem((32, 32), PatchSpec((6, 6)), Hyperparams(num_atoms=8)) as lp:
+        mask = lp.adaptive_mask(0.3, 0.5, seed=0)           # no residual yet: uniform
+        assert mask.sum() == osm.sample_budget(0.3, 1024)
+        for f in frames:
+            lp.submit_frame(f, mask)
+            res = lp.residual_map()
+            nxt = lp.adaptive_mask(0.3, 0.5, seed=0)
+            if res.any():
+                assert nxt.ravel()[osm.adaptive_exploit(res, 0.3, 0.5)].all()
+            mask = nxt

@@ -100,3 +100,24 @@ def test_input_generators_match_reference(golden):
     assert np.array_equal(inputs.synthetic_texture((64, 64), seed=0), g["tex_64_s0"])
     assert np.array_equal(inputs.synthetic_texture((40, 56), seed=3, phase=0.45),
                           g["tex_40x56_s3_ph"])
+
+
+def test_live_tail_oracle_matches_reference(golden):
+    """Wire panels, residual maps and the adaptive sampler's exploit set
+    (oracle/sampling.py) against the reference's own outputs."""
+    from oracle import sampling as osm
+
+    g = golden("live_tail.npz")
+    for name in ("q2", "q3"):
+        assert np.array_equal(osm.quantize_panel(g[f"{name}_in"]), g[f"{name}_out"]), name
+    prev = None
+    for t in range(3):
+        assert np.array_equal(osm.residual_map(g[f"r{t}_recon"], prev), g[f"r{t}_resid"]), t
+        prev = g[f"r{t}_recon"]
+    for i in range(4):
+        ratio, ef, _, _ = g[f"a{i}_spec"]
+        res, mask = g[f"a{i}_res"], g[f"a{i}_mask"]
+        budget, n_exploit = osm.adaptive_split(ratio, ef, res.size)
+        assert int(mask.sum()) == budget
+        ex = osm.adaptive_exploit(res, ratio, ef)
+        assert len(ex) == n_exploit and mask.ravel()[ex].all(), i   # the exploit set is in the reference mask
