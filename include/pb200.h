@@ -268,6 +268,13 @@ int pb_problem_residual_map(pb_problem* pr, double* host_out);
  * device mask.  status 1 = all-zero map (uniform device draw). */
 int pb_problem_adaptive_mask(pb_problem* pr, double ratio, double exploit_fraction, uint64_t seed,
                              int64_t frame_index, uint8_t* mask_host, int32_t* status_out);
+/* Adopt a dictionary (Pipeline._install_dictionary, pipeline.py:145-167): atoms
+ * (K,P) f32 and pi (K) of THIS problem's K and P (reshape first with
+ * bpfa.transfer_dictionary).  Before the first frame it is pending and seeds the
+ * cold start (install_dictionary semantics, bpfa.py:355-376: precisions at the
+ * prior means); afterwards it replaces the dictionary and keeps the precisions
+ * and the epoch counter.  freeze: 0/1 sets freeze_dict, -1 keeps it. */
+int pb_problem_install_dictionary(pb_problem* pr, const float* atoms_host, const double* pi_host, int32_t freeze);
 /* Device-side timing of the last submit_frame's GPU work (ms). */
 float pb_problem_last_gpu_ms(pb_problem* pr);
 /* Current dictionary (K,P) f32 and scalars, copied to host. */

@@ -445,6 +445,8 @@ struct pb_problem {
   int64_t panel_px = 0, panel_stride = 1;  // wire panel: rank 2, or slice 0 of rank 3
   bool have_prev = false;
   bool index_valid = false;  // the observed-element index matches the device mask
+  std::vector<float> pending_atoms;   // installed before the first frame (pipeline.py:155-157)
+  std::vector<double> pending_pi;
   pb_scalars* scalars = nullptr;
   unsigned long long* nobs_dev = nullptr;
   void* ws = nullptr;
@@ -520,9 +522,16 @@ static int problem_cold_init(pb_problem* pr) {
   // matters with freeze_dict; see infer() in bpfa.py of this package.)
   uint32_t k0, k1;
   device_key(pr->desc.seed, k0, k1);
-  int rc = launch_prior_atoms(pr->atoms, pr->k, pr->p, k0, k1, pr->stream);
-  if (rc) return rc;
   std::vector<double> pi(pr->k, pr->desc.hyper[0] / (pr->desc.hyper[0] + pr->desc.hyper[1]));
+  std::vector<float> atoms;
+  if (!pr->pending_atoms.empty()) {  // infer(initial_dict=...) -> install_dictionary (bpfa.py:355-376)
+    atoms.swap(pr->pending_atoms);
+    pi.swap(pr->pending_pi);
+    PB_CUDA_TRY(cudaMemcpyAsync(pr->atoms, atoms.data(), atoms.size() * 4, cudaMemcpyHostToDevice, pr->stream));
+  } else {
+    int rc = launch_prior_atoms(pr->atoms, pr->k, pr->p, k0, k1, pr->stream);
+    if (rc) return rc;
+  }
   PB_CUDA_TRY(cudaMemcpyAsync(pr->pi, pi.data(), pr->k * sizeof(double), cudaMemcpyHostToDevice, pr->stream));
   pb_scalars s{};
   s.gamma_s = fmax(pr->desc.hyper[2] / pr->desc.hyper[3], 1e-12);
@@ -644,6 +653,23 @@ int pb_problem_submit_frame_ex(pb_problem* pr, const double* frame_host, const u
 }
 
 float pb_problem_last_gpu_ms(pb_problem* pr) { return pr ? pr->last_ms : 0.f; }
+
+int pb_problem_install_dictionary(pb_problem* pr, const float* atoms_host, const double* pi_host, int32_t freeze) {
+  if (!pr || !atoms_host || !pi_host) { set_error("null argument"); return PB_EVALUE; }
+  if (freeze == 0 || freeze == 1) pr->desc.freeze_dict = freeze;
+  const size_t kp = (size_t)pr->k * pr->p;
+  if (!pr->have_state) {  // pending until the first frame (pipeline.py:155-157)
+    pr->pending_atoms.assign(atoms_host, atoms_host + kp);
+    pr->pending_pi.assign(pi_host, pi_host + pr->k);
+    return PB_OK;
+  }
+  // replace the dictionary; codes reset every frame, precisions and epoch carry
+  // over (pipeline.py:158-167)
+  PB_CUDA_TRY(cudaMemcpyAsync(pr->atoms, atoms_host, kp * 4, cudaMemcpyHostToDevice, pr->stream));
+  PB_CUDA_TRY(cudaMemcpyAsync(pr->pi, pi_host, (size_t)pr->k * 8, cudaMemcpyHostToDevice, pr->stream));
+  PB_CUDA_TRY(cudaStreamSynchronize(pr->stream));  // host buffers may be released on return
+  return PB_OK;
+}
 
 int pb_problem_residual_map(pb_problem* pr, double* host_out) {
   if (!pr || !host_out) { set_error("null argument"); return PB_EVALUE; }

@@ -21,7 +21,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .bpfa import Hyperparams
+from .bpfa import Dictionary, Hyperparams, transfer_dictionary
 from .patches import PatchSpec, ShapeError
 
 _VALUE = {_lib.PB_EVALUE: ValueError}
@@ -63,6 +63,7 @@ class LiveProblem:
         self._h = ctypes.c_void_p()
         _lib.check(self._lib.pb_problem_create(ctypes.byref(d), ctypes.byref(self._h)))
         self.num_atoms, self.patch_size = hp.num_atoms, patch_spec.patch_size
+        self.patch_shape = tuple(int(b) for b in patch_spec.patch_shape)
         rank = len(self.shape)
         self.panel_shape = self.shape[:2] if rank in (2, 3) else None
         self.frames_processed = 0
@@ -116,6 +117,23 @@ class LiveProblem:
         _lib.check(self._lib.pb_problem_adaptive_mask(self._h, float(ratio), float(exploit_fraction), int(seed), fi,
                                                       out.ctypes.data, ctypes.byref(status)), _VALUE)
         return out.astype(bool)
+
+    def install_dictionary(self, dictionary, freeze: bool | None = None) -> None:
+        """Pipeline._install_dictionary (pipeline.py:145-167): the dictionary is
+        reshaped to this problem's patch shape (bpfa.transfer_dictionary,
+        bpfa.py:417-458); codes reset; pending until the first frame."""
+        moved = transfer_dictionary(dictionary, self.patch_shape, self.shape)
+        if moved.num_atoms != self.num_atoms:
+            raise ShapeError(f"dictionary has {moved.num_atoms} atoms, the problem {self.num_atoms}")
+        atoms = np.ascontiguousarray(np.asarray(moved.atoms, dtype=np.float32))
+        pi = np.ascontiguousarray(np.asarray(moved.pi, dtype=np.float64))
+        _lib.check(self._lib.pb_problem_install_dictionary(self._h, atoms.ctypes.data, pi.ctypes.data,
+                                                           -1 if freeze is None else int(bool(freeze))), _VALUE)
+
+    def snapshot_dictionary(self) -> Dictionary:
+        """Pipeline.snapshot_dictionary (pipeline.py:280-286), on the host."""
+        atoms, pi, _ = self.dictionary()
+        return Dictionary(atoms.astype(np.float64), pi, self.patch_shape)
 
     def dictionary(self):
         atoms = np.empty((self.num_atoms, self.patch_size), dtype=np.float32)

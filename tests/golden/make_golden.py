@@ -246,13 +246,25 @@ def live_tail(pb):
     np.savez_compressed(os.path.join(OUT, "live_tail.npz"), **out)
 
 
+def dict_files(pb):
+    """SADF dictionary files written by the reference (formats.py:147-161)."""
+    from patchbeam.bpfa import Dictionary
+    from patchbeam.formats import write_dict
+
+    rng = np.random.default_rng(99)
+    d = Dictionary(atoms=rng.standard_normal((6, 12)), pi=rng.uniform(0, 1, 6), patch_shape=(3, 4))
+    write_dict(os.path.join(OUT, "dict_k6_3x4.sadf"), d)
+    write_dict(os.path.join(OUT, "dict_k6_3x4_nopi.sadf"), d, include_pi=False)
+    np.savez_compressed(os.path.join(OUT, "dict_src.npz"), atoms=d.atoms, pi=d.pi)
+
+
 def main():
     pb = _import_reference()
     import numba
 
     only = sys.argv[1:]
     for name, fn in (("extract", extraction_cases), ("traj", trajectories), ("masks", masks), ("live", live),
-                     ("posterior", posterior), ("live_tail", live_tail)):
+                     ("posterior", posterior), ("live_tail", live_tail), ("dicts", dict_files)):
         if not only or name in only:
             fn(pb)
     meta = {"python": platform.python_version(), "numpy": np.__version__,

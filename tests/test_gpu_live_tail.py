@@ -110,3 +110,30 @@ def test_problem_adaptive_loop(cuda_device):
             if res.any():
                 assert nxt.ravel()[osm.adaptive_exploit(res, 0.3, 0.5)].all()
             mask = nxt
+
+
+def test_install_dictionary_pending_and_live(cuda_device, tmp_path):
+    """Pipeline._install_dictionary semantics (pipeline.py:145-167) through a
+    SADF round trip: pending before the first frame (frozen: the sweep keeps it
+    bit-exact), and a live replacement keeps the epoch counter."""
+    from paper_2311_15061_b200.bpfa import Dictionary
+    from paper_2311_15061_b200.formats import read_dict, write_dict
+
+    rng = np.random.default_rng(4)
+    d = Dictionary(rng.standard_normal((8, 36)).astype(np.float32).astype(np.float64), rng.uniform(0.1, 0.9, 8),
+                   (6, 6))
+    write_dict(tmp_path / "d.sadf", d)
+    d = read_dict(tmp_path / "d.sadf")
+    frames = inputs.synthetic_frames((24, 24), 2, seed=1)
+    mask = inputs.make_mask((24, 24), 0.3, "uniform-random", 1)
+    with LiveProblem((24, 24), PatchSpec((6, 6)), Hyperparams(num_atoms=8), epochs_per_frame=2) as lp:
+        lp.install_dictionary(d, freeze=True)                  # pending: seeds the cold start
+        lp.submit_frame(frames[0], mask)
+        atoms, pi, sc = lp.dictionary()
+        assert np.array_equal(atoms, d.atoms.astype(np.float32)) and sc.epoch == 2
+        lp.install_dictionary(lp.snapshot_dictionary(), freeze=False)   # live: epoch carries over
+        lp.submit_frame(frames[1], mask)
+        atoms2, _, sc2 = lp.dictionary()
+        assert sc2.epoch == 4 and not np.array_equal(atoms2, atoms)
+        with pytest.raises(Exception):
+            lp.install_dictionary(Dictionary(np.zeros((5, 36)), np.full(5, 0.5), (6, 6)))
