@@ -11,6 +11,7 @@
 #include "../../include/pb200.h"
 #include "pb_compact.cuh"
 #include "pb_live.cuh"
+#include "pb_compose_tc.cuh"
 
 namespace pb {
 
@@ -442,6 +443,7 @@ struct pb_problem {
   int32_t *counts = nullptr, *m_count = nullptr;
   double *pi = nullptr, *recon = nullptr, *out = nullptr, *prev = nullptr, *resid = nullptr;
   uint8_t *panel = nullptr, *masked = nullptr;
+  float* bpack = nullptr;  // tensor-core compose scratch (packed D^T)
   int64_t panel_px = 0, panel_stride = 1;  // wire panel: rank 2, or slice 0 of rank 3
   bool have_prev = false;
   bool index_valid = false;  // the observed-element index matches the device mask
@@ -473,7 +475,7 @@ int pb_problem_destroy(pb_problem* pr) {
   if (!pr) return PB_OK;
   void* bufs[] = {pr->frame, pr->mask, pr->values, pr->means, pr->atoms, pr->weights, pr->est, pr->obs, pr->usage,
                   pr->counts, pr->m_count, pr->pi, pr->recon, pr->scalars, pr->nobs_dev, pr->ws, pr->index.buffer,
-                  pr->out, pr->prev, pr->resid, pr->panel, pr->masked};
+                  pr->out, pr->prev, pr->resid, pr->panel, pr->masked, pr->bpack};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (pr->ev0) cudaEventDestroy(pr->ev0);
@@ -500,6 +502,7 @@ int pb_problem_create(const pb_problem_desc* desc, pb_problem** out) {
   PB_A(frame, m) PB_A(mask, m) PB_A(values, p * n) PB_A(obs, p * n) PB_A(means, n) PB_A(counts, n)
   PB_A(atoms, k * p) PB_A(pi, k) PB_A(usage, k * ld) PB_A(weights, k * ld) PB_A(est, p * n) PB_A(recon, m)
   PB_A(m_count, k) PB_A(scalars, 1) PB_A(nobs_dev, 1) PB_A(out, m) PB_A(prev, m) PB_A(resid, m)
+  if (compose_tc_supported((int)p) && !getenv("PB_COMPOSE_TC_OFF")) PB_A(bpack, compose_tc_scratch_bytes((int)p, (int)k) / 4)
   if (pr->grid.rank == 2 || pr->grid.rank == 3) {
     pr->panel_stride = pr->grid.rank == 3 ? pr->grid.tshape[2] : 1;
     pr->panel_px = m / pr->panel_stride;
@@ -618,8 +621,12 @@ int pb_problem_submit_frame_ex(pb_problem* pr, const double* frame_host, const u
     d.resid_mode = e == 0 ? PB_RESID_FROM_VALUES : PB_RESID_CARRY;  // codes were just reset
     if ((rc = run_epoch(&d, pr->m_count, st))) return rc;
     if (e >= epochs - tail) {
-      rc = launch_accumulate_atoms(false, nullptr, nullptr, pr->usage, pr->weights, pr->atoms, pr->est, n, pr->p,
-                                   pr->k, e > epochs - tail ? 1 : 0, pr->ld, st);
+      if (pr->bpack)  // tensor-core compose with the problem's packed-D scratch
+        rc = launch_compose_tc(pr->usage, pr->weights, pr->ld, pr->atoms, pr->p, pr->k, n, pr->est,
+                               e > epochs - tail ? 1 : 0, st, pr->bpack);
+      else
+        rc = launch_accumulate_atoms(false, nullptr, nullptr, pr->usage, pr->weights, pr->atoms, pr->est, n, pr->p,
+                                     pr->k, e > epochs - tail ? 1 : 0, pr->ld, st);
       if (rc) return rc;
     }
   }
