@@ -76,13 +76,16 @@ def extraction_cases(pb):
 
 
 def _traj(pb, name, img_shape, patch, ratio, kind, k, epochs, seed, mask_seed,
-          mean_subtract=True, freeze=False, init_mode="data", initial=False, average_last=1):
+          mean_subtract=True, freeze=False, init_mode="data", initial=False, average_last=1, cube_bands=0):
     from patchbeam import bpfa
     from patchbeam.patches import PatchSpec, extract_patches
     from patchbeam.sampling import SamplerSpec, make_mask
     from patchbeam.sources import synthetic_texture
 
     img = synthetic_texture(img_shape, seed=mask_seed)
+    if cube_bands:  # hyperspectral-like cube (configs[3] shape class): texture x smooth spectrum
+        spec = 0.5 + 0.5 * np.sin(np.linspace(0, 3 * np.pi, cube_bands))
+        img = img[:, :, None] * spec[None, None, :]
     mask = make_mask(SamplerSpec(kind=kind, ratio=ratio, seed=mask_seed), img.shape)
     pm = extract_patches(img, mask, PatchSpec(patch), mean_subtract=mean_subtract)
     hp = bpfa.Hyperparams(num_atoms=k)
@@ -127,6 +130,8 @@ def trajectories(pb):
     _traj(pb, "avg", (16, 20), (3, 3), 0.5, "uniform-random", 5, 4, 13, 6,
           mean_subtract=False, average_last=2, init_mode="prior")
     _traj(pb, "cfg1crop", (48, 48), (8, 8), 0.25, "uniform-random", 16, 3, 0, 0)
+    _traj(pb, "cube", (14, 16), (4, 4, 3), 0.2, "uniform-random", 8, 3, 21, 8, mean_subtract=False,
+          cube_bands=6)
 
 
 def masks(pb):

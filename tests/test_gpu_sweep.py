@@ -93,7 +93,7 @@ def _compare_epoch(name, gstate, ref: ob.State, n, k):
     return nflip
 
 
-@pytest.mark.parametrize("name", ["small", "linehop", "cfg1crop", "frozen", "avg"])
+@pytest.mark.parametrize("name", ["small", "linehop", "cfg1crop", "frozen", "avg", "cube"])
 def test_teacher_forced_epochs_replay_mode(golden, cuda_device, name):
     """Each epoch starts from the REFERENCE state; both sides consume the
     reference's own draw streams (replay mode)."""

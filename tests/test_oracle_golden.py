@@ -37,7 +37,7 @@ def test_strict_coverage_error(golden):
         op.reconstitute(pm, pm.values, strict=True)
 
 
-@pytest.mark.parametrize("name", ["small", "linehop", "frozen", "avg", "cfg1crop"])
+@pytest.mark.parametrize("name", ["small", "linehop", "frozen", "avg", "cfg1crop", "cube"])
 def test_trajectory_bit_exact(golden, name):
     g = golden(f"traj_{name}.npz")
     patch = tuple(int(b) for b in g["patch"])
