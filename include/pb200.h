@@ -227,6 +227,15 @@ int pb_dict_profile(int32_t enable, double* slots_ns_out /* [12] or NULL */);
 int pb_adaptive_mask(const double* residual, int64_t m, double ratio, double exploit_fraction, uint64_t seed,
                      int64_t frame_index, uint8_t* mask_out, int32_t* status_out, void* stream);
 
+/* ---- dictionary atlas for the console (server.py:84-120), on device ----
+ * Canvas (height, width) = (g*B0 + g-1, g*B1 + g-1), g = ceil(sqrt(K)); rank-1
+ * patches render as one row, rank-3 as slice 0 of the last axis, rank 4 refuses.
+ * atoms (K,P) f32, pi (K) f64 device; canvas f64 and/or canvas_u8
+ * (round(clip(x,0,1)*255)) device outputs (either may be NULL). */
+int pb_atlas_shape(int32_t k, int32_t rank, const int32_t* patch_shape, int64_t* height, int64_t* width);
+int pb_render_atlas(const float* atoms, const double* pi, int32_t k, int32_t rank, const int32_t* patch_shape,
+                    double* canvas, uint8_t* canvas_u8, void* stream);
+
 /* ---- stateful problem (C-ABI with HOST buffers; the live submit_frame slice,
  *      pipeline.py:217-251).  Owns all device buffers. ---- */
 typedef struct pb_problem pb_problem;
@@ -275,6 +284,9 @@ int pb_problem_adaptive_mask(pb_problem* pr, double ratio, double exploit_fracti
  * prior means); afterwards it replaces the dictionary and keeps the precisions
  * and the epoch counter.  freeze: 0/1 sets freeze_dict, -1 keeps it. */
 int pb_problem_install_dictionary(pb_problem* pr, const float* atoms_host, const double* pi_host, int32_t freeze);
+/* The problem's current dictionary atlas as a uint8 wire panel (host buffer of
+ * pb_atlas_shape's size). */
+int pb_problem_render_atlas(pb_problem* pr, uint8_t* canvas_u8_host);
 /* Device-side timing of the last submit_frame's GPU work (ms). */
 float pb_problem_last_gpu_ms(pb_problem* pr);
 /* Current dictionary (K,P) f32 and scalars, copied to host. */

@@ -47,3 +47,35 @@ def adaptive_exploit(residual: np.ndarray, ratio: float, exploit_fraction: float
     r = np.asarray(residual, dtype=np.float64).ravel()
     _, n_exploit = adaptive_split(ratio, exploit_fraction, r.size)
     return np.argsort(-r, kind="stable")[:n_exploit]
+
+
+def render_dictionary_atlas(atoms: np.ndarray, pi: np.ndarray, patch_shape) -> np.ndarray:
+    """server.py:84-120: atoms min-max normalised (constant -> 0.5), ordered by
+    descending pi (stable), tiled into a ceil(sqrt(K)) grid with mid-grey
+    1-pixel separators and empty cells."""
+    import math
+
+    shape = tuple(int(b) for b in patch_shape)
+    k = atoms.shape[0]
+    a = np.asarray(atoms, dtype=np.float64).reshape((k,) + shape)
+    if len(shape) == 3:
+        a = a[:, :, :, 0]
+    elif len(shape) == 1:
+        a = a[:, None, :]
+    elif len(shape) != 2:
+        raise ValueError(f"cannot render atlas for patch rank {len(shape)}")
+    b0, b1 = a.shape[1], a.shape[2]
+    lo = a.min(axis=(1, 2), keepdims=True)
+    hi = a.max(axis=(1, 2), keepdims=True)
+    span = hi - lo
+    flat = span[:, 0, 0] == 0
+    with np.errstate(invalid="ignore", divide="ignore"):
+        tiles = (a - lo) / span
+    tiles[flat] = 0.5
+    order = np.argsort(-np.asarray(pi), kind="stable")
+    grid = math.ceil(math.sqrt(k))
+    canvas = np.full((grid * b0 + grid - 1, grid * b1 + grid - 1), 0.5, dtype=np.float64)
+    for slot, idx in enumerate(order):
+        r, c = divmod(slot, grid)
+        canvas[r * (b0 + 1):r * (b0 + 1) + b0, c * (b1 + 1):c * (b1 + 1) + b1] = tiles[idx]
+    return canvas

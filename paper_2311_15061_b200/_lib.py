@@ -106,6 +106,9 @@ SIGNATURES = {
     "pb_adaptive_mask": (c_i32, [c_vp, c_i64, ctypes.c_double, ctypes.c_double, ctypes.c_uint64, c_i64, c_vp,
                                  ctypes.POINTER(c_i32), c_vp]),
     "pb_problem_install_dictionary": (c_i32, [c_vp, c_vp, c_vp, c_i32]),
+    "pb_problem_render_atlas": (c_i32, [c_vp, c_vp]),
+    "pb_atlas_shape": (c_i32, [c_i32, c_i32, c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
+    "pb_render_atlas": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "pb_problem_last_gpu_ms": (c_f32, [c_vp]),
     "pb_problem_get_dictionary": (c_i32, [c_vp, c_vp, c_vp, ctypes.POINTER(Scalars)]),
 }

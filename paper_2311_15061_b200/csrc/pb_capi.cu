@@ -661,6 +661,38 @@ int pb_problem_submit_frame_ex(pb_problem* pr, const double* frame_host, const u
 
 float pb_problem_last_gpu_ms(pb_problem* pr) { return pr ? pr->last_ms : 0.f; }
 
+int pb_atlas_shape(int32_t k, int32_t rank, const int32_t* patch_shape, int64_t* height, int64_t* width) {
+  if (!patch_shape || !height || !width) { set_error("null argument"); return PB_EVALUE; }
+  int b0, b1, inner, grid;
+  return atlas_geometry(k, rank, patch_shape, b0, b1, inner, grid, *height, *width);
+}
+
+int pb_render_atlas(const float* atoms, const double* pi, int32_t k, int32_t rank, const int32_t* patch_shape,
+                    double* canvas, uint8_t* canvas_u8, void* stream) {
+  if (!atoms || !pi || !patch_shape || (!canvas && !canvas_u8)) { set_error("null argument"); return PB_EVALUE; }
+  return launch_atlas(atoms, pi, k, rank, patch_shape, canvas, canvas_u8, (cudaStream_t)stream);
+}
+
+int pb_problem_render_atlas(pb_problem* pr, uint8_t* canvas_u8_host) {
+  if (!pr || !canvas_u8_host) { set_error("null argument"); return PB_EVALUE; }
+  int32_t shape[4];
+  for (int d = 0; d < pr->grid.rank; ++d) shape[d] = pr->grid.bshape[d];
+  int b0, b1, inner, grid;
+  int64_t h, w;
+  int rc = atlas_geometry(pr->k, pr->grid.rank, shape, b0, b1, inner, grid, h, w);
+  if (rc) return rc;
+  uint8_t* dev = nullptr;
+  PB_CUDA_TRY(cudaMallocAsync((void**)&dev, (size_t)(h * w), pr->stream));
+  rc = launch_atlas(pr->atoms, pr->pi, pr->k, pr->grid.rank, shape, nullptr, dev, pr->stream);
+  if (!rc && cudaMemcpyAsync(canvas_u8_host, dev, (size_t)(h * w), cudaMemcpyDeviceToHost, pr->stream) != cudaSuccess) {
+    set_error("atlas copy failed");
+    rc = PB_ECUDA;
+  }
+  cudaFreeAsync(dev, pr->stream);
+  if (cudaStreamSynchronize(pr->stream) != cudaSuccess && !rc) { set_error("atlas failed"); rc = PB_ECUDA; }
+  return rc;
+}
+
 int pb_problem_install_dictionary(pb_problem* pr, const float* atoms_host, const double* pi_host, int32_t freeze) {
   if (!pr || !atoms_host || !pi_host) { set_error("null argument"); return PB_EVALUE; }
   if (freeze == 0 || freeze == 1) pr->desc.freeze_dict = freeze;

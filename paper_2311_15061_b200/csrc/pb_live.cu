@@ -161,4 +161,85 @@ int adaptive_mask(const double* resid, int64_t m, int64_t budget, int64_t n_expl
   return rc;
 }
 
+// --- dictionary atlas (server.py:84-120) -----------------------------------
+// Atoms tiled into a ceil(sqrt(K)) grid, highest activation probability first
+// (ties by atom index), each min-max normalised on its own (constant atoms at
+// 0.5), 1-pixel mid-grey separators and empty cells.  One CTA; the order is a
+// rank count over pi (K <= a few thousand).
+__global__ void k_atlas(const float* __restrict__ atoms, const double* __restrict__ pi, int k, int b0, int b1,
+                        int inner, int p, int grid, int64_t h, int64_t w, double* __restrict__ canvas,
+                        uint8_t* __restrict__ canvas_u8) {
+  extern __shared__ int slot_atom[];   // [grid*grid]: atom shown in each slot, -1 = empty
+  float* lo = (float*)(slot_atom + grid * grid);
+  float* hi = lo + k;
+  for (int s = threadIdx.x; s < grid * grid; s += blockDim.x) slot_atom[s] = -1;
+  __syncthreads();
+  for (int a = threadIdx.x; a < k; a += blockDim.x) {
+    const double pa = pi[a];
+    int rank = 0;   // stable argsort of -pi
+    for (int b = 0; b < k; ++b) {
+      const double pb = pi[b];
+      rank += (pb > pa) || (pb == pa && b < a);
+    }
+    slot_atom[rank] = a;
+    float mn = INFINITY, mx = -INFINITY;
+    for (int y = 0; y < b0; ++y)
+      for (int x = 0; x < b1; ++x) {
+        const float v = atoms[(int64_t)a * p + (int64_t)(y * b1 + x) * inner];
+        mn = fminf(mn, v);
+        mx = fmaxf(mx, v);
+      }
+    lo[a] = mn;
+    hi[a] = mx;
+  }
+  __syncthreads();
+  for (int64_t t = threadIdx.x; t < h * w; t += blockDim.x) {
+    const int64_t y = t / w, x = t - y * w;
+    double v = 0.5;
+    const int64_t r = y / (b0 + 1), c = x / (b1 + 1);
+    const int ty = (int)(y - r * (b0 + 1)), tx = (int)(x - c * (b1 + 1));
+    if (ty < b0 && tx < b1) {
+      const int a = slot_atom[r * grid + c];
+      if (a >= 0) {
+        const double span = (double)hi[a] - (double)lo[a];
+        const double av = atoms[(int64_t)a * p + (int64_t)(ty * b1 + tx) * inner];
+        v = span == 0.0 ? 0.5 : (av - (double)lo[a]) / span;
+      }
+    }
+    if (canvas) canvas[t] = v;
+    if (canvas_u8) canvas_u8[t] = quantize_u8(v);
+  }
+}
+
+int atlas_geometry(int k, int rank, const int32_t* shape, int& b0, int& b1, int& inner, int& grid, int64_t& h,
+                   int64_t& w) {
+  if (k < 1) { set_error("atlas needs at least one atom"); return PB_EVALUE; }
+  if (rank == 1) { b0 = 1; b1 = shape[0]; inner = 1; }
+  else if (rank == 2) { b0 = shape[0]; b1 = shape[1]; inner = 1; }
+  else if (rank == 3) { b0 = shape[0]; b1 = shape[1]; inner = shape[2]; }   // slice 0 of the last axis
+  else { set_error("cannot render atlas for patch rank %d", rank); return PB_EVALUE; }
+  grid = (int)ceil(sqrt((double)k));
+  while ((int64_t)grid * grid < k) ++grid;
+  while (grid > 1 && (int64_t)(grid - 1) * (grid - 1) >= k) --grid;
+  h = (int64_t)grid * b0 + grid - 1;
+  w = (int64_t)grid * b1 + grid - 1;
+  return PB_OK;
+}
+
+int launch_atlas(const float* atoms, const double* pi, int k, int rank, const int32_t* shape, double* canvas,
+                 uint8_t* canvas_u8, cudaStream_t st) {
+  int b0, b1, inner, grid;
+  int64_t h, w;
+  int rc = atlas_geometry(k, rank, shape, b0, b1, inner, grid, h, w);
+  if (rc) return rc;
+  int p = 1;
+  for (int d = 0; d < rank; ++d) p *= shape[d];
+  const size_t smem = (size_t)grid * grid * 4 + (size_t)k * 8;
+  if (smem > 200 * 1024) { set_error("too many atoms for the atlas (%d)", k); return PB_EUNSUPPORTED; }
+  PB_CUDA_TRY(cudaFuncSetAttribute(k_atlas, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_atlas<<<1, 1024, smem, st>>>(atoms, pi, k, b0, b1, inner, p, grid, h, w, canvas, canvas_u8);
+  PB_LAUNCH_CHECK();
+  return PB_OK;
+}
+
 }  // namespace pb

@@ -24,4 +24,10 @@ int launch_live_finish(const LiveFinishArgs& a, cudaStream_t st);
 int adaptive_mask(const double* resid, int64_t m, int64_t budget, int64_t n_exploit, uint32_t k0, uint32_t k1,
                   uint64_t frame_index, uint8_t* mask, int* status, cudaStream_t st);
 
+// server.py:84-120: atlas geometry and render (canvas f64 and/or uint8, device)
+int atlas_geometry(int k, int rank, const int32_t* shape, int& b0, int& b1, int& inner, int& grid, int64_t& h,
+                   int64_t& w);
+int launch_atlas(const float* atoms, const double* pi, int k, int rank, const int32_t* shape, double* canvas,
+                 uint8_t* canvas_u8, cudaStream_t st);
+
 }  // namespace pb

@@ -135,6 +135,14 @@ class LiveProblem:
         atoms, pi, _ = self.dictionary()
         return Dictionary(atoms.astype(np.float64), pi, self.patch_shape)
 
+    def render_atlas(self) -> np.ndarray:
+        """The current dictionary atlas as a uint8 wire panel (server.py:84-120), on device."""
+        from .display import atlas_shape
+
+        out = np.empty(atlas_shape(self.num_atoms, self.patch_shape), dtype=np.uint8)
+        _lib.check(self._lib.pb_problem_render_atlas(self._h, out.ctypes.data), _VALUE)
+        return out
+
     def dictionary(self):
         atoms = np.empty((self.num_atoms, self.patch_size), dtype=np.float32)
         pi = np.empty(self.num_atoms, dtype=np.float64)

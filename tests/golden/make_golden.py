@@ -263,13 +263,34 @@ def dict_files(pb):
     np.savez_compressed(os.path.join(OUT, "dict_src.npz"), atoms=d.atoms, pi=d.pi)
 
 
+def atlases(pb):
+    """server.render_dictionary_atlas (server.py:84-120) on f32-exact atoms:
+    pi ties, a constant atom, ranks 1-3."""
+    from patchbeam.bpfa import Dictionary
+    from patchbeam.server import render_dictionary_atlas
+
+    rng = np.random.default_rng(404)
+    out = {}
+    for name, k, shape in (("a2", 10, (4, 5)), ("a3", 7, (3, 4, 2)), ("a1", 5, (6,)), ("a2sq", 16, (3, 3))):
+        p = int(np.prod(shape))
+        atoms = rng.standard_normal((k, p)).astype(np.float32).astype(np.float64)
+        atoms[1] = 0.25                                    # constant atom -> mid-grey
+        pi = np.round(rng.uniform(0, 1, k), 1)             # ties broken by atom index
+        d = Dictionary(atoms=atoms, pi=pi, patch_shape=shape)
+        out[f"{name}_atoms"], out[f"{name}_pi"] = atoms, pi
+        out[f"{name}_shape"] = np.asarray(shape)
+        out[f"{name}_canvas"] = render_dictionary_atlas(d)
+    np.savez_compressed(os.path.join(OUT, "atlas.npz"), **out)
+
+
 def main():
     pb = _import_reference()
     import numba
 
     only = sys.argv[1:]
     for name, fn in (("extract", extraction_cases), ("traj", trajectories), ("masks", masks), ("live", live),
-                     ("posterior", posterior), ("live_tail", live_tail), ("dicts", dict_files)):
+                     ("posterior", posterior), ("live_tail", live_tail), ("dicts", dict_files),
+                     ("atlas", atlases)):
         if not only or name in only:
             fn(pb)
     meta = {"python": platform.python_version(), "numpy": np.__version__,

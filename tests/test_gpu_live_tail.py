@@ -137,3 +137,26 @@ def test_install_dictionary_pending_and_live(cuda_device, tmp_path):
         assert sc2.epoch == 4 and not np.array_equal(atoms2, atoms)
         with pytest.raises(Exception):
             lp.install_dictionary(Dictionary(np.zeros((5, 36)), np.full(5, 0.5), (6, 6)))
+
+
+def test_atlas_on_device_matches_reference(golden, cuda_device):
+    """server.render_dictionary_atlas (server.py:84-120) on device vs the
+    reference's own canvases (f32-exact atoms): bit-exact f64, exact uint8."""
+    from paper_2311_15061_b200.bpfa import Dictionary
+    from paper_2311_15061_b200.display import pack_wireframe, render_dictionary_atlas, unpack_wireframe
+
+    g = golden("atlas.npz")
+    for name in ("a2", "a3", "a1", "a2sq"):
+        d = Dictionary(g[f"{name}_atoms"], g[f"{name}_pi"], tuple(int(b) for b in g[f"{name}_shape"]))
+        c = render_dictionary_atlas(d)
+        assert np.array_equal(c, g[f"{name}_canvas"]), name
+        u8 = render_dictionary_atlas(d, as_uint8=True)
+        assert np.array_equal(u8, osm.quantize_panel(g[f"{name}_canvas"])), name
+        hdr, back = unpack_wireframe(pack_wireframe(2, 7, 3, u8))
+        assert np.array_equal(back, u8) and hdr["problem_id"] == 7 and hdr["frame_id"] == 3
+    with pytest.raises(ValueError):
+        render_dictionary_atlas(Dictionary(np.zeros((2, 16)), np.zeros(2), (2, 2, 2, 2)))
+    with LiveProblem((24, 24), PatchSpec((6, 6)), Hyperparams(num_atoms=8)) as lp:
+        lp.submit_frame(inputs.synthetic_frames((24, 24), 1, seed=0)[0], np.ones((24, 24), bool))
+        atoms, pi, _ = lp.dictionary()
+        assert np.array_equal(lp.render_atlas(), osm.quantize_panel(osm.render_dictionary_atlas(atoms, pi, (6, 6))))

@@ -121,3 +121,12 @@ def test_live_tail_oracle_matches_reference(golden):
         assert int(mask.sum()) == budget
         ex = osm.adaptive_exploit(res, ratio, ef)
         assert len(ex) == n_exploit and mask.ravel()[ex].all(), i   # the exploit set is in the reference mask
+
+
+def test_atlas_oracle_matches_reference(golden):
+    from oracle import sampling as osm
+
+    g = golden("atlas.npz")
+    for name in ("a2", "a3", "a1", "a2sq"):
+        c = osm.render_dictionary_atlas(g[f"{name}_atoms"], g[f"{name}_pi"], tuple(g[f"{name}_shape"]))
+        assert np.array_equal(c, g[f"{name}_canvas"]), name
