@@ -216,6 +216,17 @@ int pb_phase_read(double* ms_out /* [4] */, int64_t* epochs_out);
  *  grid sync 2, shift load, owner atom update, -]. */
 int pb_dict_profile(int32_t enable, double* slots_ns_out /* [12] or NULL */);
 
+/* ---- native NCCL for the sharded sweep ----
+ * libnccl.so.2 is dlopen'ed (the copy already loaded in the process if any).
+ * pb_nccl_allreduce has the pb_allreduce_fn signature: pass its address as
+ * pb_epoch_desc.allreduce and the communicator as allreduce_ctx, and every
+ * exchange of the sweep is an ncclAllReduce (in-place sum) enqueued on the
+ * epoch's stream — no host round trip.  id: 128 bytes (ncclUniqueId). */
+int pb_nccl_unique_id(uint8_t* id_out);
+int pb_nccl_comm_create(const uint8_t* id, int32_t world, int32_t rank, void** comm_out);
+int pb_nccl_comm_destroy(void* comm);
+int pb_nccl_allreduce(void* comm, void* device_buf, int64_t count, int32_t dtype, void* stream);
+
 /* ---- adaptive-residual sampling mask on device (sampling.py:184-207) ----
  * Budget round(ratio*M); exploit = the round(exploit_fraction*budget) largest
  * residuals, ties by lowest flat index (bit-exact with the reference's stable

@@ -109,6 +109,10 @@ SIGNATURES = {
     "pb_problem_render_atlas": (c_i32, [c_vp, c_vp]),
     "pb_atlas_shape": (c_i32, [c_i32, c_i32, c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
     "pb_render_atlas": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
+    "pb_nccl_unique_id": (c_i32, [c_vp]),
+    "pb_nccl_comm_create": (c_i32, [c_vp, c_i32, c_i32, ctypes.POINTER(c_vp)]),
+    "pb_nccl_comm_destroy": (c_i32, [c_vp]),
+    "pb_nccl_allreduce": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp]),
     "pb_problem_last_gpu_ms": (c_f32, [c_vp]),
     "pb_problem_get_dictionary": (c_i32, [c_vp, c_vp, c_vp, ctypes.POINTER(Scalars)]),
 }

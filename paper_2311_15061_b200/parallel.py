@@ -65,6 +65,56 @@ class TorchCollective(Collective):
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
 
 
+class NcclCollective(Collective):
+    """A native NCCL communicator owned by the C library (pb_nccl_*): the
+    sweep's exchanges are ncclAllReduce calls the library enqueues on the epoch
+    stream itself (no host callback per exchange).  The 128-byte unique id is
+    broadcast over torch.distributed (any backend); ``NcclCollective.single()``
+    makes a one-rank communicator (tests)."""
+
+    def __init__(self, group=None, _single=False):
+        import torch
+
+        torch.cuda.nccl.version()  # load the process's libnccl (the library dlopens the same copy)
+        uid = (ctypes.c_uint8 * 128)()
+        if _single:
+            self.world, self.rank = 1, 0
+            _lib.call("pb_nccl_unique_id", uid)
+        else:
+            import torch.distributed as dist
+
+            self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+            if self.rank == 0:
+                _lib.call("pb_nccl_unique_id", uid)
+            dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+            t = torch.tensor(list(bytes(uid)), dtype=torch.uint8, device=dev)
+            dist.broadcast(t, 0, group=group)
+            uid = (ctypes.c_uint8 * 128)(*t.cpu().tolist())
+        self.handle = ctypes.c_void_p()
+        _lib.call("pb_nccl_comm_create", uid, self.world, self.rank, ctypes.byref(self.handle))
+
+    @classmethod
+    def single(cls):
+        return cls(_single=True)
+
+    def allreduce_(self, t):
+        if not t.is_cuda:
+            raise ValueError("NcclCollective reduces device tensors")
+        dt = {torch.float64: 0, torch.int32: 1}[t.dtype]
+        _lib.call("pb_nccl_allreduce", self.handle, t.data_ptr(), t.numel(), dt, torch.cuda.current_stream().cuda_stream)
+
+    def close(self):
+        if self.handle:
+            _lib.call("pb_nccl_comm_destroy", self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
 class LocalCollective(Collective):
     """W ranks as host threads sharing one device (tests): a sum over the ranks'
     tensors in rank order, written back to every rank."""
@@ -158,7 +208,11 @@ def gibbs_epoch_sharded(state, pm: PatchMatrix, hp, comm: Collective, freeze_dic
     d.i_offset = pm.first_patch
     d.n_global = pm.n_global
     d.n_obs = pm.n_obs_global
-    cb = _callback(comm)
+    if isinstance(comm, NcclCollective):  # native: ncclAllReduce enqueued by the library on the epoch stream
+        cb = ctypes.cast(_lib.load().pb_nccl_allreduce, _lib.ALLREDUCE_FN)
+        d.allreduce_ctx = comm.handle
+    else:
+        cb = _callback(comm)
     d.allreduce = cb
     _lib.call("pb_gibbs_epoch", ctypes.byref(d), _ptr(m), _stream())
     if check:

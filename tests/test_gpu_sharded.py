@@ -87,3 +87,23 @@ def test_sharded_matches_single_rank(cuda_device, world):
     assert (usage == h1["usage"]).mean() >= 0.999
     assert np.abs(res[0][2] - ref).mean() <= 1e-4
     assert res[0][1]["epoch"] == 3 and abs(res[0][1]["noise_precision"] / h1["noise_precision"] - 1) < 1e-2
+
+
+def test_native_nccl_single_rank_bit_identical(cuda_device):
+    """The native NCCL path (pb_nccl_*: ncclAllReduce enqueued by the library on
+    the epoch stream) with a one-rank communicator reproduces the fused kernel
+    bit for bit, and the host-side reductions (n_obs, overlap-add) go through it."""
+    img, mask, spec, hp = _problem()
+    pm = pp.extract_patches(img, mask, spec, True)
+    st_f, est_f = gb.infer(pm, hp, 3, 5, rng="philox")
+    comm = par.NcclCollective.single()
+    try:
+        pms = par.extract_patch_shard(img, mask, spec, True, comm)
+        assert pms.n_obs_global == pm.n_obs
+        st_s, est_s = par.infer_sharded(pms, hp, 3, 5, comm)
+        rec = par.reconstitute_sharded(pms, est_s, comm)
+    finally:
+        comm.close()
+    assert torch.equal(st_f.dictionary.atoms, st_s.dictionary.atoms)
+    assert torch.equal(st_f.usage_kn, st_s.usage_kn) and torch.equal(st_f.weights_kn, st_s.weights_kn)
+    assert np.abs(rec - pp.reconstitute(pm, est_f)).max() <= 1e-6
