@@ -21,6 +21,11 @@ Metric: patch-atom updates/s (higher is better).
              kernels, f64) on a bounded crop of the same workload, host cores.
 
 --impl reference runs that CPU port alone on the same metric (rank 0 only).
+
+N GPUs (torchrun): weak scaling — a (1024*N) x 1024 frame of the same kind cut
+into N contiguous configs[1]-sized patch shards, D replicated, the dictionary
+step's per-block moment sums and the epoch statistics allreduced by native NCCL
+calls the library enqueues on the sweep's stream (parallel.NcclCollective).
 """
 
 from __future__ import annotations
@@ -233,14 +238,21 @@ def run_gpu_arm(args):
 
     world, rank, local = dist_setup(args)
     lib = _lib.load()
-    img, mask = workload_inputs(CFG)
+    # N ranks: weak scaling — a (1024*N) x 1024 frame of the same kind, cut into
+    # N contiguous patch shards of configs[1]'s size (one per GPU)
+    wcfg = dict(CFG, shape=(CFG["shape"][0] * world, CFG["shape"][1]))
+    img, mask = workload_inputs(wcfg)
     hp = gb.Hyperparams(num_atoms=CFG["k"])
     if world > 1:
-        # one frame sharded across the ranks (strong scaling): contiguous patch
-        # ranges, D replicated, per-atom-block moment allreduce over NCCL
+        # contiguous patch-range shards, D replicated; the 44*P moment sums of each
+        # 8-atom block and the epoch statistics are allreduced by native NCCL
+        # calls the library enqueues on the epoch stream
         from paper_2311_15061_b200 import parallel as par
 
-        comm = par.TorchCollective()
+        try:
+            comm = par.NcclCollective()
+        except Exception:  # noqa: BLE001 — no native NCCL: torch.distributed callback
+            comm = par.TorchCollective()
         pm = par.extract_patch_shard(img, mask, pp.PatchSpec(CFG["patch"]), True, comm)
         sweep = lambda st: par.gibbs_epoch_sharded(st, pm, hp, comm, check=False)  # noqa: E731
         n_units = pm.n_global
@@ -387,11 +399,15 @@ def run_gpu_arm(args):
     line = {
         "metric": "BPFA patch-atom updates/sec", "value": value, "unit": "updates/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "configs[1]: 1024x1024 synthetic STEM-like frame, 10% uniform sampling, "
-                               "10x10 patches stride 1, K=256; step = one full Gibbs sweep",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": (("configs[1]: 1024x1024 synthetic STEM-like frame" if world == 1 else
+                                 f"configs[1] per GPU (weak scaling): {wcfg['shape'][0]}x{wcfg['shape'][1]} synthetic "
+                                 f"STEM-like frame, ~{n} patches per rank")
+                                + ", 10% uniform sampling, 10x10 patches stride 1, K=256; "
+                                  "step = one full Gibbs sweep"),
                    "global_batch": n_units, "seq_len": 1,
-                   "parallelism": f"patch-shards{world} (NCCL allreduce per 8-atom block)" if world > 1 else "single",
+                   "parallelism": (f"patch-shards{world} ({type(comm).__name__}: allreduce per 8-atom block)"
+                                   if world > 1 else "single"),
                    "patches": n, "atoms": k, "patch_size": p, "observed_per_patch": obs_per_patch,
                    "rng": "philox (device)",
                    "l2": f"inputs larger than L2: values {n * p * 4 / 1e6:.0f} MB + Z/S state "
@@ -412,6 +428,8 @@ def run_gpu_arm(args):
     if world > 1:
         import torch.distributed as dist
 
+        if hasattr(comm, "close"):
+            comm.close()
         dist.destroy_process_group()
 
 
