@@ -129,6 +129,10 @@ typedef struct pb_patch_index {
   int64_t nnz;      /* observed elements = sum of counts (caller supplies) */
   int32_t cmax;     /* max observed per patch (set by pb_build_index) */
   void* buffer;     /* device buffer of pb_index_bytes(n, p, nnz) bytes */
+  int32_t split_count;  /* set by pb_build_index: the code step runs patches with more
+                           observed elements in a second, wider launch (0 = one launch) */
+  int32_t reserved;
+  int64_t n_outliers;   /* patches above split_count */
 } pb_patch_index;
 
 size_t pb_index_bytes(int64_t n, int32_t p, int64_t nnz);

@@ -70,7 +70,7 @@ static size_t ws_bytes(int64_t n, int p, int k, int64_t nnz, EpochWs* ws, char* 
   char* pa = take(dict_gram_partials_bytes(p, kMaxDictBlocks));
   char* rd = take(dict_gram_reduced_bytes(p));
   char* bar = take(16);
-  char* bs = take((size_t)ceil_div(n * 32, 256) * 2 * 8);  // upper bound of code-step blocks
+  char* bs = take((size_t)(ceil_div(n * 64, 256) + 8) * 2 * 8);  // upper bound of code-step blocks (two launches)
   char* mc = take((size_t)k * 4);
   char* dg = take((size_t)8 * p * 4);
   if (ws) {
@@ -203,7 +203,22 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
   }
   int nblocks = 0;
   phase_mark(kPhCode, st);
-  if ((rc = launch_code_compact(c, d->rng_mode, nblocks, st))) return rc;
+  c.zero_mcount = 1;
+  if (d->index->split_count > 0) {  // narrow launch for most patches, wide launch for the listed rest
+    CompactArgs c1 = c, c2 = c;
+    c1.cmax = d->index->split_count;
+    c1.split = d->index->split_count;
+    int nb1 = 0, nb2 = 0;
+    if ((rc = launch_code_compact(c1, d->rng_mode, nb1, st))) return rc;
+    c2.plist = ix.outliers;
+    c2.plist_n = d->index->n_outliers;
+    c2.zero_mcount = 0;
+    c2.block_sums = ws.block_sums + 2 * (size_t)nb1;
+    if ((rc = launch_code_compact(c2, d->rng_mode, nb2, st))) return rc;
+    nblocks = nb1 + nb2;
+  } else if ((rc = launch_code_compact(c, d->rng_mode, nblocks, st))) {
+    return rc;
+  }
   phase_mark(kPhStats, st);
   if ((rc = launch_finish_stats(ws.block_sums, nblocks, sc, st))) return rc;
   if (d->allreduce) {  // epoch statistics across ranks: sum S^2, sum R^2, usage counts m_k
@@ -345,10 +360,26 @@ int pb_build_index(pb_patch_index* pi, const uint8_t* observed, const float* val
   cudaStream_t st = (cudaStream_t)stream;
   int rc = launch_build_index(ix, observed, values, counts, st);
   if (rc) return rc;
+  // code-step split: from the histogram of observed counts, the main launch's
+  // per-patch limit; the (few) wider patches get a second, wider launch
+  if ((rc = launch_count_hist(ix, counts, st))) return rc;
+  std::vector<int32_t> hist(pi->p + 2, 0);
   int32_t cmax = 0;
   PB_CUDA_TRY(cudaMemcpyAsync(&cmax, ix.cmax_dev, 4, cudaMemcpyDeviceToHost, st));
+  PB_CUDA_TRY(cudaMemcpyAsync(hist.data(), ix.hist, (size_t)(pi->p + 1) * 4, cudaMemcpyDeviceToHost, st));
   PB_CUDA_TRY(cudaStreamSynchronize(st));
   pi->cmax = cmax;
+  pi->split_count = getenv("PB_CODE_SPLIT_OFF") ? 0 : code_split_choose(hist.data(), pi->p, cmax);
+  pi->reserved = 0;
+  pi->n_outliers = 0;
+  if (pi->split_count > 0) {
+    if ((rc = launch_outliers(ix, counts, pi->split_count, st))) return rc;
+    int64_t nout = 0;
+    PB_CUDA_TRY(cudaMemcpyAsync(&nout, ix.out_base + ix.ntiles, 8, cudaMemcpyDeviceToHost, st));
+    PB_CUDA_TRY(cudaStreamSynchronize(st));
+    pi->n_outliers = nout;
+    if (nout == 0) pi->split_count = 0;
+  }
   return PB_OK;
 }
 

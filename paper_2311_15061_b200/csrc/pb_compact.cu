@@ -367,16 +367,26 @@ __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
   t.sq_w8 = 0.0f;
   double sq_r = 0.0;
   const int per_blk = blockDim.x / G;
-  const int64_t nblk = ceil_div(a.n, per_blk);
+  const int64_t nblk = ceil_div(a.plist ? a.plist_n : a.n, per_blk);
   for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
-    c.i = b * per_blk + threadIdx.x / G;
-    c.live = c.i < a.n;
-    c.ic = c.live ? c.i : 0;
+    const int64_t slot = b * per_blk + threadIdx.x / G;
+    if (a.plist) {  // second launch of a split: exactly the listed (wide) patches
+      c.live = slot < a.plist_n;
+      c.i = c.live ? a.plist[slot] : 0;
+    } else {
+      c.i = slot;
+      c.live = c.i < a.n;
+    }
     float r[CMAX];
     int addr[CMAX];
     int cnt = 0;
     int64_t r0 = 0;
-    if (c.live) { cnt = a.counts[c.i]; r0 = a.rowptr[c.i]; }
+    if (c.live) {
+      cnt = a.counts[c.i];
+      if (a.split && cnt > a.split) { c.live = false; cnt = 0; }  // handled by the second launch
+      else r0 = a.rowptr[c.i];
+    }
+    c.ic = c.live ? c.i : 0;
     const int wmax = __reduce_max_sync(0xffffffffu, lane_slots<G>(cnt, c.g));
 #pragma unroll
     for (int j = 0; j < CMAX; ++j) {
@@ -1096,6 +1106,37 @@ static bool pick_compact(int cmax, int& c, int& g) {
     default: set_error("unsupported compact layout c=%d g=%d", c, g); return PB_EUNSUPPORTED;       \
   }
 
+// Relative cost of one patch-atom update in a (c slots, g lanes) code-step
+// launch: g lanes each run the sampling (~100 instructions) and c slots (~4.5).
+static double code_cost(int c, int g) { return g * (100.0 + 4.5 * c); }
+
+int code_split_choose(const int32_t* hist, int p, int cmax) {
+  int cw, gw;
+  if (!pick_compact(cmax, cw, gw)) return 0;
+  if (gw >= 2) cw = 32;
+  const double wide = code_cost(cw, gw);
+  double total_n = 0;
+  for (int c = 0; c <= p; ++c) total_n += hist[c];
+  double best = total_n * wide;  // one launch for everything
+  int best_t = 0;
+  static const int kT[] = {8, 16, 24, 32, 64, 128, 256, 512};
+  for (int t : kT) {
+    if (t >= cmax) break;
+    int cm, gm;
+    if (!pick_compact(t, cm, gm)) continue;
+    if (gm >= 2) cm = 32;
+    double below = 0;
+    for (int c = 0; c <= p && c <= t; ++c) below += hist[c];
+    // the narrow launch still spends a lane on every patch; the wide launch
+    // gathers its listed patches' state (uncoalesced: ~3x), plus a fixed cost
+    const double cost = total_n * code_cost(cm, gm) + (total_n - below) * wide * 3.0 + 2048.0 * wide;
+    if (cost < best) { best = cost; best_t = t; }
+  }
+  // split only for a clear modeled win (measured: marginal splits lose to the
+  // second launch's restaging and scattered state accesses)
+  return best < 0.85 * total_n * wide ? best_t : 0;
+}
+
 static void normalize_cg(int& c, int& g) {
   // collapse to the instantiated set
   if (g >= 2) c = 32;
@@ -1139,8 +1180,9 @@ int launch_code_compact(const CompactArgs& a_in, int mode, int& nblocks, cudaStr
   a.kc = kc >= k8 ? k8 : kc;
   const size_t smem = (size_t)(a.kc + 2) * (a.p + 1) * 4 + fixed;
   if (smem > 220 * 1024) { set_error("too many atoms for the code step (K=%d)", a.k); return PB_EUNSUPPORTED; }
-  const int64_t nb = ceil_div(a.n * g, th);
-  PB_CUDA_TRY(cudaMemsetAsync(a.m_count, 0, (size_t)a.k * sizeof(int32_t), st));
+  const int64_t nb = ceil_div((a.plist ? a.plist_n : a.n) * g, th);
+  if (a.zero_mcount) PB_CUDA_TRY(cudaMemsetAsync(a.m_count, 0, (size_t)a.k * sizeof(int32_t), st));
+  if (nb == 0) { nblocks = 0; return PB_OK; }
 #define PB_C(C, GG)                                                                                  \
   case C * 100 + GG: {                                                                               \
     auto kern = mode == kRngReplay ? k_code_compact<C, GG, kRngReplay> : k_code_compact<C, GG, kRngPhilox>; \

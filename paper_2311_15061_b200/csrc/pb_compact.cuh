@@ -38,6 +38,12 @@ struct CompactArgs {
   int p, k, kc;
   uint32_t key0, key1;
   int64_t i_offset;     // global index of local patch 0 (draw counters of a shard)
+  // code-step split: the main launch skips patches with more than `split`
+  // observed elements; the second launch runs exactly the patches in plist
+  int split;
+  const int32_t* plist;
+  int64_t plist_n;
+  int zero_mcount;      // the launch zeroes the usage counts first
 };
 
 struct DictGramArgs {
@@ -77,6 +83,8 @@ struct DictGramArgs {
 
 int launch_resid_compact(const CompactArgs& a, cudaStream_t st);
 int launch_code_compact(const CompactArgs& a, int mode, int& nblocks, cudaStream_t st);
+// the code step's per-patch limit for the main launch from the count histogram (0 = no split)
+int code_split_choose(const int32_t* hist, int p, int cmax);
 int launch_dict_gram(const DictGramArgs& a, cudaStream_t st);
 int launch_dict_update(const DictGramArgs& a, int blk, cudaStream_t st);
 int dict_gram_blocks(int k);

@@ -189,6 +189,10 @@ int index_bytes(int64_t n, int p, int64_t nnz_upper, size_t* out) {
   a((size_t)nnz_upper * 2);           // csr_p
   a((size_t)nnz_upper * 4);           // csr_pos
   a(64);                              // cmax + misc
+  a((size_t)n * 4);                   // outliers: patches above the code-step split
+  a((size_t)ntiles * 4);              // outlier counts per tile
+  a((size_t)(ntiles + 1) * 8);        // outlier bases per tile
+  a((size_t)(p + 2) * 4);             // histogram of observed counts
   *out = b;
   return PB_OK;
 }
@@ -207,6 +211,70 @@ void carve_index(PatchIndex& ix, char* base, int64_t n, int p, int64_t nnz_upper
   ix.csr_p = (uint16_t*)take((size_t)nnz_upper * 2);
   ix.csr_pos = (uint32_t*)take((size_t)nnz_upper * 4);
   ix.cmax_dev = (int32_t*)take(64);
+  ix.outliers = (int32_t*)take((size_t)n * 4);
+  ix.out_tot = (int32_t*)take((size_t)ntiles * 4);
+  ix.out_base = (int64_t*)take((size_t)(ntiles + 1) * 8);
+  ix.hist = (int32_t*)take((size_t)(p + 2) * 4);
+}
+
+// Histogram of the per-patch observed counts (0..p): shared-memory bins per block.
+__global__ void k_count_hist(const int32_t* __restrict__ counts, int64_t n, int p, int32_t* __restrict__ hist) {
+  extern __shared__ int bins[];
+  for (int b = threadIdx.x; b <= p; b += blockDim.x) bins[b] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&bins[min(max(counts[i], 0), p)], 1);
+  __syncthreads();
+  for (int b = threadIdx.x; b <= p; b += blockDim.x)
+    if (bins[b]) atomicAdd(&hist[b], bins[b]);
+}
+
+// Outliers (count > split) per tile, then their ids in ascending order.
+__global__ void k_outlier_totals(const int32_t* __restrict__ counts, int64_t n, int split, int32_t* __restrict__ tot) {
+  __shared__ int red[32];
+  const int64_t base = (int64_t)blockIdx.x * kTile;
+  int s = 0;
+  for (int li = threadIdx.x; li < kTile; li += blockDim.x) {
+    const int64_t i = base + li;
+    s += (i < n && counts[i] > split) ? 1 : 0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    tot[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kTile) k_outlier_fill(const int32_t* __restrict__ counts, int64_t n, int split,
+                                                        const int64_t* __restrict__ out_base,
+                                                        int32_t* __restrict__ outliers) {
+  __shared__ int wsum[33];   // block_excl_scan writes the total at [32]
+  const int64_t i = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  const int f = (i < n && counts[i] > split) ? 1 : 0;
+  int tot = 0;
+  const int rank = block_excl_scan(f, wsum, tot);
+  if (f) outliers[out_base[blockIdx.x] + rank] = (int32_t)i;
+}
+
+int launch_count_hist(const PatchIndex& ix, const int32_t* counts, cudaStream_t st) {
+  PB_CUDA_TRY(cudaMemsetAsync(ix.hist, 0, (size_t)(ix.p + 2) * 4, st));
+  int64_t nb = ceil_div(ix.n, 256);
+  if (nb > 1184) nb = 1184;
+  k_count_hist<<<(unsigned)(nb < 1 ? 1 : nb), 256, (size_t)(ix.p + 1) * 4, st>>>(counts, ix.n, ix.p, ix.hist);
+  PB_LAUNCH_CHECK();
+  return PB_OK;
+}
+
+int launch_outliers(const PatchIndex& ix, const int32_t* counts, int split, cudaStream_t st) {
+  k_outlier_totals<<<ix.ntiles, 256, 0, st>>>(counts, ix.n, split, ix.out_tot);
+  k_tile_scan<<<1, 1024, 0, st>>>(ix.out_tot, ix.ntiles, ix.out_base);
+  k_outlier_fill<<<ix.ntiles, kTile, 0, st>>>(counts, ix.n, split, ix.out_base, ix.outliers);
+  PB_LAUNCH_CHECK();
+  return PB_OK;
 }
 
 int launch_build_index(PatchIndex& ix, const uint8_t* obs, const float* values, const int32_t* counts,

@@ -31,6 +31,10 @@ struct PatchIndex {
   uint16_t* csr_p;      // [nnz] CSR: patch offset p of each slot
   uint32_t* csr_pos;    // [nnz] CSR: CSC position of each slot
   int32_t* cmax_dev;    // max observed count over patches
+  int32_t* outliers;    // [n] ids of the patches above the code-step split, ascending
+  int32_t* out_tot;     // [ntiles]
+  int64_t* out_base;    // [ntiles + 1]; out_base[ntiles] = number of outliers
+  int32_t* hist;        // [p + 1] histogram of the observed counts
 };
 
 int index_bytes(int64_t n, int p, int64_t nnz, size_t* out);
@@ -38,5 +42,7 @@ void carve_index(PatchIndex& ix, char* base, int64_t n, int p, int64_t nnz);
 int launch_build_index(PatchIndex& ix, const uint8_t* obs, const float* values, const int32_t* counts,
                        cudaStream_t st);
 int launch_scatter_x(const PatchIndex& ix, const float* values, const int32_t* counts, cudaStream_t st);
+int launch_count_hist(const PatchIndex& ix, const int32_t* counts, cudaStream_t st);
+int launch_outliers(const PatchIndex& ix, const int32_t* counts, int split, cudaStream_t st);
 
 }  // namespace pb
