@@ -106,3 +106,25 @@ def test_native_quality_tracks_oracle(cuda_device):
             assert abs(psnr(out, f) - psnr(ref, f)) <= 1.5, (psnr(out, f), psnr(ref, f))
     finally:
         _lib.load().pb_problem_destroy(pr)
+
+
+def test_live_sequence_replay_matches_reference(golden, cuda_device):
+    """The reference Pipeline's 3 warm-started frames (tests/golden/live.npz,
+    produced by patchbeam itself) through this package's API in replay mode
+    (the reference's own draw streams, same warm-start idiom): per-frame
+    reconstruction within 1e-3 (f32 arithmetic; no Z flip expected) and PSNR
+    within 0.05 dB."""
+    g = golden("live.npz")
+    hp = gb.Hyperparams(num_atoms=8)
+    st = None
+    for t in range(3):
+        frame, mask = g[f"f{t}_frame"], g[f"f{t}_mask"]
+        pm = pp.extract_patches(frame, mask, pp.PatchSpec((6, 6)), True)
+        if st is not None:
+            st.usage[:] = False
+            st.weights[:] = 0.0
+        st, est = gb.infer(pm, hp, 2, 0, rng="numpy", state=st)
+        rec = pp.reconstitute(pm, est)
+        ref = g[f"f{t}_recon"]
+        assert abs(psnr(rec, frame) - psnr(ref, frame)) <= 0.05, t
+        assert np.abs(rec - ref).max() <= 1e-3, (t, np.abs(rec - ref).max())

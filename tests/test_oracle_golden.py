@@ -130,3 +130,21 @@ def test_atlas_oracle_matches_reference(golden):
     for name in ("a2", "a3", "a1", "a2sq"):
         c = osm.render_dictionary_atlas(g[f"{name}_atoms"], g[f"{name}_pi"], tuple(g[f"{name}_shape"]))
         assert np.array_equal(c, g[f"{name}_canvas"]), name
+
+
+def test_live_pipeline_sequence_bit_exact(golden):
+    """Pipeline.submit_frame (pipeline.py:217-276) over 3 warm-started frames,
+    replayed by the oracle: codes re-burn each frame, dictionary / pi / gammas
+    and the epoch counter carry over — reconstructions bit-exact."""
+    g = golden("live.npz")
+    hp = ob.Hyper(num_atoms=8)
+    st = None
+    for t in range(3):
+        frame, mask = g[f"f{t}_frame"], g[f"f{t}_mask"]
+        pm = op.extract_patches(frame, mask, (6, 6), (), True)
+        if st is not None:
+            st.usage[:] = False
+            st.weights[:] = 0.0
+        st, est = ob.infer(pm, hp, 2, 0, state=st)
+        assert np.array_equal(op.reconstitute(pm, est), g[f"f{t}_recon"]), t
+        assert np.array_equal(st.atoms, g[f"f{t}_atoms"]), t
