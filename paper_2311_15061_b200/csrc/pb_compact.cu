@@ -1129,6 +1129,10 @@ int code_split_choose(const int32_t* hist, int p, int cmax) {
     for (int c = 0; c <= p && c <= t; ++c) below += hist[c];
     // the narrow launch still spends a lane on every patch; the wide launch
     // gathers its listed patches' state (uncoalesced: ~3x), plus a fixed cost
+    // a wide launch over only a few patches cannot fill the GPU (each CTA still
+    // walks all K atoms): require at least half a wave of outliers
+    const double wave = 2.0 * sm_count_c() * (256.0 / gw);
+    if (total_n - below < 0.5 * wave) continue;
     const double cost = total_n * code_cost(cm, gm) + (total_n - below) * wide * 3.0 + 2048.0 * wide;
     if (cost < best) { best = cost; best_t = t; }
   }
