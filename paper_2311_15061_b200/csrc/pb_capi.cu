@@ -58,6 +58,7 @@ struct EpochWs {
   double* block_sums;
   int32_t* m_count;
   float* delta_g;   // atom shifts of the last updated block [8][P] (dictionary step exchange)
+  unsigned* ctr;    // dynamic block counters of the code-step launches [2]
 };
 static const int kMaxDictBlocks = 148 * 8;
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -73,7 +74,9 @@ static size_t ws_bytes(int64_t n, int p, int k, int64_t nnz, EpochWs* ws, char* 
   char* bs = take((size_t)(ceil_div(n * 64, 256) + 8) * 2 * 8);  // upper bound of code-step blocks (two launches)
   char* mc = take((size_t)k * 4);
   char* dg = take((size_t)8 * p * 4);
+  char* ct = take(16);
   if (ws) {
+    ws->ctr = (unsigned*)ct;
     ws->delta_g = (float*)dg;
     ws->r_csc = (float*)r; ws->wt = (float*)wt; ws->wt_bytes = wtb;
     ws->partials = (float*)pa; ws->reduced = (double*)rd;
@@ -203,21 +206,40 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
   }
   int nblocks = 0;
   phase_mark(kPhCode, st);
-  c.zero_mcount = 1;
-  if (d->index->split_count > 0) {  // narrow launch for most patches, wide launch for the listed rest
+  c.blk_ctr = ws.ctr;
+  if (d->index->split_count > 0) {
+    // narrow launch for most patches (stream st) and, concurrently on a side
+    // stream, the wide launch over the listed outliers; both claim blocks
+    // dynamically and write per-block sums (deterministic)
+    PB_CUDA_TRY(cudaMemsetAsync(ws.m_count, 0, (size_t)d->k * sizeof(int32_t), st));
     CompactArgs c1 = c, c2 = c;
     c1.cmax = d->index->split_count;
     c1.split = d->index->split_count;
-    int nb1 = 0, nb2 = 0;
-    if ((rc = launch_code_compact(c1, d->rng_mode, nb1, st))) return rc;
+    c1.zero_mcount = c2.zero_mcount = 0;
+    const int nb1_expect = code_launch_blocks(c1.cmax, d->n);
     c2.plist = ix.outliers;
     c2.plist_n = d->index->n_outliers;
-    c2.zero_mcount = 0;
-    c2.block_sums = ws.block_sums + 2 * (size_t)nb1;
-    if ((rc = launch_code_compact(c2, d->rng_mode, nb2, st))) return rc;
+    c2.block_sums = ws.block_sums + 2 * (size_t)nb1_expect;
+    c2.blk_ctr = ws.ctr + 1;
+    static thread_local cudaStream_t side = nullptr;
+    static thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    if (!side) {
+      PB_CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+      PB_CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+      PB_CUDA_TRY(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    }
+    int nb1 = 0, nb2 = 0;
+    PB_CUDA_TRY(cudaEventRecord(ev_fork, st));
+    PB_CUDA_TRY(cudaStreamWaitEvent(side, ev_fork, 0));
+    if ((rc = launch_code_compact(c2, d->rng_mode, nb2, side))) return rc;
+    PB_CUDA_TRY(cudaEventRecord(ev_join, side));
+    if ((rc = launch_code_compact(c1, d->rng_mode, nb1, st))) return rc;
+    PB_CUDA_TRY(cudaStreamWaitEvent(st, ev_join, 0));
+    if (nb1 != nb1_expect) { set_error("code-step block count mismatch"); return PB_EUNSUPPORTED; }
     nblocks = nb1 + nb2;
-  } else if ((rc = launch_code_compact(c, d->rng_mode, nblocks, st))) {
-    return rc;
+  } else {
+    c.zero_mcount = 1;
+    if ((rc = launch_code_compact(c, d->rng_mode, nblocks, st))) return rc;
   }
   phase_mark(kPhStats, st);
   if ((rc = launch_finish_stats(ws.block_sums, nblocks, sc, st))) return rc;
@@ -370,6 +392,10 @@ int pb_build_index(pb_patch_index* pi, const uint8_t* observed, const float* val
   PB_CUDA_TRY(cudaStreamSynchronize(st));
   pi->cmax = cmax;
   pi->split_count = getenv("PB_CODE_SPLIT_OFF") ? 0 : code_split_choose(hist.data(), pi->p, cmax);
+  if (const char* f = getenv("PB_CODE_SPLIT_AT")) {  // experiments: force the split threshold
+    const int t = atoi(f);
+    pi->split_count = (t > 0 && t < cmax) ? t : 0;
+  }
   pi->reserved = 0;
   pi->n_outliers = 0;
   if (pi->split_count > 0) {

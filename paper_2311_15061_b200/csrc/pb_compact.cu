@@ -344,6 +344,7 @@ __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
   int* mcnt = (int*)(logit + a.k);             // K
   float* wwin = (float*)(mcnt + a.k);          // (blockDim / G) * 9
   __shared__ double red[32];
+  __shared__ long long next_blk;
   CodeConst c;
   c.g = threadIdx.x % G;
   c.lane = threadIdx.x & 31;
@@ -363,12 +364,20 @@ __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
   __syncthreads();
   const int row_bytes = kp * 4;
   CodeThread t;
-  t.sq_w = 0.0;
   t.sq_w8 = 0.0f;
-  double sq_r = 0.0;
   const int per_blk = blockDim.x / G;
   const int64_t nblk = ceil_div(a.plist ? a.plist_n : a.n, per_blk);
-  for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
+  // blocks of patches are claimed dynamically (the launch may share the GPU with
+  // a concurrent one); each block writes its own S^2 / R^2 sums, summed later in
+  // block order, so the result does not depend on which CTA took which block
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) next_blk = (long long)atomicAdd(a.blk_ctr, 1u);
+    __syncthreads();
+    const int64_t b = next_blk;
+    if (b >= nblk) break;
+    t.sq_w = 0.0;
+    double sq_r = 0.0;
     const int64_t slot = b * per_blk + threadIdx.x / G;
     if (a.plist) {  // second launch of a split: exactly the listed (wide) patches
       c.live = slot < a.plist_n;
@@ -413,13 +422,13 @@ __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
       const int s = j * G + c.g;
       if (c.live && j < wmax && s < cnt) a.r_csc[a.csr_pos[r0 + s]] = r[j];
     }
-  }
-  const double bw = block_sum_d(t.sq_w, red);
-  __syncthreads();
-  const double br = block_sum_d(sq_r, red);
-  if (threadIdx.x == 0) {
-    a.block_sums[2 * blockIdx.x] = bw;
-    a.block_sums[2 * blockIdx.x + 1] = br;
+    const double bw = block_sum_d(t.sq_w, red);
+    __syncthreads();
+    const double br = block_sum_d(sq_r, red);
+    if (threadIdx.x == 0) {
+      a.block_sums[2 * b] = bw;
+      a.block_sums[2 * b + 1] = br;
+    }
   }
   __syncthreads();
   for (int k = threadIdx.x; k < a.k; k += blockDim.x)
@@ -1108,7 +1117,19 @@ static bool pick_compact(int cmax, int& c, int& g) {
 
 // Relative cost of one patch-atom update in a (c slots, g lanes) code-step
 // launch: g lanes each run the sampling (~100 instructions) and c slots (~4.5).
-static double code_cost(int c, int g) { return g * (100.0 + 4.5 * c); }
+// relative per-patch cost of the code step by launch shape, measured on B200
+// (cfg2 1024^2/10x10: 16 lanes 2.50 ms, 24 lanes 2.58, 32 lanes 2.77; cfg4
+// cube: 2 lanes-per-patch groups cost ~0.73x of 4)
+static double code_cost(int c, int g) {
+  if (g == 1) return c <= 8 ? 0.98 : c <= 16 ? 1.0 : c <= 24 ? 1.03 : 1.11;
+  return 1.11 * sqrt((double)g);
+}
+
+int code_launch_blocks(int cmax, int64_t n) {
+  int c, g;
+  if (!pick_compact(cmax, c, g)) return 0;
+  return (int)ceil_div(n * g, 256);
+}
 
 int code_split_choose(const int32_t* hist, int p, int cmax) {
   int cw, gw;
@@ -1128,17 +1149,20 @@ int code_split_choose(const int32_t* hist, int p, int cmax) {
     double below = 0;
     for (int c = 0; c <= p && c <= t; ++c) below += hist[c];
     // the narrow launch still spends a lane on every patch; the wide launch
-    // gathers its listed patches' state (uncoalesced: ~3x), plus a fixed cost
-    // a wide launch over only a few patches cannot fill the GPU (each CTA still
-    // walks all K atoms): require at least half a wave of outliers
+    // gathers its listed patches' state (uncoalesced: ~4x), plus a fixed cost.
+    // The wide launch runs concurrently on a side stream; with fewer than half
+    // a wave of outliers it is a latency tail (each of its CTAs walks all K
+    // atoms for its patches) that hides only behind a narrow launch of at
+    // least 4 waves
     const double wave = 2.0 * sm_count_c() * (256.0 / gw);
-    if (total_n - below < 0.5 * wave) continue;
-    const double cost = total_n * code_cost(cm, gm) + (total_n - below) * wide * 3.0 + 2048.0 * wide;
+    const double narrow_waves = total_n * gm / (256.0 * 2.0 * sm_count_c());
+    if (total_n - below < 0.5 * wave && narrow_waves < 4.0) continue;
+    const double cost = total_n * code_cost(cm, gm) + (total_n - below) * wide * 4.0 + 2048.0 * wide;
     if (cost < best) { best = cost; best_t = t; }
   }
-  // split only for a clear modeled win (measured: marginal splits lose to the
-  // second launch's restaging and scattered state accesses)
-  return best < 0.85 * total_n * wide ? best_t : 0;
+  // split only for a clear modeled win (marginal splits lose to the second
+  // launch's restaging and scattered state accesses)
+  return best < 0.95 * total_n * wide ? best_t : 0;
 }
 
 static void normalize_cg(int& c, int& g) {
@@ -1186,7 +1210,9 @@ int launch_code_compact(const CompactArgs& a_in, int mode, int& nblocks, cudaStr
   if (smem > 220 * 1024) { set_error("too many atoms for the code step (K=%d)", a.k); return PB_EUNSUPPORTED; }
   const int64_t nb = ceil_div((a.plist ? a.plist_n : a.n) * g, th);
   if (a.zero_mcount) PB_CUDA_TRY(cudaMemsetAsync(a.m_count, 0, (size_t)a.k * sizeof(int32_t), st));
-  if (nb == 0) { nblocks = 0; return PB_OK; }
+  nblocks = (int)nb;   // one S^2 / R^2 pair per block of patches
+  if (nb == 0) return PB_OK;
+  PB_CUDA_TRY(cudaMemsetAsync(a.blk_ctr, 0, sizeof(unsigned), st));
 #define PB_C(C, GG)                                                                                  \
   case C * 100 + GG: {                                                                               \
     auto kern = mode == kRngReplay ? k_code_compact<C, GG, kRngReplay> : k_code_compact<C, GG, kRngPhilox>; \
@@ -1194,7 +1220,6 @@ int launch_code_compact(const CompactArgs& a_in, int mode, int& nblocks, cudaStr
     int per_sm = 0;                                                                                  \
     PB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, th, smem));             \
     const int64_t grid = std::min<int64_t>(nb, (int64_t)std::max(per_sm, 1) * sm_count_c());         \
-    nblocks = (int)grid;                                                                             \
     kern<<<(unsigned)grid, th, smem, st>>>(a);                                                       \
     break;                                                                                           \
   }

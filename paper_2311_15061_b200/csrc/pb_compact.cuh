@@ -44,6 +44,7 @@ struct CompactArgs {
   const int32_t* plist;
   int64_t plist_n;
   int zero_mcount;      // the launch zeroes the usage counts first
+  unsigned* blk_ctr;    // dynamic block counter of the launch (zeroed by the launcher)
 };
 
 struct DictGramArgs {
@@ -85,6 +86,7 @@ int launch_resid_compact(const CompactArgs& a, cudaStream_t st);
 int launch_code_compact(const CompactArgs& a, int mode, int& nblocks, cudaStream_t st);
 // the code step's per-patch limit for the main launch from the count histogram (0 = no split)
 int code_split_choose(const int32_t* hist, int p, int cmax);
+int code_launch_blocks(int cmax, int64_t n);  // blocks of patches (= S^2/R^2 pairs) of a launch
 int launch_dict_gram(const DictGramArgs& a, cudaStream_t st);
 int launch_dict_update(const DictGramArgs& a, int blk, cudaStream_t st);
 int dict_gram_blocks(int k);

@@ -6,7 +6,10 @@ replay, the reference's draw streams) or the reference's stated behaviour:
   a multiple of 8: replay parity per epoch (Z flips <= 2, D <= 2e-5);
 * an all-unobserved mask (nnz = 0): the sweep runs, every atom is a prior draw
   and the estimates are zero (bpfa.py:299-307 with A = C = 0);
-* a fully observed frame: replay parity.
+* a fully observed frame: replay parity;
+* the split code step (a narrow launch for most patches and, concurrently on
+  a side stream, a wide launch over the listed outlier patches), forced via
+  PB_CODE_SPLIT_AT with many and with few outliers: replay parity.
 """
 
 import numpy as np
@@ -65,3 +68,15 @@ def test_empty_mask_sweep(cuda_device):
     assert np.all(est.cpu().numpy() == 0.0) or np.isfinite(est.cpu().numpy()).all()
     rec = pp.reconstitute(pm, est)
     assert np.isfinite(rec).all()
+
+
+@pytest.mark.parametrize("split", [8, 16])
+def test_split_code_step_replay(cuda_device, monkeypatch, split):
+    monkeypatch.setenv("PB_CODE_SPLIT_AT", str(split))
+    rng = np.random.default_rng(15)
+    img = rng.random((40, 41))
+    mask = rng.random(img.shape) < 0.3   # 6x6 patches: ~11 observed, max ~20
+    pm, _ = _pm_pair(img, mask, (6, 6), True)
+    ix = pm.index()
+    assert ix.split_count == split and ix.n_outliers > 0
+    assert _replay(img, mask, (6, 6), True, 10, 3, 2) <= 4
