@@ -191,7 +191,7 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
       if ((rc = launch_dict_gram(g, st))) return rc;   // fused: all passes in one persistent launch
     } else {
       // split (sharded) mode: per atom block, local pass -> allreduce of the
-      // 44*P moment sums across ranks -> identical atom draws on every rank
+      // 48*P moment sums across ranks -> identical atom draws on every rank
       g.split = 1;
       const int nblk = dict_gram_blocks(d->k);
       for (int b = 0; b <= nblk; ++b) {

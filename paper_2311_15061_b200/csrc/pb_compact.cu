@@ -21,6 +21,7 @@
 //                   observed residual in registers, the dictionary in shared
 //                   memory (gathered by the patch's observed offsets), atoms
 //                   k = 0..K-1 in order with the z/s draw in registers.
+#include <type_traits>
 #include <math.h>
 
 #include "pb_compact.cuh"
@@ -513,20 +514,19 @@ __device__ __forceinline__ void group_transpose_reduce(float (&v)[NP], int sub) 
 }
 
 // Accumulator layout of one atom block (B even): C_0..C_{B-1}, then per row j
-// of the Gram triangle the PAIRS (G_j,2m, G_j,2m+1) for 2m+1 <= j, then the
-// even-row diagonals G_00, G_22, ... — every update is a packed f32x2 FMA
-// (FFMA2) on an aligned pair; G_jj = A_j.
+// of the Gram triangle the PAIRS (G_j,2m, G_j,2m+1) for 2m <= j — every update
+// is a packed f32x2 FMA (FFMA2) of the broadcast w_j with the aligned pair
+// (w_2m, w_2m+1) as loaded; G_jj = A_j.  Even rows carry one redundant entry
+// (G_j,j+1, also in row j+1) so that no operand pair has to be assembled.
 template <int B>
 struct GramLayout {
   static_assert(B % 2 == 0, "pair layout needs an even block");
-  static constexpr int NACC = B + B * (B + 1) / 2;
+  __host__ __device__ static constexpr int pairbase(int j) { return j + (j / 2) * ((j - 1) / 2); }
+  static constexpr int NACC = B + 2 * pairbase(B);
   static constexpr int NP = ((NACC + 15) / 16) * 16;    // padded for the transpose reduce
-  __host__ __device__ static constexpr int pairbase(int j) { return (j / 2) * ((j + 1) / 2); }
-  static constexpr int DIAG = B + 2 * pairbase(B);     // first even-row diagonal
-  __host__ __device__ static constexpr int gidx(int j, int l) {
-    return ((j & 1) == 0 && l == j) ? DIAG + j / 2 : B + 2 * (pairbase(j) + l / 2) + (l & 1);
-  }
+  __host__ __device__ static constexpr int gidx(int j, int l) { return B + 2 * (pairbase(j) + l / 2) + (l & 1); }
 };
+static_assert(GramLayout<8>::NACC == 48 && GramLayout<8>::NP == 48, "layout of the 8-atom block");
 
 // --- mbarrier + 1-D bulk async copy (TMA engine) helpers --------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -881,56 +881,58 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
           int ec = ms + sub;
           float* rc = r_t + ec;
           const uint16_t* ecp = eloc_t + ec;
-          for (int it = 0; it < its; it += kPf) {
+          // the pass's block flags are compile-time inside the element loop
+          auto elements = [&](auto hp_c, auto hc_c) {
+            constexpr bool HP = decltype(hp_c)::value, HC = decltype(hc_c)::value;
+            for (int it = 0; it < its; it += kPf) {
 #pragma unroll
-            for (int d = 0; d < kPf; ++d) {
-              if (it + d >= its) break;
-              const int il = ilb[d];
-              float r = rb[d];
-              if (ec + kPf * S < mt) { ilb[d] = ecp[kPf * S]; rb[d] = rc[kPf * S]; }
-              if (ec < mt) {
-                const uint32_t wo[2] = {(uint32_t)il, (uint32_t)il ^ 16u};  // e_loc holds w_row_off
-                if (has_prev) {  // r += w_prev . delta  (packed pairs, two independent chains)
-                  float2 sh[B / 4];
+              for (int d = 0; d < kPf; ++d) {
+                if (it + d >= its) break;
+                const int il = ilb[d];
+                float r = rb[d];
+                if (ec + kPf * S < mt) { ilb[d] = ecp[kPf * S]; rb[d] = rc[kPf * S]; }
+                if (ec < mt) {
+                  const uint32_t wo[2] = {(uint32_t)il, (uint32_t)il ^ 16u};  // e_loc holds w_row_off
+                  if constexpr (HP) {  // r += w_prev . delta  (packed pairs, two independent chains)
+                    float2 sh[B / 4];
 #pragma unroll
-                  for (int h = 0; h < B / 4; ++h) {
-                    const float4 w4 = lds128(wprev_s + wo[h]);
-                    sh[h] = __fmul2_rn(make_float2(w4.x, w4.y), dl2[2 * h]);
-                    sh[h] = __ffma2_rn(make_float2(w4.z, w4.w), dl2[2 * h + 1], sh[h]);
+                    for (int h = 0; h < B / 4; ++h) {
+                      const float4 w4 = lds128(wprev_s + wo[h]);
+                      sh[h] = __fmul2_rn(make_float2(w4.x, w4.y), dl2[2 * h]);
+                      sh[h] = __ffma2_rn(make_float2(w4.z, w4.w), dl2[2 * h + 1], sh[h]);
+                    }
+#pragma unroll
+                    for (int h = 0; h < B / 4; ++h) r += sh[h].x + sh[h].y;
+                    *rc = r;
                   }
+                  if constexpr (HC) {
+                    float wc[B];
 #pragma unroll
-                  for (int h = 0; h < B / 4; ++h) r += sh[h].x + sh[h].y;
-                  *rc = r;
+                    for (int h = 0; h < B / 4; ++h) {
+                      const float4 w4 = lds128(wcur_s + wo[h]);
+                      wc[4 * h + 0] = w4.x; wc[4 * h + 1] = w4.y; wc[4 * h + 2] = w4.z; wc[4 * h + 3] = w4.w;
+                    }
+                    const float2 rr2 = make_float2(r, r);
+#pragma unroll
+                    for (int h = 0; h < B / 2; ++h) pfma(v, h, make_float2(wc[2 * h], wc[2 * h + 1]), rr2);  // C
+#pragma unroll
+                    for (int j = 0; j < B; ++j) {   // Gram pairs (G_j,2m, G_j,2m+1)
+                      const float2 wj = make_float2(wc[j], wc[j]);
+#pragma unroll
+                      for (int m = 0; 2 * m <= j; ++m)
+                        pfma(v, L::gidx(j, 2 * m) / 2, wj, make_float2(wc[2 * m], wc[2 * m + 1]));
+                    }
+                  }
                 }
-                if (has_cur) {
-                  float wc[B];
-#pragma unroll
-                  for (int h = 0; h < B / 4; ++h) {
-                    const float4 w4 = lds128(wcur_s + wo[h]);
-                    wc[4 * h + 0] = w4.x; wc[4 * h + 1] = w4.y; wc[4 * h + 2] = w4.z; wc[4 * h + 3] = w4.w;
-                  }
-                  const float2 rr2 = make_float2(r, r);
-#pragma unroll
-                  for (int h = 0; h < B / 2; ++h) pfma(v, h, make_float2(wc[2 * h], wc[2 * h + 1]), rr2);  // C
-#pragma unroll
-                  for (int j = 1; j < B; ++j) {   // Gram pairs (G_j,2m, G_j,2m+1)
-                    const float2 wj = make_float2(wc[j], wc[j]);
-#pragma unroll
-                    for (int m = 0; 2 * m + 1 <= j; ++m)
-                      pfma(v, L::gidx(j, 2 * m) / 2, wj, make_float2(wc[2 * m], wc[2 * m + 1]));
-                  }
-#pragma unroll
-                  for (int j = 0; j < B; j += 4) {   // even-row diagonals, two per pair
-                    const float2 d2 = make_float2(wc[j], wc[j + 2]);
-                    pfma(v, L::DIAG / 2 + j / 4, d2, d2);
-                  }
-                }
+                ec += S;
+                rc += S;
+                ecp += S;
               }
-              ec += S;
-              rc += S;
-              ecp += S;
             }
-          }
+          };
+          if (has_prev && has_cur) elements(std::true_type{}, std::true_type{});
+          else if (has_cur) elements(std::false_type{}, std::true_type{});
+          else elements(std::true_type{}, std::false_type{});
           const int mc_done = mc;
           const bool more = pos < we;
           if (more) carve();  // next round's loads overlap this round's reduction

@@ -1,6 +1,6 @@
 // pb200 — native NCCL allreduce for the sharded sweep.
 //
-// The dictionary step of a sharded sweep exchanges the 44·P moment sums of
+// The dictionary step of a sharded sweep exchanges the 48·P moment sums of
 // every 8-atom block (K/8 small allreduces per sweep) plus the epoch
 // statistics.  Routing each through a host callback costs tens of µs of host
 // work per exchange; here the exchange is an `ncclAllReduce` enqueued on the

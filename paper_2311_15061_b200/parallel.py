@@ -4,7 +4,7 @@ One process per GPU.  The patch grid of one frame is cut into contiguous patch
 ranges (rank r holds global patches [N*r/W, N*(r+1)/W)); the dictionary D, pi
 and the precisions are replicated.  Exchanges per epoch:
 
-* dictionary step — per block of 8 atoms, the 44*P per-pixel moment/Gram sums
+* dictionary step — per block of 8 atoms, the 48*P per-pixel moment/Gram sums
   (f64) each rank accumulated over its own observed elements are allreduced,
   then every rank performs the same 8 sequential atom draws (draws keyed by
   global atom and pixel index) — bpfa.py:299-307 with the reduction split
