@@ -752,6 +752,20 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
   if (a.split && a.blk_begin > 0) {  // split mode: the previous pass's shifts come from global memory
     for (int t = threadIdx.x; t < B * p; t += blockDim.x) dprev[t] = a.delta_g[t];
   }
+  // async staging: bulk-copy a tile's W blocks (current, previous) of pass `bk` into a stage
+  auto issue = [&](int tile, uint32_t stage, int bk) {
+    fence_proxy_async();
+    const bool hc = bk < nblk, hp = bk > 0;
+    const uint32_t bytes = (hc ? kTile * B * 4u : 0u) + (hp ? kTile * B * 4u : 0u) + cpp * 4u;
+    mbar_expect_tx(&mbar[stage], bytes);
+    bulk_copy_g2s(cps + stage * cpp, a.colptr + (int64_t)tile * cpp, cpp * 4u, &mbar[stage]);
+    float* dst = wbuf + (size_t)stage * 2 * kTile * B;
+    if (hc) bulk_copy_g2s(dst, a.wt + ((int64_t)tile * a.nblk8 + bk) * kTile * B, kTile * B * 4u, &mbar[stage]);
+    if (hp)
+      bulk_copy_g2s(dst + kTile * B, a.wt + ((int64_t)tile * a.nblk8 + bk - 1) * kTile * B, kTile * B * 4u,
+                    &mbar[stage]);
+  };
+  bool prefetched = false;
   for (int blk = a.split ? a.blk_begin : 0; blk <= (a.split ? a.blk_begin : nblk); ++blk) {
     const bool has_cur = blk < nblk, has_prev = blk > 0;
     const int k0 = blk * B;
@@ -763,29 +777,19 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
       const int j = t / p, pe = t - j * p;
       dold[t] = j < nb ? a.atoms[(int64_t)(k0 + j) * p + pe] : 0.0f;
     }
-    // async staging: bulk-copy the tile's W blocks (current, previous) into a stage
-    auto issue = [&](int tile, uint32_t stage) {
-      fence_proxy_async();
-      const uint32_t bytes = (has_cur ? kTile * B * 4u : 0u) + (has_prev ? kTile * B * 4u : 0u) + cpp * 4u;
-      mbar_expect_tx(&mbar[stage], bytes);
-      bulk_copy_g2s(cps + stage * cpp, a.colptr + (int64_t)tile * cpp, cpp * 4u, &mbar[stage]);
-      float* dst = wbuf + (size_t)stage * 2 * kTile * B;
-      if (has_cur) bulk_copy_g2s(dst, a.wt + ((int64_t)tile * a.nblk8 + blk) * kTile * B, kTile * B * 4u, &mbar[stage]);
-      if (has_prev)
-        bulk_copy_g2s(dst + kTile * B, a.wt + ((int64_t)tile * a.nblk8 + blk - 1) * kTile * B, kTile * B * 4u,
-                      &mbar[stage]);
-    };
+    const bool pf = prefetched;   // this pass's first tile was issued at the end of the previous pass
+    prefetched = false;
     __syncthreads();
-    if (NSTAGE == 2 && t_lo < t_hi) {
-      if (threadIdx.x == 0 && !(a.dbg & 4)) issue(t_lo, seq & 1);
+    if (NSTAGE == 2 && t_lo < t_hi && !pf) {
+      if (threadIdx.x == 0 && !(a.dbg & 4)) issue(t_lo, seq & 1, blk);
     }
     for (int tile = t_lo; tile < t_hi; ++tile, ++seq) {
       const uint32_t st = NSTAGE == 2 ? (seq & 1) : 0;
       __syncthreads();   // previous tile fully consumed: its stage and cps buffer are free
       prof(0);
       if (threadIdx.x == 0 && !(a.dbg & 4)) {
-        if (NSTAGE == 1) issue(tile, 0);
-        else if (tile + 1 < t_hi) issue(tile + 1, st ^ 1);
+        if (NSTAGE == 1) { if (!(pf && tile == t_lo)) issue(tile, 0, blk); }
+        else if (tile + 1 < t_hi) issue(tile + 1, st ^ 1, blk);
       }
       if (lane == 0) { slot_col[wid * 2] = -1; slot_col[wid * 2 + 1] = -1; }
       const int64_t tb = tile_start(tile);
@@ -1064,6 +1068,12 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
     }
     prof(7);
     if (a.split) return;  // split mode: the caller allreduces `reduced` across ranks, then k_dict_update
+    // the next pass's first tile does not depend on the shifts: stage it now
+    // (the owner scratch it overwrites is done) so it lands during the barrier
+    if (t_lo < t_hi && !(a.dbg & 4)) {
+      if (threadIdx.x == 0) issue(t_lo, NSTAGE == 2 ? (seq & 1) : 0u, blk + 1);
+      prefetched = true;
+    }
     __threadfence();
     prof(10);
     grid_sync(a.bar);
