@@ -228,6 +228,90 @@ def problem_desc(cfg, epochs, warm, dc):
     return d
 
 
+# BASELINE.json configs other than the headline configs[1], one device sweep each
+# (configs[3]/[4] state no epoch count: 10 is assumed)
+OTHER_CFGS = {
+    0: dict(shape=(256, 256), ratio=0.25, kind="uniform-random", patch=(8, 8), k=64, epochs=10,
+            what="2D 256x256 STEM-like, 25% uniform, 8x8, K=64, 10 iterations"),
+    2: dict(shape=(512, 512), ratio=0.25, kind="line-hop", patch=(8, 8), k=256, epochs=2,
+            what="512x512 live frame, 25% line-hop, 8x8, K=256 (sweep rate; frames/s under 'live')"),
+    3: dict(shape=(256, 256, 128), ratio=0.20, kind="uniform-random", patch=(8, 8, 4), k=512, epochs=10,
+            what="hyperspectral cube 256x256x128, 20% uniform, 8x8x4 patches, K=512, mean subtraction off"),
+    4: dict(shape=(4096, 4096), ratio=0.10, kind="uniform-random", patch=(8, 8), k=256, epochs=10,
+            what="2D 4096x4096 STEM-like, 10% uniform, 8x8, K=256 (single GPU)"),
+}
+FP32_PEAK_TF = 74.45  # derived: 148 SM x 128 lanes x 2 x 1.965 GHz
+
+
+def config_inputs(cfg, seed=0):
+    from paper_2311_15061_b200 import inputs
+
+    if len(cfg["shape"]) == 2:
+        img = inputs.stem_lattice(cfg["shape"], seed=seed)
+    else:  # cube: a STEM-like band image with a smooth spectral modulation per band
+        base = inputs.stem_lattice(cfg["shape"][:2], seed=seed)
+        spec = 0.5 + 0.5 * np.sin(np.linspace(0.0, 3.0 * np.pi, cfg["shape"][2]))
+        img = base[:, :, None] * spec[None, None, :]
+    mask = inputs.make_mask(cfg["shape"], cfg["ratio"], cfg["kind"], seed)
+    return img, mask
+
+
+def all_configs(args):
+    """Device sweep throughput of every other BASELINE config (same code path as
+    `value`: state resident, CUDA events, philox draws), with the sweep's
+    roofline: floor = max(12*|Omega|*K flops / FP32 peak, 15 B per update / HBM)."""
+    import torch
+
+    from paper_2311_15061_b200 import _lib
+    from paper_2311_15061_b200 import bpfa as gb
+    from paper_2311_15061_b200 import patches as pp
+    from paper_2311_15061_b200.metrics import psnr
+
+    lib = _lib.load()
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    out = {}
+    for cid, cfg in OTHER_CFGS.items():
+        img, mask = config_inputs(cfg)
+        pm = pp.extract_patches(img, mask, pp.PatchSpec(cfg["patch"]), len(cfg["shape"]) == 2)
+        hp = gb.Hyperparams(num_atoms=cfg["k"])
+        st = gb.init_state(pm, hp, 0, "prior")
+        for _ in range(3):
+            gb.gibbs_epoch(st, pm, hp, rng="philox", check=False)
+        torch.cuda.synchronize()
+        lib.pb_phase_timing(1)
+        stream = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.config_steps):
+            gb.gibbs_epoch(st, pm, hp, rng="philox", check=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.config_steps
+        phase = (ctypes.c_double * 4)()
+        nph = ctypes.c_int64()
+        lib.pb_phase_read(phase, ctypes.byref(nph))
+        lib.pb_phase_timing(0)
+        n, k = pm.num_patches, cfg["k"]
+        upd = n * k
+        floor_ms = 1e3 * max(12.0 * pm.n_obs * k / (FP32_PEAK_TF * 1e12), 15.0 * upd / (peaks["hbm_gbs"] * 1e9))
+        est = gb.compose_estimates(st)
+        rec = pp.reconstitute(pm, est)
+        out[f"configs[{cid}]"] = {
+            "workload": cfg["what"], "patches": n, "atoms": k, "patch_size": pm.patch_size,
+            "observed_per_patch": pm.n_obs / n, "ms_per_sweep": ms, "updates_per_s": upd / (ms * 1e-3),
+            "ms_per_run": ms * cfg["epochs"], "epochs_per_run": cfg["epochs"],
+            "dict_ms": phase[1] / max(1, nph.value), "code_ms": phase[2] / max(1, nph.value),
+            "roofline_floor_ms": floor_ms, "roofline_frac": floor_ms / ms,
+            "psnr_db_after": psnr(rec, img), "sweeps": 3 + args.config_steps,
+        }
+        if st._sc().diverged:
+            out[f"configs[{cid}]"]["diverged"] = True
+        del st, pm, est, rec
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_gpu_arm(args):
     import torch
 
@@ -395,6 +479,7 @@ def run_gpu_arm(args):
                       + (" (per rank; ranks run independent streams)" if world > 1 else ""),
             "target_fps": 30}
     lib.pb_problem_destroy(lpr)
+    del st, pm, est
 
     line = {
         "metric": "BPFA patch-atom updates/sec", "value": value, "unit": "updates/s", "n_gpus": world,
@@ -418,6 +503,8 @@ def run_gpu_arm(args):
         "gpu_launches": (4 if world == 1 else 2 * ((k + 7) // 8) + 4) * args.steps,
         "e2e": e2e, "live": live, "quality": quality, "roofline": roofline,
     }
+    if world == 1 and not args.no_configs:
+        line["configs"] = all_configs(args)
     if rank == 0 and world == 1 and not args.no_cpu:
         r = cpu_epoch_sample(seconds_budget=args.cpu_seconds)
         tot = sum(r["times"])
@@ -443,6 +530,8 @@ def main():
     ap.add_argument("--live-frames", type=int, default=20)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config sweep timings")
+    ap.add_argument("--config-steps", type=int, default=3)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -163,8 +163,9 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
   if (d->resid_mode == PB_RESID_RECOMPUTE) {
     rc = launch_resid_compact(c, st);                    // residual_full (bpfa.py:297)
   } else if (d->resid_mode == PB_RESID_FROM_VALUES) {    // Z*S == 0  =>  R = X
-    if (cudaMemcpyAsync(ws.r_csc, ix.x_csc, (size_t)d->index->nnz * 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
-        cudaMemsetAsync(ws.wt, 0, ws.wt_bytes, st) != cudaSuccess) {
+    // (the tile-blocked code copy W is not cleared: the prior-draw dictionary
+    // step below does not read it and the code step rewrites all of it)
+    if (cudaMemcpyAsync(ws.r_csc, ix.x_csc, (size_t)d->index->nnz * 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
       set_error("residual copy failed");
       rc = PB_ECUDA;
     }
@@ -187,7 +188,12 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
     g.ld = c.ld;
     g.nnz = d->index->nnz;
     g.delta_g = ws.delta_g;   // atom shifts of the last updated block [8][P]
-    if (!d->allreduce) {
+    if (d->resid_mode == PB_RESID_FROM_VALUES) {
+      // Z*S == 0: every moment sum is 0 on every rank, the atoms are prior
+      // redraws and the residual does not move (the first sweep of a cold
+      // inpaint and of every warm-reset live frame)
+      if ((rc = launch_dict_prior(g, st))) return rc;
+    } else if (!d->allreduce) {
       if ((rc = launch_dict_gram(g, st))) return rc;   // fused: all passes in one persistent launch
     } else {
       // split (sharded) mode: per atom block, local pass -> allreduce of the

@@ -1102,6 +1102,45 @@ __global__ void k_dict_update(DictGramArgs a, int blk) {
   for (int t = threadIdx.x; t < B * a.p; t += blockDim.x) a.delta_g[t] = dprev[t];
 }
 
+// Dictionary step on all-zero codes (fresh or warm-reset state, Z*S == 0):
+// every moment sum is exactly 0, so each atom is redrawn from its prior
+// d_k = g / sqrt(P) (bpfa.py:161-166, 300-307) and the
+// residual shifts R += w (x) delta vanish.  The same f64 draw arithmetic as the
+// full step (atom_pixel_update on zero sums), so the atoms are bit-identical to
+// it, without the K/8 passes over the residual.  One CTA per atom block.
+template <int B>
+__global__ void k_dict_prior(DictGramArgs a) {
+  using L = GramLayout<B>;
+  extern __shared__ float sp[];
+  float* dsh = sp;                       // B * p shifts (discarded: W == 0)
+  __shared__ double zero[L::NACC];
+  for (int q = threadIdx.x; q < L::NACC; q += blockDim.x) zero[q] = 0.0;
+  __syncthreads();
+  const int blk = blockIdx.x, k0 = blk * B;
+  const int nb = min(B, a.k - k0);
+  for (int pe = threadIdx.x; pe < a.p; pe += blockDim.x) {
+    // the old atoms go to shared memory first (atom_pixel_update reads d_old
+    // after writing the new atom); slot [j*p+pe] is then overwritten by the
+    // (unused) shift of atom j only after its last read
+#pragma unroll
+    for (int j = 0; j < B; ++j) dsh[j * a.p + pe] = j < nb ? a.atoms[(int64_t)(k0 + j) * a.p + pe] : 0.0f;
+    atom_pixel_update<B>(zero, pe, a.p, k0, nb, a.sc->gamma_eps, a.sc->epoch + 1, a.draws, a.key0, a.key1, dsh,
+                         a.atoms, dsh, nullptr, nullptr);
+  }
+}
+
+int launch_dict_prior(const DictGramArgs& a, cudaStream_t st) {
+  constexpr int B = kWB;
+  const int nblk = (a.k + B - 1) / B;
+  const int th = a.p < 256 ? ((a.p + 31) / 32) * 32 : 256;
+  const size_t smem = (size_t)B * a.p * sizeof(float);
+  if (smem > 48 * 1024) PB_CUDA_TRY(cudaFuncSetAttribute(k_dict_prior<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         (int)smem));
+  k_dict_prior<B><<<nblk, th, smem, st>>>(a);
+  PB_LAUNCH_CHECK();
+  return PB_OK;
+}
+
 // ---------------------------------------------------------------------------
 static int sm_count_c() {
   int dev = 0, sms = 148;

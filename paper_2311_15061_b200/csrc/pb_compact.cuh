@@ -88,6 +88,8 @@ int launch_code_compact(const CompactArgs& a, int mode, int& nblocks, cudaStream
 int code_split_choose(const int32_t* hist, int p, int cmax);
 int code_launch_blocks(int cmax, int64_t n);  // blocks of patches (= S^2/R^2 pairs) of a launch
 int launch_dict_gram(const DictGramArgs& a, cudaStream_t st);
+// dictionary step on all-zero codes: prior redraw of every atom (bit-identical to launch_dict_gram on W == 0)
+int launch_dict_prior(const DictGramArgs& a, cudaStream_t st);
 int launch_dict_update(const DictGramArgs& a, int blk, cudaStream_t st);
 int dict_gram_blocks(int k);
 size_t dict_gram_partials_bytes(int p, int max_blocks);

@@ -273,3 +273,28 @@ def test_residual_carry_matches_recompute(cuda_device):
     ok = ~(ha["usage"] != hb["usage"]).any(axis=1)
     assert np.abs(ha["weights"][ok] - hb["weights"][ok]).max() <= 1e-3
     assert np.abs(ha["atoms"] - hb["atoms"]).max() <= 1e-4
+
+
+@pytest.mark.parametrize("rng", ["philox", "numpy"])
+def test_zero_codes_dictionary_step_is_prior_redraw(cuda_device, rng):
+    """With Z*S == 0 (fresh init, warm-reset live frame) the dictionary step is
+    the prior redraw d_k = g/sqrt(P).  The short path
+    (k_dict_prior, taken when the codes are known to be zero) must give the same
+    state, bit for bit, as the full K/8-pass kernel run on the same zero codes."""
+    from paper_2311_15061_b200 import inputs
+
+    img = inputs.synthetic_texture((64, 64), seed=4)
+    mask = inputs.make_mask(img.shape, 0.25, "uniform-random", 4)
+    hp = gb.Hyperparams(num_atoms=20)
+    pm = pp.extract_patches(img, mask, pp.PatchSpec((8, 8)), True)
+    a = gb.init_state(pm, hp, 11, "data")
+    b = gb.init_state(pm, hp, 11, "data")
+    b._zero_key = None                       # not known to be zero: residual_full + full dictionary step
+    for _ in range(2):
+        gb.gibbs_epoch(a, pm, hp, rng=rng, check=False)
+        gb.gibbs_epoch(b, pm, hp, rng=rng, check=False)
+        ha, hb = a.to_host(), b.to_host()
+        for key in ("atoms", "usage", "weights", "pi"):
+            assert np.array_equal(ha[key], hb[key]), key
+        assert ha["weight_precision"] == hb["weight_precision"]
+        assert ha["noise_precision"] == hb["noise_precision"]
