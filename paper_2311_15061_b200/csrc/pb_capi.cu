@@ -59,6 +59,7 @@ struct EpochWs {
   int32_t* m_count;
   float* delta_g;   // atom shifts of the last updated block [8][P] (dictionary step exchange)
   unsigned* ctr;    // dynamic block counters of the code-step launches [2]
+  float* dt_img;    // the code step's pre-packed transposed dictionary chunks
 };
 static const int kMaxDictBlocks = 148 * 8;
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -75,8 +76,13 @@ static size_t ws_bytes(int64_t n, int p, int k, int64_t nnz, EpochWs* ws, char* 
   char* mc = take((size_t)k * 4);
   char* dg = take((size_t)8 * p * 4);
   char* ct = take(16);
+  int dt_nch = 0;
+  int64_t dt_imgf = 0;
+  code_dt_layout(p, k, nullptr, &dt_imgf, &dt_nch);
+  char* di = take((size_t)dt_imgf * dt_nch * 4);
   if (ws) {
     ws->ctr = (unsigned*)ct;
+    ws->dt_img = (float*)di;
     ws->delta_g = (float*)dg;
     ws->r_csc = (float*)r; ws->wt = (float*)wt; ws->wt_bytes = wtb;
     ws->partials = (float*)pa; ws->reduced = (double*)rd;
@@ -213,6 +219,8 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
   int nblocks = 0;
   phase_mark(kPhCode, st);
   c.blk_ctr = ws.ctr;
+  c.dt_img = ws.dt_img;
+  if ((rc = launch_pack_dt(d->atoms, d->p, d->k, ws.dt_img, st))) return rc;
   if (d->index->split_count > 0) {
     // narrow launch for most patches (stream st) and, concurrently on a side
     // stream, the wide launch over the listed outliers; both claim blocks

@@ -134,6 +134,35 @@ __global__ void __launch_bounds__(256) k_resid_compact(CompactArgs a) {
 // both uniforms (x, y) and a Box-Muller normal pair (z, w); counter = (global
 // patch, k/2, epoch | domain).  The kernel is persistent: D is staged once per
 // CTA and the CTA walks patch blocks of blockDim/G.
+// --- mbarrier + 1-D bulk async copy (TMA engine) helpers --------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// 16-byte shared load from a precomputed shared-window address (volatile: the
+// staged tile is produced by the async proxy, keep it behind the mbarrier wait)
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// global -> shared bulk copy completing on an mbarrier (size and addresses 16-byte aligned)
+__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
 struct CodeConst {
   int64_t i, ic;
   bool live;
@@ -308,8 +337,20 @@ __device__ __forceinline__ void code_atoms(const CompactArgs& a, const CodeConst
   }
 }
 
-// Stage atoms [k0, k0+kn) transposed into DT (pitch kp, P+1 rows, zero row P and
-// zero pad columns).  Coalesced global reads along p.
+// Stage chunk `ci` of the pre-packed transposed dictionary (k_pack_dt): a
+// plain 16-byte vector copy (no index arithmetic; the image is L2-resident).
+// The caller synchronizes the CTA before (previous contents consumed) and after.
+__device__ __forceinline__ void stage_dt_chunk(float* dt, const CompactArgs& a, int ci) {
+  const float4* __restrict__ src = (const float4*)(a.dt_img + (int64_t)ci * a.dt_img_floats);
+  float4* dst = (float4*)dt;
+  const int n4 = (int)(a.dt_img_floats >> 2);
+#pragma unroll 4
+  for (int t = threadIdx.x; t < n4; t += blockDim.x) dst[t] = __ldg(src + t);
+}
+
+// Stage atoms [k0, k0+kn) transposed into DT straight from D (pitch kp, P+1
+// rows, zero row P and zero pad columns): the multi-lane (G > 1) variants, whose
+// register allocation the vector-copy path perturbs into spills.
 __device__ __forceinline__ void stage_atoms_t(float* dt, const float* __restrict__ atoms, int k0, int kn, int p,
                                               int kp) {
   for (int t = threadIdx.x; t < (p + 1) * kp; t += blockDim.x) {
@@ -327,7 +368,8 @@ __device__ __forceinline__ void code_patch_range(const CompactArgs& a, const Cod
     for (int k0 = 0; k0 < a.k; k0 += a.kc) {
       const int kn = min(a.kc, a.k - k0);
       __syncthreads();
-      stage_atoms_t(dt, a.atoms, k0, kn, a.p, kp);
+      if constexpr (G == 1) stage_dt_chunk(dt, a, k0 / a.kc);
+      else stage_atoms_t(dt, a.atoms, k0, kn, a.p, kp);
       __syncthreads();
       code_atoms<CMAX, W, G, MODE>(a, c, t, k0, k0 + kn, dt, r, addr);
 #pragma unroll
@@ -341,7 +383,7 @@ __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
   extern __shared__ __align__(16) float sm[];
   const int kp = a.kc + 2;                     // DT row pitch (kc % 8 == 0  =>  kp/2 odd)
   float* dt = sm;                              // (P+1) * kp
-  float* logit = dt + (size_t)(a.p + 1) * kp;  // K
+  float* logit = dt + (G == 1 ? a.dt_img_floats : (int64_t)(a.p + 1) * kp);  // K (after the DT chunk)
   int* mcnt = (int*)(logit + a.k);             // K
   float* wwin = (float*)(mcnt + a.k);          // (blockDim / G) * 9
   __shared__ double red[32];
@@ -361,7 +403,10 @@ __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
     logit[k] = (float)(log(pk) - log1p(-pk));
     mcnt[k] = 0;
   }
-  if (a.kc >= a.k) stage_atoms_t(dt, a.atoms, 0, a.k, a.p, kp);
+  if (a.kc >= a.k) {
+    if constexpr (G == 1) stage_dt_chunk(dt, a, 0);
+    else stage_atoms_t(dt, a.atoms, 0, a.k, a.p, kp);
+  }
   __syncthreads();
   const int row_bytes = kp * 4;
   CodeThread t;
@@ -527,35 +572,6 @@ struct GramLayout {
   __host__ __device__ static constexpr int gidx(int j, int l) { return B + 2 * (pairbase(j) + l / 2) + (l & 1); }
 };
 static_assert(GramLayout<8>::NACC == 48 && GramLayout<8>::NP == 48, "layout of the 8-atom block");
-
-// --- mbarrier + 1-D bulk async copy (TMA engine) helpers --------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
-}
-// 16-byte shared load from a precomputed shared-window address (volatile: the
-// staged tile is produced by the async proxy, keep it behind the mbarrier wait)
-__device__ __forceinline__ float4 lds128(uint32_t addr) {
-  float4 v;
-  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
-  return v;
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-// global -> shared bulk copy completing on an mbarrier (size and addresses 16-byte aligned)
-__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
 
 __device__ __forceinline__ uint64_t gtimer() {
   uint64_t t;
@@ -1141,6 +1157,45 @@ int launch_dict_prior(const DictGramArgs& a, cudaStream_t st) {
   return PB_OK;
 }
 
+// The code step's transposed dictionary, pre-packed once per sweep in exactly
+// the shared-memory layout of each staged chunk: image[ci][pe * kp + kk] =
+// D[ci*kc + kk][pe] (0 for the pad columns and the zero row pe == P), each chunk
+// padded to a multiple of 16 bytes, so staging is a single bulk copy.
+__global__ void k_pack_dt(const float* __restrict__ atoms, int p, int k, int kc, int64_t img_floats, int nchunks,
+                          float* __restrict__ img) {
+  const int kp = kc + 2;
+  const int64_t total = (int64_t)nchunks * img_floats;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int ci = (int)(t / img_floats);
+    const int rem = (int)(t - (int64_t)ci * img_floats);
+    const int pe = rem / kp, kk = rem - pe * kp;
+    const int katom = ci * kc + kk;
+    img[t] = (pe < p && kk < kc && katom < k) ? atoms[(int64_t)katom * p + pe] : 0.0f;
+  }
+}
+
+void code_dt_layout(int p, int k, int* kc_out, int64_t* img_floats_out, int* nchunks_out) {
+  // DT chunk: kc atoms (a multiple of 8) x (P+1) rows of pitch kc+2 within ~100 KB
+  // (two CTAs per SM); the whole dictionary when it fits
+  const int k8 = (int)ceil_div(k, 8) * 8;
+  int kc = (int)(((100 * 1024) / ((size_t)(p + 1) * 4) - 2) & ~(size_t)7);
+  if (kc < 8) kc = 8;
+  if (kc > k8) kc = k8;
+  if (kc_out) *kc_out = kc;
+  if (img_floats_out) *img_floats_out = (((int64_t)(p + 1) * (kc + 2)) + 3) & ~(int64_t)3;
+  if (nchunks_out) *nchunks_out = (int)ceil_div(k, kc);
+}
+
+int launch_pack_dt(const float* atoms, int p, int k, float* img, cudaStream_t st) {
+  int kc, nch;
+  int64_t imgf;
+  code_dt_layout(p, k, &kc, &imgf, &nch);
+  const int64_t total = imgf * nch;
+  k_pack_dt<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 1184), 256, 0, st>>>(atoms, p, k, kc, imgf, nch, img);
+  PB_LAUNCH_CHECK();
+  return PB_OK;
+}
+
 // ---------------------------------------------------------------------------
 static int sm_count_c() {
   int dev = 0, sms = 148;
@@ -1250,14 +1305,11 @@ int launch_code_compact(const CompactArgs& a_in, int mode, int& nblocks, cudaStr
   if (!pick_compact(a.cmax, c, g)) { set_error("patch has too many observed elements (%d)", a.cmax); return PB_EUNSUPPORTED; }
   normalize_cg(c, g);
   const int th = 256;
-  // DT chunk: kc atoms (a multiple of 8) x (P+1) rows of pitch kc+2 within ~100 KB
-  // (two CTAs per SM); the whole dictionary when it fits
+  // DT chunks as pre-packed by launch_pack_dt (the caller packs a.dt_img first)
+  if (!a.dt_img) { set_error("code step without the packed dictionary image"); return PB_EVALUE; }
   const size_t fixed = (size_t)a.k * 8 + (size_t)(th / g) * 9 * 4;
-  const int k8 = (int)ceil_div(a.k, 8) * 8;
-  int kc = (int)(((100 * 1024) / ((size_t)(a.p + 1) * 4) - 2) & ~(size_t)7);
-  if (kc < 8) kc = 8;
-  a.kc = kc >= k8 ? k8 : kc;
-  const size_t smem = (size_t)(a.kc + 2) * (a.p + 1) * 4 + fixed;
+  code_dt_layout(a.p, a.k, &a.kc, &a.dt_img_floats, nullptr);
+  const size_t smem = (size_t)a.dt_img_floats * 4 + fixed;
   if (smem > 220 * 1024) { set_error("too many atoms for the code step (K=%d)", a.k); return PB_EUNSUPPORTED; }
   const int64_t nb = ceil_div((a.plist ? a.plist_n : a.n) * g, th);
   if (a.zero_mcount) PB_CUDA_TRY(cudaMemsetAsync(a.m_count, 0, (size_t)a.k * sizeof(int32_t), st));

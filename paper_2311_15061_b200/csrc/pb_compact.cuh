@@ -45,6 +45,8 @@ struct CompactArgs {
   int64_t plist_n;
   int zero_mcount;      // the launch zeroes the usage counts first
   unsigned* blk_ctr;    // dynamic block counter of the launch (zeroed by the launcher)
+  const float* dt_img;  // pre-packed transposed dictionary chunks (launch_pack_dt)
+  int64_t dt_img_floats;
 };
 
 struct DictGramArgs {
@@ -90,6 +92,9 @@ int code_launch_blocks(int cmax, int64_t n);  // blocks of patches (= S^2/R^2 pa
 int launch_dict_gram(const DictGramArgs& a, cudaStream_t st);
 // dictionary step on all-zero codes: prior redraw of every atom (bit-identical to launch_dict_gram on W == 0)
 int launch_dict_prior(const DictGramArgs& a, cudaStream_t st);
+// code step's transposed-dictionary chunks: layout and the per-sweep packing kernel
+void code_dt_layout(int p, int k, int* kc_out, int64_t* img_floats_out, int* nchunks_out);
+int launch_pack_dt(const float* atoms, int p, int k, float* img, cudaStream_t st);
 int launch_dict_update(const DictGramArgs& a, int blk, cudaStream_t st);
 int dict_gram_blocks(int k);
 size_t dict_gram_partials_bytes(int p, int max_blocks);

@@ -80,3 +80,14 @@ def test_split_code_step_replay(cuda_device, monkeypatch, split):
     ix = pm.index()
     assert ix.split_count == split and ix.n_outliers > 0
     assert _replay(img, mask, (6, 6), True, 10, 3, 2) <= 4
+
+
+def test_chunked_dictionary_staging_replay(cuda_device):
+    """Code step with the dictionary staged in chunks (10x10 patches, K = 264:
+    (P+1) x (K+2) floats exceed a CTA's DT budget, so k_pack_dt builds two
+    chunks and each block of patches stages them in turn; single-lane patches,
+    K not a multiple of the chunk): replay parity per epoch."""
+    rng = np.random.default_rng(16)
+    img = rng.random((30, 31))
+    mask = rng.random(img.shape) < 0.12
+    assert _replay(img, mask, (10, 10), True, 264, 4, 2) <= 4
