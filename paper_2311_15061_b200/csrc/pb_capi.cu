@@ -161,6 +161,7 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
   c.g_draw = d->rng_mode == PB_RNG_REPLAY ? d->code_g : nullptr;
   c.block_sums = ws.block_sums; c.m_count = ws.m_count;
   c.n = d->n; c.p = d->p; c.k = d->k; c.key0 = k0; c.key1 = k1;
+  philox_round_keys(k0, k1, c.rk);
   c.ld = d->ld > d->n ? d->ld : d->n;
   c.i_offset = d->i_offset;
   const int64_t n_global = d->n_global > 0 ? d->n_global : d->n;

@@ -58,6 +58,24 @@ __device__ __forceinline__ u32x4 philox4x32_10(u32x4 c, uint32_t k0, uint32_t k1
   return c;
 }
 
+// The same generator with the 10 round keys precomputed (kernel parameters:
+// the XORs take them as constant-bank operands, no key schedule per block).
+__device__ __forceinline__ u32x4 philox4x32_10_rk(u32x4 c, const uint32_t (&rk)[20]) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = u32x4{hi1 ^ c.y ^ rk[2 * r], lo1, hi0 ^ c.w ^ rk[2 * r + 1], lo0};
+  }
+  return c;
+}
+inline void philox_round_keys(uint32_t k0, uint32_t k1, uint32_t (&rk)[20]) {
+  for (int r = 0; r < 10; ++r) {
+    rk[2 * r] = k0 + (uint32_t)r * 0x9E3779B9u;
+    rk[2 * r + 1] = k1 + (uint32_t)r * 0xBB67AE85u;
+  }
+}
+
 // (0,1) uniform with 24 random bits, exactly representable in f32.
 __device__ __forceinline__ float u01_24(uint32_t u) {
   return (float)(u >> 8) * 5.9604644775390625e-08f + 2.98023223876953125e-08f;

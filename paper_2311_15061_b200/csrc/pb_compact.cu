@@ -290,9 +290,9 @@ __device__ __forceinline__ void code_atoms(const CompactArgs& a, const CodeConst
         if (k + 1 < k1) { ud1 = a.u_draw[di + a.n]; gd1 = a.g_draw[di + a.n]; }
       } else {
         const int64_t gi = c.i + a.i_offset;  // global patch index: shards draw the 1-GPU streams
-        const u32x4 rnd = philox4x32_10(u32x4{(uint32_t)gi, (uint32_t)(gi >> 32), (uint32_t)(k >> 1),
-                                              ((uint32_t)c.epoch & 0xFFFFFFu) | (kDomCode << 24)},
-                                        a.key0, a.key1);
+        const u32x4 rnd = philox4x32_10_rk(u32x4{(uint32_t)gi, (uint32_t)(gi >> 32), (uint32_t)(k >> 1),
+                                                 ((uint32_t)c.epoch & 0xFFFFFFu) | (kDomCode << 24)},
+                                           a.rk);
         box_muller_fast(rnd.z, rnd.w, g0, g1);
         uu0 = u01_24(rnd.x);
         uu1 = u01_24(rnd.y);

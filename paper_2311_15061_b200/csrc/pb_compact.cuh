@@ -37,6 +37,7 @@ struct CompactArgs {
   int64_t ld;           // row pitch of usage/weights (K, ld), ld >= n
   int p, k, kc;
   uint32_t key0, key1;
+  uint32_t rk[20];      // Philox round keys of (key0, key1) (philox_round_keys)
   int64_t i_offset;     // global index of local patch 0 (draw counters of a shard)
   // code-step split: the main launch skips patches with more than `split`
   // observed elements; the second launch runs exactly the patches in plist
