@@ -11,7 +11,10 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libpb200.so")
+# PB200_LIB_VARIANT=name loads _lib/variants/libpb200_<name>.so (kernel-tuning experiments)
+_VARIANT = os.environ.get("PB200_LIB_VARIANT")
+LIB_PATH = os.path.join(_HERE, "_lib", "variants", f"libpb200_{_VARIANT}.so") if _VARIANT else \
+    os.path.join(_HERE, "_lib", "libpb200.so")
 
 PB_OK = 0
 PB_ESHAPE = -1

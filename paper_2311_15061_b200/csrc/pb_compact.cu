@@ -680,7 +680,7 @@ __device__ __forceinline__ void atom_block_update(const double* red, int p, int 
 }
 
 constexpr double kTileVisitCost = 3000.0;  // element-equivalents of one tile visit (work split)
-constexpr int kDictGroupLanes = 8;  // lanes per segment group in the element phase
+constexpr int kDictGroupLanes = 16;  // lanes per segment group in the element phase (8: +3 % at configs[1])
 constexpr int kDictSegLen = 256;   // max elements of one segment (a multiple of the group size)
 
 // NW warps per CTA, NSTAGE staging buffers (2: the next tile is bulk-copied
@@ -856,7 +856,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
         __syncwarp();
         // carve the next NG segments (warp-uniform) and put the first kPf
         // elements of this lane's segment in flight
-        constexpr int kPf = 4;
+        constexpr int kPf = 6;   // elements in flight per lane (2: 2.7x slower; 8: spills)
         const uint16_t* eloc_t = a.e_loc + tb;
         float* r_t = a.r_csc + tb;
         int ms = 0, mt = 0, mc = -1, its = 0;
