@@ -573,6 +573,39 @@ struct GramLayout {
 };
 static_assert(GramLayout<8>::NACC == 48 && GramLayout<8>::NP == 48, "layout of the 8-atom block");
 
+// L2 residency hints: the dictionary step re-reads the residual and the element
+// index in every one of its K/8+1 passes (61 MB at configs[1], L2 is 126 MB)
+// while the code copy W streams through (each block is read twice: as the
+// current block, then as the previous block of the next pass).
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ float ldg_hint(const float* p, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint16_t ldg_hint(const uint16_t* p, uint64_t pol) {
+  uint16_t v;
+  asm volatile("ld.global.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void stg_hint(float* p, float v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void bulk_copy_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                                   uint64_t pol) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
+
 __device__ __forceinline__ uint64_t gtimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -769,6 +802,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
     for (int t = threadIdx.x; t < B * p; t += blockDim.x) dprev[t] = a.delta_g[t];
   }
   // async staging: bulk-copy a tile's W blocks (current, previous) of pass `bk` into a stage
+  const uint64_t pol_last = l2_policy_evict_last(), pol_first = l2_policy_evict_first();
   auto issue = [&](int tile, uint32_t stage, int bk) {
     fence_proxy_async();
     const bool hc = bk < nblk, hp = bk > 0;
@@ -777,9 +811,9 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
     bulk_copy_g2s(cps + stage * cpp, a.colptr + (int64_t)tile * cpp, cpp * 4u, &mbar[stage]);
     float* dst = wbuf + (size_t)stage * 2 * kTile * B;
     if (hc) bulk_copy_g2s(dst, a.wt + ((int64_t)tile * a.nblk8 + bk) * kTile * B, kTile * B * 4u, &mbar[stage]);
-    if (hp)
-      bulk_copy_g2s(dst + kTile * B, a.wt + ((int64_t)tile * a.nblk8 + bk - 1) * kTile * B, kTile * B * 4u,
-                    &mbar[stage]);
+    if (hp)  // last use of the previous block
+      bulk_copy_g2s_hint(dst + kTile * B, a.wt + ((int64_t)tile * a.nblk8 + bk - 1) * kTile * B, kTile * B * 4u,
+                         &mbar[stage], pol_first);
   };
   bool prefetched = false;
   for (int blk = a.split ? a.blk_begin : 0; blk <= (a.split ? a.blk_begin : nblk); ++blk) {
@@ -884,7 +918,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
             const int e = ms + sub + d * S;
             ilb[d] = 0;
             rb[d] = 0.0f;
-            if (e < mt) { ilb[d] = eloc_t[e]; rb[d] = r_t[e]; }
+            if (e < mt) { ilb[d] = ldg_hint(eloc_t + e, pol_last); rb[d] = ldg_hint(r_t + e, pol_last); }
           }
         };
         carve();
@@ -910,7 +944,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
                 if (it + d >= its) break;
                 const int il = ilb[d];
                 float r = rb[d];
-                if (ec + kPf * S < mt) { ilb[d] = ecp[kPf * S]; rb[d] = rc[kPf * S]; }
+                if (ec + kPf * S < mt) { ilb[d] = ldg_hint(ecp + kPf * S, pol_last); rb[d] = ldg_hint(rc + kPf * S, pol_last); }
                 if (ec < mt) {
                   const uint32_t wo[2] = {(uint32_t)il, (uint32_t)il ^ 16u};  // e_loc holds w_row_off
                   if constexpr (HP) {  // r += w_prev . delta  (packed pairs, two independent chains)
@@ -923,7 +957,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
                     }
 #pragma unroll
                     for (int h = 0; h < B / 4; ++h) r += sh[h].x + sh[h].y;
-                    *rc = r;
+                    stg_hint(rc, r, pol_last);
                   }
                   if constexpr (HC) {
                     float wc[B];
@@ -1356,6 +1390,9 @@ static int launch_dict_gram_b(DictGramArgs a, cudaStream_t st) {
   if (per_sm < 1) { set_error("dictionary step cannot be resident"); return PB_EUNSUPPORTED; }
   int blocks = sm_count_c() * per_sm;
   if (blocks > a.max_blocks) blocks = a.max_blocks;
+  static int cap = -1;   // PB_DICT_MAX_CTAS: grid cap for tuning experiments
+  if (cap < 0) { const char* e = getenv("PB_DICT_MAX_CTAS"); cap = e ? atoi(e) : 0; }
+  if (cap > 0 && blocks > cap) blocks = cap;
   PB_CUDA_TRY(cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned), st));
   void* args[] = {&a};
   PB_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(blocks), dim3(th), args, smem, st));
