@@ -738,11 +738,15 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
   float* dold = (float*)(tbs + kTbCache);                // B * p
   float* dprev = dold + B * p;                           // B * p
   double* red64 = (double*)smraw;                        // p * NACC (aliases the staging)
-  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ __align__(8) uint64_t mbar[3];   // [0..1] staging stages, [2] owner partials
   if (threadIdx.x == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
+    mbar_init(&mbar[2], 1);
   }
+  uint32_t pphase = 0;  // parity of mbar[2]
+  // owner reads: shared memory when staged, else L2 (ld.cg)
+  auto ld_part = [&](const float* q) -> float { return a.pstage_off ? *q : __ldcg(q); };
   __syncthreads();
   uint32_t phase_bits = 0;   // parity of each stage's mbarrier
   uint32_t seq = 0;          // running tile-visit counter -> stage = seq & 1
@@ -1059,8 +1063,12 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
     }
     if (!has_cur) break;
     __syncthreads();
-    float* mine = a.partials + (size_t)blockIdx.x * p * L::NACC;
-    for (int t = threadIdx.x; t < p * L::NACC; t += blockDim.x) mine[t] = acc[t];
+    // pixel-major partials [pixel][CTA][NACC]: an owner stages all of its
+    // pixel's partials with one bulk copy
+    for (int t = threadIdx.x; t < p * L::NACC; t += blockDim.x) {
+      const int pe = t / L::NACC, q = t - pe * L::NACC;
+      a.partials[((size_t)pe * gridDim.x + blockIdx.x) * L::NACC + q] = acc[t];
+    }
     __threadfence();
     prof(5);
     grid_sync(a.bar);
@@ -1069,28 +1077,40 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
     // one warp per (pixel, value) sums the G partials lane-strided then by a
     // fixed shuffle tree (f64, deterministic), and the owner performs that
     // pixel's B sequential atom draws right away (pixels are independent).
-    const int nv = p * L::NACC;
     const int npl = blockIdx.x < (unsigned)p ? (p - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     constexpr int NPART = (NW * 32) / L::NACC;   // threads per value
     double* part64 = red64 + (size_t)((p + gridDim.x - 1) / gridDim.x) * L::NACC;  // [NPART][NACC] scratch
     AtomPre* pre = (AtomPre*)(part64 + NPART * L::NACC);                          // [B]
+    // the pixel's G x NACC partials staged in shared memory behind the scratch
+    float* pstage = (float*)(smraw + a.pstage_off);
     for (int i = 0; i < npl; ++i) {
       const int pe = blockIdx.x + i * gridDim.x;
+      const float* pix = a.partials + (size_t)pe * gridDim.x * L::NACC;
+      if (a.pstage_off) {   // one bulk copy of the pixel's partials (contiguous, L2-resident)
+        if (threadIdx.x == 0) {
+          fence_proxy_async();
+          const uint32_t bytes = gridDim.x * L::NACC * 4u;
+          mbar_expect_tx(&mbar[2], bytes);
+          bulk_copy_g2s(pstage, pix, bytes, &mbar[2]);
+        }
+        mbar_wait(&mbar[2], pphase);
+        pphase ^= 1u;
+      }
       if (threadIdx.x < NPART * L::NACC) {
-        // value q over partials b = part, part + NPART, ...: 16 independent loads in flight
+        // value q over partials b = part, part + NPART, ...: 16 independent chains
         const int q = threadIdx.x % L::NACC, part = threadIdx.x / L::NACC;
-        const float* src = a.partials + (size_t)pe * L::NACC + q;
+        const float* src = (a.pstage_off ? (const float*)pstage : pix) + q;
         double acc16[16];
 #pragma unroll
         for (int u = 0; u < 16; ++u) acc16[u] = 0.0;
         int b = part;
         for (; b + 15 * NPART < (int)gridDim.x; b += 16 * NPART) {
 #pragma unroll
-          for (int u = 0; u < 16; ++u) acc16[u] += (double)__ldcg(src + (size_t)(b + u * NPART) * nv);
+          for (int u = 0; u < 16; ++u) acc16[u] += (double)ld_part(src + (size_t)(b + u * NPART) * L::NACC);
         }
 #pragma unroll
         for (int u = 0; u < 16; ++u)  // tail: at most 15 more partials, still independent
-          if (b + u * NPART < (int)gridDim.x) acc16[u] += (double)__ldcg(src + (size_t)(b + u * NPART) * nv);
+          if (b + u * NPART < (int)gridDim.x) acc16[u] += (double)ld_part(src + (size_t)(b + u * NPART) * L::NACC);
 #pragma unroll
         for (int h = 8; h >= 1; h >>= 1)
 #pragma unroll
@@ -1393,6 +1413,15 @@ static int launch_dict_gram_b(DictGramArgs a, cudaStream_t st) {
   static int cap = -1;   // PB_DICT_MAX_CTAS: grid cap for tuning experiments
   if (cap < 0) { const char* e = getenv("PB_DICT_MAX_CTAS"); cap = e ? atoi(e) : 0; }
   if (cap > 0 && blocks > cap) blocks = cap;
+  {  // owner partials staged behind the owner scratch (inside the W staging area) when they fit
+    using L = GramLayout<B>;
+    const size_t npart = (size_t)(NW * 32) / L::NACC;
+    const size_t scratch = ((size_t)(a.p + blocks - 1) / blocks * L::NACC + npart * L::NACC) * 8 + (size_t)B * 40;
+    const size_t off = (scratch + 127) & ~(size_t)127;
+    static int nostage = -1;   // PB_DICT_NO_PSTAGE=1: owners read the partials from L2 (A/B)
+    if (nostage < 0) { const char* e = getenv("PB_DICT_NO_PSTAGE"); nostage = e ? atoi(e) : 0; }
+    a.pstage_off = (!nostage && off + (size_t)blocks * L::NACC * 4 <= wbytes) ? (int)off : 0;
+  }
   PB_CUDA_TRY(cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned), st));
   void* args[] = {&a};
   PB_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(blocks), dim3(th), args, smem, st));

@@ -78,6 +78,7 @@ struct DictGramArgs {
   float* delta_g;
   int max_blocks;
   int wbytes;
+  int pstage_off;       // byte offset of the staged owner partials in shared memory (0: read from L2)
   int64_t n;
   int64_t ld;           // row pitch of usage/weights (K, ld), ld >= n
   int64_t nnz;          // observed elements (host copy of tile_base[ntiles])
