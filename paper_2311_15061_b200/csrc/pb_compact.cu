@@ -507,6 +507,21 @@ __device__ __forceinline__ void grid_sync(unsigned* bar) {
   __syncthreads();
 }
 
+// Monotonic-counter grid barrier: every CTA adds 1 with a release reduction
+// (no returned value to wait for, no reset) and polls until the counter reaches
+// the next multiple of the grid size.  bar[0] is zeroed before the launch.
+__device__ __forceinline__ void grid_sync_mono(unsigned* bar, unsigned& target) {
+  __syncthreads();
+  target += gridDim.x;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    while (ld_acquire(bar) < target) __nanosleep(32);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 // Recursive-halving transpose reduction of NP (= 16*R) per-lane values across a
 // warp: afterwards lane pair (l, l^1) holds the warp sums of values
 // [base(l), base(l)+R) with base = 8R*b4 + 4R*b3 + 2R*b2 + R*b1 (b = lane bits).
@@ -745,6 +760,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
     mbar_init(&mbar[2], 1);
   }
   uint32_t pphase = 0;  // parity of mbar[2]
+  unsigned bar_target = 0;  // grid_sync_mono: arrivals expected so far
   // owner reads: shared memory when staged, else L2 (ld.cg)
   auto ld_part = [&](const float* q) -> float { return a.pstage_off ? *q : __ldcg(q); };
   __syncthreads();
@@ -1069,9 +1085,10 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
       const int pe = t / L::NACC, q = t - pe * L::NACC;
       a.partials[((size_t)pe * gridDim.x + blockIdx.x) * L::NACC + q] = acc[t];
     }
-    __threadfence();
+    // (no per-thread fence: the barrier's bar.sync + the master's gpu-scope
+    // fence and release publish the CTA's partials, as in cooperative groups)
     prof(5);
-    grid_sync(a.bar);
+    if (a.dbg & 16) grid_sync(a.bar); else grid_sync_mono(a.bar + 2, bar_target);
     prof(6);
     // Cross-CTA reduction distributed by PIXEL: CTA c owns pixels c, c+G, ...;
     // one warp per (pixel, value) sums the G partials lane-strided then by a
@@ -1088,7 +1105,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
       const float* pix = a.partials + (size_t)pe * gridDim.x * L::NACC;
       if (a.pstage_off) {   // one bulk copy of the pixel's partials (contiguous, L2-resident)
         if (threadIdx.x == 0) {
-          fence_proxy_async();
+          asm volatile("fence.proxy.async;" ::: "memory");   // generic-proxy partials -> async-proxy read
           const uint32_t bytes = gridDim.x * L::NACC * 4u;
           mbar_expect_tx(&mbar[2], bytes);
           bulk_copy_g2s(pstage, pix, bytes, &mbar[2]);
@@ -1144,9 +1161,8 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
       if (threadIdx.x == 0) issue(t_lo, NSTAGE == 2 ? (seq & 1) : 0u, blk + 1);
       prefetched = true;
     }
-    __threadfence();
     prof(10);
-    grid_sync(a.bar);
+    if (a.dbg & 16) grid_sync(a.bar); else grid_sync_mono(a.bar + 2, bar_target);
     prof(8);
     for (int t = threadIdx.x; t < B * p; t += blockDim.x) dprev[t] = __ldcg(a.delta_g + t);
     __syncthreads();
@@ -1422,7 +1438,7 @@ static int launch_dict_gram_b(DictGramArgs a, cudaStream_t st) {
     if (nostage < 0) { const char* e = getenv("PB_DICT_NO_PSTAGE"); nostage = e ? atoi(e) : 0; }
     a.pstage_off = (!nostage && off + (size_t)blocks * L::NACC * 4 <= wbytes) ? (int)off : 0;
   }
-  PB_CUDA_TRY(cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned), st));
+  PB_CUDA_TRY(cudaMemsetAsync(a.bar, 0, 4 * sizeof(unsigned), st));
   void* args[] = {&a};
   PB_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(blocks), dim3(th), args, smem, st));
   return PB_OK;
