@@ -195,6 +195,10 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
     g.ld = c.ld;
     g.nnz = d->index->nnz;
     g.delta_g = ws.delta_g;   // atom shifts of the last updated block [8][P]
+    g.seg_base = ix.seg_base;
+    { static double sc_env = -1.0;   // PB_DICT_SEG_COST: tuning override of the segment cost
+      if (sc_env < 0.0) { const char* e = getenv("PB_DICT_SEG_COST"); sc_env = e ? atof(e) : kDictSegCost; }
+      g.seg_cost = sc_env; }
     if (d->resid_mode == PB_RESID_FROM_VALUES) {
       // Z*S == 0: every moment sum is 0 on every rank, the atoms are prior
       // redraws and the residual does not move (the first sweep of a cold

@@ -730,6 +730,7 @@ __device__ __forceinline__ void atom_block_update(const double* red, int p, int 
 constexpr double kTileVisitCost = 3000.0;  // element-equivalents of one tile visit (work split)
 constexpr int kDictGroupLanes = 16;  // lanes per segment group in the element phase (8: +3 % at configs[1])
 constexpr int kDictSegLen = 256;   // max elements of one segment (a multiple of the group size)
+static_assert(kDictSegLen == kSegCountLen, "the cost model counts segments of the element phase");
 
 // NW warps per CTA, NSTAGE staging buffers (2: the next tile is bulk-copied
 // while this one is processed; 1: two CTAs share an SM and cover each other's
@@ -777,17 +778,26 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
   // the prefix cost C(e) = e + kTileVisitCost * (tiles started up to e) reaches
   // c/G of the total; a boundary falling in a tile's visit cost snaps to the
   // tile start.  Static and deterministic.
+  // A segment (a column run of <= kSegLen elements) adds a fixed round cost
+  // (transpose reduction, segment carve, first-load latency): kSegCost element
+  // equivalents, spread linearly over the tile's elements.
+  const double seg_cost = a.seg_base ? a.seg_cost : 0.0;
+  auto cost_at = [&](int t) {
+    return (double)a.tile_base[t] + kTileVisitCost * t + (seg_cost > 0.0 ? seg_cost * (double)a.seg_base[t] : 0.0);
+  };
   auto boundary = [&](int c) -> int64_t {
     if (c <= 0) return 0;
     if (c >= (int)gridDim.x) return nnz;
-    const double target = ((double)nnz + kTileVisitCost * a.ntiles) * c / gridDim.x;
+    const double target = cost_at(a.ntiles) * c / gridDim.x;
     int lo = 0, hi = a.ntiles - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if ((double)a.tile_base[mid] + kTileVisitCost * mid <= target) lo = mid; else hi = mid - 1;
+      if (cost_at(mid) <= target) lo = mid; else hi = mid - 1;
     }
-    const double over = target - ((double)a.tile_base[lo] + kTileVisitCost * lo) - kTileVisitCost;
-    const int64_t e = a.tile_base[lo] + (over > 0.0 ? (int64_t)over : 0);
+    const double over = target - cost_at(lo) - kTileVisitCost;
+    const int64_t el = a.tile_base[lo + 1] - a.tile_base[lo];
+    const double work = cost_at(lo + 1) - cost_at(lo) - kTileVisitCost;   // elements + segment costs of tile lo
+    const int64_t e = a.tile_base[lo] + (over > 0.0 && work > 0.0 ? (int64_t)(over * (double)el / work) : 0);
     return min(e, a.tile_base[lo + 1]);
   };
   const int64_t e_lo = boundary(blockIdx.x), e_hi = boundary(blockIdx.x + 1);

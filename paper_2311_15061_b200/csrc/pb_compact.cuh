@@ -79,6 +79,8 @@ struct DictGramArgs {
   int max_blocks;
   int wbytes;
   int pstage_off;       // byte offset of the staged owner partials in shared memory (0: read from L2)
+  const int64_t* seg_base;  // per-tile column-segment prefix (work-split cost model) or null
+  double seg_cost;          // element equivalents of one segment
   int64_t n;
   int64_t ld;           // row pitch of usage/weights (K, ld), ld >= n
   int64_t nnz;          // observed elements (host copy of tile_base[ntiles])
@@ -91,6 +93,7 @@ int launch_code_compact(const CompactArgs& a, int mode, int& nblocks, cudaStream
 // the code step's per-patch limit for the main launch from the count histogram (0 = no split)
 int code_split_choose(const int32_t* hist, int p, int cmax);
 int code_launch_blocks(int cmax, int64_t n);  // blocks of patches (= S^2/R^2 pairs) of a launch
+constexpr double kDictSegCost = 40.0;  // element equivalents of one element-phase segment (work split; live -5 %)
 int launch_dict_gram(const DictGramArgs& a, cudaStream_t st);
 // dictionary step on all-zero codes: prior redraw of every atom (bit-identical to launch_dict_gram on W == 0)
 int launch_dict_prior(const DictGramArgs& a, cudaStream_t st);

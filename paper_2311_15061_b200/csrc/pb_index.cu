@@ -193,6 +193,8 @@ int index_bytes(int64_t n, int p, int64_t nnz_upper, size_t* out) {
   a((size_t)ntiles * 4);              // outlier counts per tile
   a((size_t)(ntiles + 1) * 8);        // outlier bases per tile
   a((size_t)(p + 2) * 4);             // histogram of observed counts
+  a((size_t)ntiles * 4);              // tile_segs
+  a((size_t)(ntiles + 1) * 8);        // seg_base
   *out = b;
   return PB_OK;
 }
@@ -215,6 +217,20 @@ void carve_index(PatchIndex& ix, char* base, int64_t n, int p, int64_t nnz_upper
   ix.out_tot = (int32_t*)take((size_t)ntiles * 4);
   ix.out_base = (int64_t*)take((size_t)(ntiles + 1) * 8);
   ix.hist = (int32_t*)take((size_t)(p + 2) * 4);
+  ix.tile_segs = (int32_t*)take((size_t)ntiles * 4);
+  ix.seg_base = (int64_t*)take((size_t)(ntiles + 1) * 8);
+}
+
+// Column segments of each tile: sum over columns of ceil(len / kSegCountLen).
+__global__ void k_tile_segs(const int32_t* __restrict__ colptr, int ntiles, int p, int32_t* __restrict__ segs) {
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (t >= ntiles) return;
+  const int32_t* cp = colptr + (int64_t)t * colptr_pitch(p);
+  int s = 0;
+  for (int c = lane; c < p; c += 32) s += (cp[c + 1] - cp[c] + kSegCountLen - 1) / kSegCountLen;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) segs[t] = s;
 }
 
 // Histogram of the per-patch observed counts (0..p): shared-memory bins per block.
@@ -284,6 +300,8 @@ int launch_build_index(PatchIndex& ix, const uint8_t* obs, const float* values, 
   k_tile_scan<<<1, 1024, 0, st>>>(ix.tile_tot, ix.ntiles, ix.tile_base);
   k_tile_fill<<<ix.ntiles, kFillThreads, 0, st>>>(obs, values, counts, ix.n, ix.p, ix.tile_base, ix.colptr, ix.e_loc,
                                            ix.x_csc, ix.rowptr, ix.csr_p, ix.csr_pos);
+  k_tile_segs<<<(unsigned)ceil_div(ix.ntiles, 8), 256, 0, st>>>(ix.colptr, ix.ntiles, ix.p, ix.tile_segs);
+  k_tile_scan<<<1, 1024, 0, st>>>(ix.tile_segs, ix.ntiles, ix.seg_base);
   PB_LAUNCH_CHECK();
   return PB_OK;
 }

@@ -7,6 +7,7 @@ namespace pb {
 constexpr int kTile = 1024;        // patches per CSC tile (one dict-step work unit)
 constexpr int kFillThreads = 512;  // index-build block size (two patches per thread)
 constexpr int kWB = 8;             // atoms per block of the tile-blocked code copy W
+constexpr int kSegCountLen = 256;  // segment length of the dictionary step's element phase (cost model)
 
 __host__ __device__ constexpr int colptr_pitch(int p) { return (p + 1 + 3) & ~3; }
 
@@ -35,6 +36,8 @@ struct PatchIndex {
   int32_t* out_tot;     // [ntiles]
   int64_t* out_base;    // [ntiles + 1]; out_base[ntiles] = number of outliers
   int32_t* hist;        // [p + 1] histogram of the observed counts
+  int32_t* tile_segs;   // [ntiles] column segments of each tile (columns cut every kSegCountLen elements)
+  int64_t* seg_base;    // [ntiles + 1] prefix of tile_segs (the dictionary step's work-split cost model)
 };
 
 int index_bytes(int64_t n, int p, int64_t nnz, size_t* out);
