@@ -221,6 +221,70 @@ void carve_index(PatchIndex& ix, char* base, int64_t n, int p, int64_t nnz_upper
   ix.seg_base = (int64_t*)take((size_t)(ntiles + 1) * 8);
 }
 
+// Bank spreading of the CSC order (after k_tile_fill).  The dictionary step's
+// lanes gather each element's W row from shared memory with 16-byte loads whose
+// quarter-warps are 8 CONSECUTIVE elements of a column run; rows land on one of
+// 8 bank quads ((e_loc >> 4) & 7), so a random order costs ~2.2x the ideal
+// wavefronts.  One warp per (tile, column) reorders the run into groups of 8
+// with as few repeated quads as possible (each slot takes the bin with the most
+// elements left among the least used in the group), rewrites e_loc / x_csc and
+// repoints csr_pos.  Deterministic; the sums only see a different fixed order.
+constexpr int kSpreadWarps = 4;   // 32 KB of static shared memory per block
+__global__ void __launch_bounds__(kSpreadWarps * 32) k_csc_spread(const int64_t* __restrict__ tile_base,
+                                                                  const int32_t* __restrict__ colptr, int ntiles, int p,
+                                                                  int64_t n, const int64_t* __restrict__ rowptr,
+                                                                  const uint16_t* __restrict__ csr_p,
+                                                                  uint16_t* __restrict__ e_loc, float* __restrict__ x_csc,
+                                                                  uint32_t* __restrict__ csr_pos) {
+  __shared__ uint16_t s_e[kSpreadWarps][kTile];
+  __shared__ float s_x[kSpreadWarps][kTile];
+  __shared__ uint16_t s_ord[kSpreadWarps][kTile];   // by bin, ascending inside a bin
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t job = (int64_t)blockIdx.x * kSpreadWarps + w;
+  if (job >= (int64_t)ntiles * p) return;
+  const int t = (int)(job / p), pe = (int)(job - (int64_t)t * p);
+  const int32_t* cp = colptr + (int64_t)t * colptr_pitch(p);
+  const int64_t base = tile_base[t] + cp[pe];
+  const int len = cp[pe + 1] - cp[pe];
+  if (len <= 8) return;
+  for (int i = lane; i < len; i += 32) { s_e[w][i] = e_loc[base + i]; s_x[w][i] = x_csc[base + i]; }
+  __syncwarp();
+  if (lane == 0) {
+    int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, start[8], take[8];
+    for (int i = 0; i < len; ++i) ++cnt[(s_e[w][i] >> 4) & 7];
+    int acc = 0;
+    for (int q = 0; q < 8; ++q) { start[q] = acc; take[q] = acc; acc += cnt[q]; }
+    for (int i = 0; i < len; ++i) s_ord[w][take[(s_e[w][i] >> 4) & 7]++] = (uint16_t)i;
+    for (int q = 0; q < 8; ++q) take[q] = start[q];   // next unused of each bin
+    int left[8];
+    for (int q = 0; q < 8; ++q) left[q] = cnt[q];
+    int j = 0;
+    while (j < len) {
+      int used[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int sl = 0; sl < 8 && j < len; ++sl, ++j) {
+        int best = -1;
+        for (int q = 0; q < 8; ++q) {
+          if (!left[q]) continue;
+          if (best < 0 || used[q] < used[best] || (used[q] == used[best] && left[q] > left[best])) best = q;
+        }
+        const int src = s_ord[w][take[best]];
+        ++take[best];
+        --left[best];
+        ++used[best];
+        // element src moves to position j (the shared copies keep the old order)
+        e_loc[base + j] = s_e[w][src];
+        x_csc[base + j] = s_x[w][src];
+        // repoint the CSR slot of (patch, pe)
+        const int il = (int)(((s_e[w][src] >> 7) << 2) | ((((s_e[w][src] >> 4) & 7) ^ ((s_e[w][src] >> 7) & 7)) >> 1));
+        const int64_t g = (int64_t)t * kTile + il;
+        const int64_t r0 = rowptr[g], r1 = rowptr[g + 1];
+        for (int64_t r = r0; r < r1; ++r)
+          if (csr_p[r] == pe) { csr_pos[r] = (uint32_t)(base + j); break; }
+      }
+    }
+  }
+}
+
 // Column segments of each tile: sum over columns of ceil(len / kSegCountLen).
 __global__ void k_tile_segs(const int32_t* __restrict__ colptr, int ntiles, int p, int32_t* __restrict__ segs) {
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
@@ -300,6 +364,13 @@ int launch_build_index(PatchIndex& ix, const uint8_t* obs, const float* values, 
   k_tile_scan<<<1, 1024, 0, st>>>(ix.tile_tot, ix.ntiles, ix.tile_base);
   k_tile_fill<<<ix.ntiles, kFillThreads, 0, st>>>(obs, values, counts, ix.n, ix.p, ix.tile_base, ix.colptr, ix.e_loc,
                                            ix.x_csc, ix.rowptr, ix.csr_p, ix.csr_pos);
+  {
+    static int spread = -1;   // PB_INDEX_NO_SPREAD=1: keep ascending patch order inside columns (A/B)
+    if (spread < 0) { const char* e = getenv("PB_INDEX_NO_SPREAD"); spread = (e && atoi(e)) ? 0 : 1; }
+    if (spread)
+      k_csc_spread<<<(unsigned)ceil_div((int64_t)ix.ntiles * ix.p, kSpreadWarps), kSpreadWarps * 32, 0, st>>>(
+          ix.tile_base, ix.colptr, ix.ntiles, ix.p, ix.n, ix.rowptr, ix.csr_p, ix.e_loc, ix.x_csc, ix.csr_pos);
+  }
   k_tile_segs<<<(unsigned)ceil_div(ix.ntiles, 8), 256, 0, st>>>(ix.colptr, ix.ntiles, ix.p, ix.tile_segs);
   k_tile_scan<<<1, 1024, 0, st>>>(ix.tile_segs, ix.ntiles, ix.seg_base);
   PB_LAUNCH_CHECK();
