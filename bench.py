@@ -345,6 +345,7 @@ def run_gpu_arm(args):
         sweep = lambda st: gb.gibbs_epoch(st, pm, hp, rng="philox", check=False)  # noqa: E731
         n_units = pm.num_patches
     n, k, p = pm.num_patches, CFG["k"], pm.patch_size
+    split_code = pm.index().split_count > 0   # two code-step launches per sweep
     st = gb.init_state(pm, hp, CFG["seed"], "prior")
     clk = ClockSampler(local).__enter__()
     for _ in range(args.warmup):
@@ -498,9 +499,10 @@ def run_gpu_arm(args):
                    "l2": f"inputs larger than L2: values {n * p * 4 / 1e6:.0f} MB + Z/S state "
                          f"{n * k * 5 / 1e6:.0f} MB per rank"},
         "clocks": clk.summary(),
-        # per sweep: k_dict_gram, k_code_compact, k_finish_stats, k_draw_pi_gamma (residual carried);
-        # sharded: k_dict_gram per atom block + 1, k_dict_update per block
-        "gpu_launches": (4 if world == 1 else 2 * ((k + 7) // 8) + 4) * args.steps,
+        # per sweep: k_pack_dt, k_dict_gram, k_code_compact (+ the outlier launch on a side
+        # stream when the index splits the code step), k_finish_stats, k_draw_pi_gamma (residual
+        # carried); sharded: k_dict_gram per atom block + 1 and k_dict_update per block instead
+        "gpu_launches": ((5 if world == 1 else 2 * ((k + 7) // 8) + 5) + (1 if split_code else 0)) * args.steps,
         "e2e": e2e, "live": live, "quality": quality, "roofline": roofline,
     }
     if world == 1 and not args.no_configs:
