@@ -170,7 +170,8 @@ struct CodeConst {
   float geps, gs, inv_sqrt_gs;
   const float* logit;
   int* mcnt;
-  float* wrow;  // this patch's 8-atom window of w (pitch 9, lane g == 0 only)
+  float* wrow;  // this patch's 8-atom window of w (pitch 8, XOR-swizzled by wx; lane g == 0 only)
+  int wx;       // window swizzle: element q lives at wrow[q ^ wx] (conflict-free per-atom stores)
 };
 
 struct CodeThread {
@@ -253,7 +254,7 @@ __device__ __forceinline__ void code_one(const CompactArgs& a, const CodeConst& 
     a.weights[zo] = s_new;
     if (MODE == kRngReplay) t.sq_w += (double)s_new * (double)s_new;
     else t.sq_w8 = fmaf(s_new, s_new, t.sq_w8);
-    c.wrow[k & 7] = w_new;
+    c.wrow[(k & 7) ^ c.wx] = w_new;
   }
   const unsigned bal = __ballot_sync(0xffffffffu, z && own);
   if (c.lane == 0 && bal) atomicAdd(&c.mcnt[k], __popc(bal));
@@ -328,11 +329,12 @@ __device__ __forceinline__ void code_atoms(const CompactArgs& a, const CodeConst
     if (c.live && c.g == 0) {
       if (MODE != kRngReplay) { t.sq_w += (double)t.sq_w8; t.sq_w8 = 0.0f; }
       float* wrow = c.wrow;
-      for (int q = k1 - kg; q < 8; ++q) wrow[q] = 0.0f;  // partial last group
+      for (int q = k1 - kg; q < 8; ++q) wrow[q ^ c.wx] = 0.0f;  // partial last group
       float* blk = a.wt + ((c.i / kTile) * a.nblk8 + (kg >> 3)) * kTile * kWB;
       const int il = (int)(c.i % kTile);
-      *(float4*)(blk + wsw(il, 0)) = make_float4(wrow[0], wrow[1], wrow[2], wrow[3]);
-      *(float4*)(blk + wsw(il, 1)) = make_float4(wrow[4], wrow[5], wrow[6], wrow[7]);
+      const int x = c.wx;
+      *(float4*)(blk + wsw(il, 0)) = make_float4(wrow[0 ^ x], wrow[1 ^ x], wrow[2 ^ x], wrow[3 ^ x]);
+      *(float4*)(blk + wsw(il, 1)) = make_float4(wrow[4 ^ x], wrow[5 ^ x], wrow[6 ^ x], wrow[7 ^ x]);
     }
   }
 }
@@ -378,14 +380,16 @@ __device__ __forceinline__ void code_patch_range(const CompactArgs& a, const Cod
   }
 }
 
-template <int CMAX, int G, int MODE>
+// WS: pitch-8 XOR-swizzled w windows (1 KB less shared memory per CTA than the
+// pitch-9 rows: lets the whole D of configs[1] fit two CTAs per SM)
+template <int CMAX, int G, int MODE, bool WS>
 __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
   extern __shared__ __align__(16) float sm[];
   const int kp = a.kc + 2;                     // DT row pitch (kc % 8 == 0  =>  kp/2 odd)
   float* dt = sm;                              // (P+1) * kp
   float* logit = dt + (G == 1 ? a.dt_img_floats : (int64_t)(a.p + 1) * kp);  // K (after the DT chunk)
   int* mcnt = (int*)(logit + a.k);             // K
-  float* wwin = (float*)(mcnt + a.k);          // (blockDim / G) * 9
+  float* wwin = (float*)(mcnt + a.k);          // (blockDim / G) * (WS ? 8 : 9)
   __shared__ double red[32];
   __shared__ long long next_blk;
   CodeConst c;
@@ -397,7 +401,8 @@ __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
   c.inv_sqrt_gs = (float)(1.0 / sqrt(a.sc->gamma_s));
   c.logit = logit;
   c.mcnt = mcnt;
-  c.wrow = wwin + (threadIdx.x / G) * 9;
+  c.wrow = wwin + (threadIdx.x / G) * (WS ? 8 : 9);
+  c.wx = WS ? ((threadIdx.x / G) >> 2) & 7 : 0;   // constant 0 folds the XORs away
   for (int k = threadIdx.x; k < a.k; k += blockDim.x) {
     const double pk = fmin(fmax(a.pi[k], 1e-15), 1.0 - 1e-15);  // bpfa.py:173
     logit[k] = (float)(log(pk) - log1p(-pk));
@@ -1255,10 +1260,14 @@ __global__ void k_pack_dt(const float* __restrict__ atoms, int p, int k, int kc,
 }
 
 void code_dt_layout(int p, int k, int* kc_out, int64_t* img_floats_out, int* nchunks_out) {
-  // DT chunk: kc atoms (a multiple of 8) x (P+1) rows of pitch kc+2 within ~100 KB
-  // (two CTAs per SM); the whole dictionary when it fits
+  // DT chunk: kc atoms (a multiple of 8) x (P+1) rows of pitch kc+2, as many as
+  // two 256-thread CTAs per SM can hold next to the logits, usage counts and
+  // w windows (228 KB per SM, 1 KB reserved per CTA, static shared memory);
+  // the whole dictionary when it fits (configs[1]: P = 100, K = 256 just fits)
   const int k8 = (int)ceil_div(k, 8) * 8;
-  int kc = (int)(((100 * 1024) / ((size_t)(p + 1) * 4) - 2) & ~(size_t)7);
+  const size_t per_cta = 228 * 1024 / 2 - 1024 - 512;
+  const size_t fixed = (size_t)k * 8 + (size_t)256 * 8 * 4;
+  int kc = per_cta > fixed ? (int)(((per_cta - fixed) / ((size_t)(p + 1) * 4) - 2) & ~(size_t)7) : 8;
   if (kc < 8) kc = 8;
   if (kc > k8) kc = k8;
   if (kc_out) *kc_out = kc;
@@ -1387,8 +1396,11 @@ int launch_code_compact(const CompactArgs& a_in, int mode, int& nblocks, cudaStr
   const int th = 256;
   // DT chunks as pre-packed by launch_pack_dt (the caller packs a.dt_img first)
   if (!a.dt_img) { set_error("code step without the packed dictionary image"); return PB_EVALUE; }
-  const size_t fixed = (size_t)a.k * 8 + (size_t)(th / g) * 9 * 4;
   code_dt_layout(a.p, a.k, &a.kc, &a.dt_img_floats, nullptr);
+  // pitch-9 windows unless only the pitch-8 swizzled ones let two CTAs share an SM
+  const size_t per_cta = 228 * 1024 / 2 - 1024 - 512;
+  const bool ws = g == 1 && (size_t)a.dt_img_floats * 4 + (size_t)a.k * 8 + (size_t)(th / g) * 9 * 4 > per_cta;
+  const size_t fixed = (size_t)a.k * 8 + (size_t)(th / g) * (ws ? 8 : 9) * 4;
   const size_t smem = (size_t)a.dt_img_floats * 4 + fixed;
   if (smem > 220 * 1024) { set_error("too many atoms for the code step (K=%d)", a.k); return PB_EUNSUPPORTED; }
   const int64_t nb = ceil_div((a.plist ? a.plist_n : a.n) * g, th);
@@ -1398,7 +1410,10 @@ int launch_code_compact(const CompactArgs& a_in, int mode, int& nblocks, cudaStr
   PB_CUDA_TRY(cudaMemsetAsync(a.blk_ctr, 0, sizeof(unsigned), st));
 #define PB_C(C, GG)                                                                                  \
   case C * 100 + GG: {                                                                               \
-    auto kern = mode == kRngReplay ? k_code_compact<C, GG, kRngReplay> : k_code_compact<C, GG, kRngPhilox>; \
+    auto kern = ws ? (mode == kRngReplay ? k_code_compact<C, GG, kRngReplay, GG == 1>                           \
+                                         : k_code_compact<C, GG, kRngPhilox, GG == 1>)                          \
+                   : (mode == kRngReplay ? k_code_compact<C, GG, kRngReplay, false>                              \
+                                         : k_code_compact<C, GG, kRngPhilox, false>);                            \
     PB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     int per_sm = 0;                                                                                  \
     PB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, th, smem));             \
