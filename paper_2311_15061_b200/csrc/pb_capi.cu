@@ -235,7 +235,7 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
     c1.cmax = d->index->split_count;
     c1.split = d->index->split_count;
     c1.zero_mcount = c2.zero_mcount = 0;
-    const int nb1_expect = code_launch_blocks(c1.cmax, d->n);
+    const int nb1_expect = code_launch_blocks(c1.cmax, d->n, d->p, d->k);
     c2.plist = ix.outliers;
     c2.plist_n = d->index->n_outliers;
     c2.block_sums = ws.block_sums + 2 * (size_t)nb1_expect;

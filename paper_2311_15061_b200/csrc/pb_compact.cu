@@ -382,7 +382,9 @@ __device__ __forceinline__ void code_patch_range(const CompactArgs& a, const Cod
 
 // WS: pitch-8 XOR-swizzled w windows (1 KB less shared memory per CTA than the
 // pitch-9 rows: lets the whole D of configs[1] fit two CTAs per SM)
-template <int CMAX, int G, int MODE, bool WS>
+// WC: every warp claims its own blocks of 32 patches (whole D staged once: no
+// CTA barrier in the loop, warps of different slot counts never wait for each other)
+template <int CMAX, int G, int MODE, bool WS, bool WC>
 __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
   extern __shared__ __align__(16) float sm[];
   const int kp = a.kc + 2;                     // DT row pitch (kc % 8 == 0  =>  kp/2 odd)
@@ -416,20 +418,27 @@ __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
   const int row_bytes = kp * 4;
   CodeThread t;
   t.sq_w8 = 0.0f;
-  const int per_blk = blockDim.x / G;
+  const int per_blk = WC ? 32 / G : blockDim.x / G;
   const int64_t nblk = ceil_div(a.plist ? a.plist_n : a.n, per_blk);
   // blocks of patches are claimed dynamically (the launch may share the GPU with
   // a concurrent one); each block writes its own S^2 / R^2 sums, summed later in
   // block order, so the result does not depend on which CTA took which block
   for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) next_blk = (long long)atomicAdd(a.blk_ctr, 1u);
-    __syncthreads();
-    const int64_t b = next_blk;
+    int64_t b;
+    if constexpr (WC) {
+      unsigned v = 0;
+      if (c.lane == 0) v = atomicAdd(a.blk_ctr, 1u);
+      b = __shfl_sync(0xffffffffu, v, 0);
+    } else {
+      __syncthreads();
+      if (threadIdx.x == 0) next_blk = (long long)atomicAdd(a.blk_ctr, 1u);
+      __syncthreads();
+      b = next_blk;
+    }
     if (b >= nblk) break;
     t.sq_w = 0.0;
     double sq_r = 0.0;
-    const int64_t slot = b * per_blk + threadIdx.x / G;
+    const int64_t slot = b * per_blk + (WC ? c.lane : (int)threadIdx.x) / G;
     if (a.plist) {  // second launch of a split: exactly the listed (wide) patches
       c.live = slot < a.plist_n;
       c.i = c.live ? a.plist[slot] : 0;
@@ -473,12 +482,20 @@ __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
       const int s = j * G + c.g;
       if (c.live && j < wmax && s < cnt) a.r_csc[a.csr_pos[r0 + s]] = r[j];
     }
-    const double bw = block_sum_d(t.sq_w, red);
-    __syncthreads();
-    const double br = block_sum_d(sq_r, red);
-    if (threadIdx.x == 0) {
-      a.block_sums[2 * b] = bw;
-      a.block_sums[2 * b + 1] = br;
+    if constexpr (WC) {
+      const double bw = warp_sum_d(t.sq_w), br = warp_sum_d(sq_r);
+      if (c.lane == 0) {
+        a.block_sums[2 * b] = bw;
+        a.block_sums[2 * b + 1] = br;
+      }
+    } else {
+      const double bw = block_sum_d(t.sq_w, red);
+      __syncthreads();
+      const double br = block_sum_d(sq_r, red);
+      if (threadIdx.x == 0) {
+        a.block_sums[2 * b] = bw;
+        a.block_sums[2 * b + 1] = br;
+      }
     }
   }
   __syncthreads();
@@ -1320,10 +1337,25 @@ static double code_cost(int c, int g) {
   return 1.11 * sqrt((double)g);
 }
 
-int code_launch_blocks(int cmax, int64_t n) {
+// Window layout and block claiming of a code-step launch (256 threads per CTA):
+// pitch-8 swizzled w windows when only they let two CTAs share an SM; warps
+// claim their own 32-patch blocks when D is staged whole with pitch-9 windows
+// (configs[0]/[2]/[4]: -4 %; with the pitch-8 windows of configs[1] +1.5 %).
+static void code_window_claim(int64_t n, int p, int k, int g, bool& ws, bool& wc) {
+  int kc;
+  int64_t imgf;
+  code_dt_layout(p, k, &kc, &imgf, nullptr);
+  const size_t per_cta = 228 * 1024 / 2 - 1024 - 512;
+  ws = g == 1 && (size_t)imgf * 4 + (size_t)k * 8 + (size_t)(256 / g) * 9 * 4 > per_cta;
+  wc = g == 1 && kc >= k && !ws && n >= (1 << 20);   // small problems: CTA claiming (configs[0] +30 % otherwise)
+}
+
+int code_launch_blocks(int cmax, int64_t n, int p, int k) {
   int c, g;
   if (!pick_compact(cmax, c, g)) return 0;
-  return (int)ceil_div(n * g, 256);
+  bool ws, wc;
+  code_window_claim(n * g, p, k, g, ws, wc);
+  return (int)ceil_div(n * g, wc ? 32 : 256);
 }
 
 int code_split_choose(const int32_t* hist, int p, int cmax) {
@@ -1397,23 +1429,24 @@ int launch_code_compact(const CompactArgs& a_in, int mode, int& nblocks, cudaStr
   // DT chunks as pre-packed by launch_pack_dt (the caller packs a.dt_img first)
   if (!a.dt_img) { set_error("code step without the packed dictionary image"); return PB_EVALUE; }
   code_dt_layout(a.p, a.k, &a.kc, &a.dt_img_floats, nullptr);
-  // pitch-9 windows unless only the pitch-8 swizzled ones let two CTAs share an SM
-  const size_t per_cta = 228 * 1024 / 2 - 1024 - 512;
-  const bool ws = g == 1 && (size_t)a.dt_img_floats * 4 + (size_t)a.k * 8 + (size_t)(th / g) * 9 * 4 > per_cta;
+  bool ws, wc;
+  code_window_claim((a.plist ? a.plist_n : a.n) * g, a.p, a.k, g, ws, wc);
   const size_t fixed = (size_t)a.k * 8 + (size_t)(th / g) * (ws ? 8 : 9) * 4;
   const size_t smem = (size_t)a.dt_img_floats * 4 + fixed;
   if (smem > 220 * 1024) { set_error("too many atoms for the code step (K=%d)", a.k); return PB_EUNSUPPORTED; }
   const int64_t nb = ceil_div((a.plist ? a.plist_n : a.n) * g, th);
   if (a.zero_mcount) PB_CUDA_TRY(cudaMemsetAsync(a.m_count, 0, (size_t)a.k * sizeof(int32_t), st));
-  nblocks = (int)nb;   // one S^2 / R^2 pair per block of patches
+  nblocks = (int)(wc ? ceil_div((a.plist ? a.plist_n : a.n) * g, 32) : nb);   // one S^2 / R^2 pair per claimed block
   if (nb == 0) return PB_OK;
   PB_CUDA_TRY(cudaMemsetAsync(a.blk_ctr, 0, sizeof(unsigned), st));
 #define PB_C(C, GG)                                                                                  \
   case C * 100 + GG: {                                                                               \
-    auto kern = ws ? (mode == kRngReplay ? k_code_compact<C, GG, kRngReplay, GG == 1>                           \
-                                         : k_code_compact<C, GG, kRngPhilox, GG == 1>)                          \
-                   : (mode == kRngReplay ? k_code_compact<C, GG, kRngReplay, false>                              \
-                                         : k_code_compact<C, GG, kRngPhilox, false>);                            \
+    auto kern = ws ? (mode == kRngReplay ? k_code_compact<C, GG, kRngReplay, GG == 1, false>                    \
+                                         : k_code_compact<C, GG, kRngPhilox, GG == 1, false>)                  \
+           : wc ? (mode == kRngReplay ? k_code_compact<C, GG, kRngReplay, false, GG == 1>                      \
+                                      : k_code_compact<C, GG, kRngPhilox, false, GG == 1>)                     \
+                : (mode == kRngReplay ? k_code_compact<C, GG, kRngReplay, false, false>                        \
+                                      : k_code_compact<C, GG, kRngPhilox, false, false>);                      \
     PB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     int per_sm = 0;                                                                                  \
     PB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, th, smem));             \

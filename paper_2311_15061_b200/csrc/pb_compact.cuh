@@ -92,7 +92,7 @@ int launch_resid_compact(const CompactArgs& a, cudaStream_t st);
 int launch_code_compact(const CompactArgs& a, int mode, int& nblocks, cudaStream_t st);
 // the code step's per-patch limit for the main launch from the count histogram (0 = no split)
 int code_split_choose(const int32_t* hist, int p, int cmax);
-int code_launch_blocks(int cmax, int64_t n);  // blocks of patches (= S^2/R^2 pairs) of a launch
+int code_launch_blocks(int cmax, int64_t n, int p, int k);  // blocks of patches (= S^2/R^2 pairs) of a launch
 constexpr double kDictSegCost = 40.0;  // element equivalents of one element-phase segment (work split; live -5 %)
 int launch_dict_gram(const DictGramArgs& a, cudaStream_t st);
 // dictionary step on all-zero codes: prior redraw of every atom (bit-identical to launch_dict_gram on W == 0)

@@ -349,8 +349,58 @@ int launch_accumulate_atoms(bool resid, const float* values, const uint8_t* obs,
   return PB_OK;
 }
 
+// Two-level variant for many block sums (warp-claimed code steps of large
+// problems): CTA c sums the contiguous range c of the block sums (fixed tree),
+// the last CTA to finish sums the CTA partials in index order — deterministic.
+// Partials and the ticket live right after the block sums.
+__global__ void k_finish_stats_2l(double* __restrict__ block_sums, int nblocks, int per_cta, SweepScalars* sc) {
+  __shared__ double red[32];
+  __shared__ bool last;
+  double* part = block_sums + 2 * (size_t)nblocks;
+  unsigned* ticket = (unsigned*)(part + 2 * (size_t)gridDim.x);
+  const int b0 = blockIdx.x * per_cta, b1 = min(nblocks, b0 + per_cta);
+  double w = 0.0, r = 0.0;
+  for (int b = b0 + threadIdx.x; b < b1; b += blockDim.x) {
+    w += block_sums[2 * b];
+    r += block_sums[2 * b + 1];
+  }
+  const double tw = block_sum_d(w, red);
+  __syncthreads();
+  const double tr = block_sum_d(r, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = tw;
+    part[2 * blockIdx.x + 1] = tr;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double pw = 0.0, pr = 0.0;
+  for (int c = threadIdx.x; c < (int)gridDim.x; c += blockDim.x) {
+    pw += __ldcg(part + 2 * c);
+    pr += __ldcg(part + 2 * c + 1);
+  }
+  const double sw = block_sum_d(pw, red);
+  __syncthreads();
+  const double sr = block_sum_d(pr, red);
+  if (threadIdx.x == 0) {
+    sc->sq_w = sw;
+    sc->sq_r = sr;
+    *ticket = 0u;
+  }
+}
+
 int launch_finish_stats(const double* block_sums, int nblocks, SweepScalars* sc, cudaStream_t st) {
-  k_finish_stats<<<1, 1024, 0, st>>>(block_sums, nblocks, sc);
+  constexpr int kPer = 4096;
+  if (nblocks <= 2 * kPer) {
+    k_finish_stats<<<1, 1024, 0, st>>>(block_sums, nblocks, sc);
+  } else {
+    const int ctas = (int)ceil_div(nblocks, kPer);
+    unsigned* ticket = (unsigned*)(const_cast<double*>(block_sums) + 2 * (size_t)nblocks + 2 * (size_t)ctas);
+    PB_CUDA_TRY(cudaMemsetAsync(ticket, 0, sizeof(unsigned), st));
+    k_finish_stats_2l<<<ctas, 1024, 0, st>>>(const_cast<double*>(block_sums), nblocks, kPer, sc);
+  }
   PB_LAUNCH_CHECK();
   return PB_OK;
 }
