@@ -452,6 +452,13 @@ int pb_dict_profile(int32_t enable, double* slots_ns_out) {
         for (int i = 0; i < kProfSlots; ++i) slots_ns_out[i] += (double)h[b * kProfSlots + i];
       }
       for (int i = 0; i < kProfSlots; ++i) slots_ns_out[i] /= nb ? nb : 1;
+      if (getenv("PB_DICT_PROF_CTAS")) {  // per-CTA element-phase and barrier-1 times (profiling aid)
+        for (int b = 0; b < kMaxDictBlocks; ++b) {
+          if (!h[b * kProfSlots + 2]) continue;
+          fprintf(stderr, "cta %d elems %.4f tile_end %.4f sync1 %.4f\n", b, h[b * kProfSlots + 2] / 1e6,
+                  h[b * kProfSlots + 3] / 1e6, h[b * kProfSlots + 6] / 1e6);
+        }
+      }
       if (getenv("PB_DICT_PROF_DUMP")) {  // per-CTA spread of each slot (profiling aid)
         for (int i = 0; i < kProfSlots; ++i) {
           std::vector<double> v;
