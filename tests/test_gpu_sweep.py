@@ -298,3 +298,25 @@ def test_zero_codes_dictionary_step_is_prior_redraw(cuda_device, rng):
             assert np.array_equal(ha[key], hb[key]), key
         assert ha["weight_precision"] == hb["weight_precision"]
         assert ha["noise_precision"] == hb["noise_precision"]
+
+
+def test_epoch_statistics_large_problem(cuda_device):
+    """A problem past 2^20 patches runs the warp-claimed code step (one S^2/R^2
+    pair per 32-patch block, > 8192 blocks) and the two-level finish: the epoch's
+    sum S^2 (all codes, bpfa.py:321) and sum R^2 (observed residual, bpfa.py:325)
+    equal host recomputations from the state within f32 accumulation noise."""
+    from paper_2311_15061_b200 import inputs
+
+    img = inputs.synthetic_texture((1032, 1032), seed=6)
+    mask = inputs.make_mask(img.shape, 0.1, "uniform-random", 6)
+    hp = gb.Hyperparams(num_atoms=16)
+    pm = pp.extract_patches(img, mask, pp.PatchSpec((8, 8)), True)
+    assert pm.num_patches >= 1 << 20
+    st = gb.init_state(pm, hp, 3, "prior")
+    for _ in range(2):
+        gb.gibbs_epoch(st, pm, hp, rng="philox", check=False)
+    s = st._sc()
+    w = st.weights_kn[:, :pm.num_patches].double()
+    assert abs(s.sq_w - float((w * w).sum())) <= 1e-6 * s.sq_w
+    r = gb._residual(pm, st).double()
+    assert abs(s.sq_r - float((r * r).sum())) <= 1e-3 * s.sq_r
