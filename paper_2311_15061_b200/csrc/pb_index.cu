@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kFillThreads) k_tile_fill(
     if (o0) {
       const int64_t pos = col + rank;
       e_loc[pos] = (uint16_t)w_row_off(l0);
-      x_csc[pos] = values[(int64_t)pe * n + g0];
+      ((uint32_t*)x_csc)[pos] = (uint32_t)(row0 + j0);   // CSR slot (k_csc_spread); values: k_scatter_x
       csr_p[row0 + j0] = (uint16_t)pe;
       csr_pos[row0 + j0] = (uint32_t)pos;
       ++j0;
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kFillThreads) k_tile_fill(
     if (o1) {
       const int64_t pos = col + rank + o0;
       e_loc[pos] = (uint16_t)w_row_off(l0 + 1);
-      x_csc[pos] = values[(int64_t)pe * n + g1];
+      ((uint32_t*)x_csc)[pos] = (uint32_t)(row1 + j1);
       csr_p[row1 + j1] = (uint16_t)pe;
       csr_pos[row1 + j1] = (uint32_t)pos;
       ++j1;
@@ -221,24 +221,24 @@ void carve_index(PatchIndex& ix, char* base, int64_t n, int p, int64_t nnz_upper
   ix.seg_base = (int64_t*)take((size_t)(ntiles + 1) * 8);
 }
 
-// Bank spreading of the CSC order (after k_tile_fill).  The dictionary step's
-// lanes gather each element's W row from shared memory with 16-byte loads whose
-// quarter-warps are 8 CONSECUTIVE elements of a column run; rows land on one of
-// 8 bank quads ((e_loc >> 4) & 7), so a random order costs ~2.2x the ideal
-// wavefronts.  One warp per (tile, column) reorders the run into groups of 8
-// with as few repeated quads as possible (each slot takes the bin with the most
-// elements left among the least used in the group), rewrites e_loc / x_csc and
-// repoints csr_pos.  Deterministic; the sums only see a different fixed order.
-constexpr int kSpreadWarps = 4;   // 32 KB of static shared memory per block
+// Bank spreading of the CSC order (after k_tile_fill, before k_scatter_x).
+// The dictionary step's lanes gather each element's W row from shared memory
+// with 16-byte loads whose quarter-warps are 8 CONSECUTIVE elements of a column
+// run; rows land on one of 8 bank quads ((e_loc >> 4) & 7), so a random order
+// costs ~2.2x the ideal wavefronts.  One warp per (tile, column) sorts the run
+// by quad (stable ranks by warp ballots) and reads it column-major out of 8 rows:
+// consecutive groups of 8 take elements ceil(len/8) apart in the sorted run,
+// i.e. distinct quads unless one quad holds more than that many.  (A greedy
+// group planner is ~1 % better for the sweep but triples the index build.)  The fill left each element's
+// CSR slot in x_csc, so csr_pos is repointed without searching; the values are
+// scattered afterwards.  Deterministic.
+constexpr int kSpreadWarps = 8;
 __global__ void __launch_bounds__(kSpreadWarps * 32) k_csc_spread(const int64_t* __restrict__ tile_base,
                                                                   const int32_t* __restrict__ colptr, int ntiles, int p,
-                                                                  int64_t n, const int64_t* __restrict__ rowptr,
-                                                                  const uint16_t* __restrict__ csr_p,
-                                                                  uint16_t* __restrict__ e_loc, float* __restrict__ x_csc,
+                                                                  uint16_t* __restrict__ e_loc,
+                                                                  const uint32_t* __restrict__ slot_of,
                                                                   uint32_t* __restrict__ csr_pos) {
   __shared__ uint16_t s_e[kSpreadWarps][kTile];
-  __shared__ float s_x[kSpreadWarps][kTile];
-  __shared__ uint16_t s_ord[kSpreadWarps][kTile];   // by bin, ascending inside a bin
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t job = (int64_t)blockIdx.x * kSpreadWarps + w;
   if (job >= (int64_t)ntiles * p) return;
@@ -247,40 +247,47 @@ __global__ void __launch_bounds__(kSpreadWarps * 32) k_csc_spread(const int64_t*
   const int64_t base = tile_base[t] + cp[pe];
   const int len = cp[pe + 1] - cp[pe];
   if (len <= 8) return;
-  for (int i = lane; i < len; i += 32) { s_e[w][i] = e_loc[base + i]; s_x[w][i] = x_csc[base + i]; }
+  int cnt[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) cnt[q] = 0;
+  for (int i0 = 0; i0 < len; i0 += 32) {   // warp-uniform trip count: full-mask ballots
+    const int i = i0 + lane;
+    const bool live = i < len;
+    const uint16_t e = live ? e_loc[base + i] : 0;
+    if (live) s_e[w][i] = e;
+    const int q = (e >> 4) & 7;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) cnt[b] += __popc(__ballot_sync(0xffffffffu, live && q == b));
+  }
   __syncwarp();
-  if (lane == 0) {
-    int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, start[8], take[8];
-    for (int i = 0; i < len; ++i) ++cnt[(s_e[w][i] >> 4) & 7];
-    int acc = 0;
-    for (int q = 0; q < 8; ++q) { start[q] = acc; take[q] = acc; acc += cnt[q]; }
-    for (int i = 0; i < len; ++i) s_ord[w][take[(s_e[w][i] >> 4) & 7]++] = (uint16_t)i;
-    for (int q = 0; q < 8; ++q) take[q] = start[q];   // next unused of each bin
-    int left[8];
-    for (int q = 0; q < 8; ++q) left[q] = cnt[q];
-    int j = 0;
-    while (j < len) {
-      int used[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int sl = 0; sl < 8 && j < len; ++sl, ++j) {
-        int best = -1;
-        for (int q = 0; q < 8; ++q) {
-          if (!left[q]) continue;
-          if (best < 0 || used[q] < used[best] || (used[q] == used[best] && left[q] > left[best])) best = q;
-        }
-        const int src = s_ord[w][take[best]];
-        ++take[best];
-        --left[best];
-        ++used[best];
-        // element src moves to position j (the shared copies keep the old order)
-        e_loc[base + j] = s_e[w][src];
-        x_csc[base + j] = s_x[w][src];
-        // repoint the CSR slot of (patch, pe)
-        const int il = (int)(((s_e[w][src] >> 7) << 2) | ((((s_e[w][src] >> 4) & 7) ^ ((s_e[w][src] >> 7) & 7)) >> 1));
-        const int64_t g = (int64_t)t * kTile + il;
-        const int64_t r0 = rowptr[g], r1 = rowptr[g + 1];
-        for (int64_t r = r0; r < r1; ++r)
-          if (csr_p[r] == pe) { csr_pos[r] = (uint32_t)(base + j); break; }
-      }
+  int seen[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) seen[q] = 0;
+  for (int i0 = 0; i0 < len; i0 += 32) {
+    const int i = i0 + lane;
+    const bool live = i < len;
+    const uint16_t e = live ? s_e[w][i] : 0;
+    const int q = (e >> 4) & 7;
+    int r = 0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const unsigned m = __ballot_sync(0xffffffffu, live && q == b);
+      if (q == b) r = seen[b] + __popc(m & ((1u << lane) - 1u));   // stable rank inside the quad
+      seen[b] += __popc(m);
+    }
+    if (live) {
+      int st = 0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) st += b < q ? cnt[b] : 0;
+      // the quad-sorted run read column-major out of 8 rows of c = ceil(len/8):
+      // group g takes sorted elements g, g + c, ..., g + 7c (distinct quads
+      // unless a quad holds more than c elements)
+      const int sidx = st + r;
+      const int c = (len + 7) >> 3, nf = len / c, rem = len - nf * c;
+      const int row = sidx / c, col = sidx - row * c;
+      const int j = col * nf + min(col, rem) + row;
+      e_loc[base + j] = e;
+      csr_pos[slot_of[base + i]] = (uint32_t)(base + j);
     }
   }
 }
@@ -369,8 +376,11 @@ int launch_build_index(PatchIndex& ix, const uint8_t* obs, const float* values, 
     if (spread < 0) { const char* e = getenv("PB_INDEX_NO_SPREAD"); spread = (e && atoi(e)) ? 0 : 1; }
     if (spread)
       k_csc_spread<<<(unsigned)ceil_div((int64_t)ix.ntiles * ix.p, kSpreadWarps), kSpreadWarps * 32, 0, st>>>(
-          ix.tile_base, ix.colptr, ix.ntiles, ix.p, ix.n, ix.rowptr, ix.csr_p, ix.e_loc, ix.x_csc, ix.csr_pos);
+          ix.tile_base, ix.colptr, ix.ntiles, ix.p, ix.e_loc, (const uint32_t*)ix.x_csc, ix.csr_pos);
   }
+  // the observed values into the (final) CSC order
+  k_scatter_x<<<(unsigned)ceil_div(ix.n, 256), 256, 0, st>>>(values, counts, ix.rowptr, ix.csr_p, ix.csr_pos, ix.n,
+                                                             ix.x_csc);
   k_tile_segs<<<(unsigned)ceil_div(ix.ntiles, 8), 256, 0, st>>>(ix.colptr, ix.ntiles, ix.p, ix.tile_segs);
   k_tile_scan<<<1, 1024, 0, st>>>(ix.tile_segs, ix.ntiles, ix.seg_base);
   PB_LAUNCH_CHECK();
