@@ -225,11 +225,11 @@ void carve_index(PatchIndex& ix, char* base, int64_t n, int p, int64_t nnz_upper
 // The dictionary step's lanes gather each element's W row from shared memory
 // with 16-byte loads whose quarter-warps are 8 CONSECUTIVE elements of a column
 // run; rows land on one of 8 bank quads ((e_loc >> 4) & 7), so a random order
-// costs ~2.2x the ideal wavefronts.  One warp per (tile, column) sorts the run
-// by quad (stable ranks by warp ballots) and reads it column-major out of 8 rows:
-// consecutive groups of 8 take elements ceil(len/8) apart in the sorted run,
-// i.e. distinct quads unless one quad holds more than that many.  (A greedy
-// group planner is ~1 % better for the sweep but triples the index build.)  The fill left each element's
+// costs ~2.2x the ideal wavefronts.  One warp per (tile, column) ranks the
+// elements inside their quad (warp ballots) and orders the run by relative
+// position inside the quad (a proportional interleave: each group of 8 repeats
+// a quad only as often as the quad counts force); runs longer than 256 read the
+// quad-sorted run column-major out of 8 rows instead (linear cost).  The fill left each element's
 // CSR slot in x_csc, so csr_pos is repointed without searching; the values are
 // scattered afterwards.  Deterministic.
 constexpr int kSpreadWarps = 8;
@@ -239,6 +239,8 @@ __global__ void __launch_bounds__(kSpreadWarps * 32) k_csc_spread(const int64_t*
                                                                   const uint32_t* __restrict__ slot_of,
                                                                   uint32_t* __restrict__ csr_pos) {
   __shared__ uint16_t s_e[kSpreadWarps][kTile];
+  __shared__ uint16_t s_rq[kSpreadWarps][kTile];   // rank inside the quad << 3 | quad
+  __shared__ int s_cnt[kSpreadWarps][8];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t job = (int64_t)blockIdx.x * kSpreadWarps + w;
   if (job >= (int64_t)ntiles * p) return;
@@ -275,17 +277,39 @@ __global__ void __launch_bounds__(kSpreadWarps * 32) k_csc_spread(const int64_t*
       if (q == b) r = seen[b] + __popc(m & ((1u << lane) - 1u));   // stable rank inside the quad
       seen[b] += __popc(m);
     }
-    if (live) {
-      int st = 0;
+    if (live) s_rq[w][i] = (uint16_t)((r << 3) | q);
+  }
+  __syncwarp();
+  if (lane < 8) {
 #pragma unroll
-      for (int b = 0; b < 8; ++b) st += b < q ? cnt[b] : 0;
-      // the quad-sorted run read column-major out of 8 rows of c = ceil(len/8):
-      // group g takes sorted elements g, g + c, ..., g + 7c (distinct quads
-      // unless a quad holds more than c elements)
-      const int sidx = st + r;
+    for (int b = 0; b < 8; ++b)
+      if (lane == b) s_cnt[w][b] = cnt[b];
+  }
+  __syncwarp();
+  // proportional interleave: element (q, r) sits at the relative position
+  // (r + 1/2) / cnt_q of its quad; the new order sorts those keys (ties by
+  // quad), so every quad is spread evenly and each group of 8 repeats a quad
+  // only as often as the counts force
+  for (int i = lane; i < len; i += 32) {
+    const int rq = s_rq[w][i], q = rq & 7, r2 = 2 * (rq >> 3) + 1;
+    const int cq = s_cnt[w][q];
+    int j = 0;
+    if (len <= 256) {   // O(len^2) ranking: short runs
+      for (int k = 0; k < len; ++k) {
+        const int rk = s_rq[w][k], qk = rk & 7, rk2 = 2 * (rk >> 3) + 1;
+        const int lhs = rk2 * cq, rhs = r2 * s_cnt[w][qk];   // key_k < key_i  <=>  rk2 / cnt_qk < r2 / cq
+        j += (lhs < rhs || (lhs == rhs && qk < q)) ? 1 : 0;
+      }
+    } else {            // long runs: the quad-sorted run read column-major out of 8 rows
+      int st = 0;
+      for (int b = 0; b < q; ++b) st += s_cnt[w][b];
+      const int sidx = st + (rq >> 3);
       const int c = (len + 7) >> 3, nf = len / c, rem = len - nf * c;
       const int row = sidx / c, col = sidx - row * c;
-      const int j = col * nf + min(col, rem) + row;
+      j = col * nf + min(col, rem) + row;
+    }
+    {
+      const uint16_t e = s_e[w][i];
       e_loc[base + j] = e;
       csr_pos[slot_of[base + i]] = (uint32_t)(base + j);
     }
