@@ -228,7 +228,7 @@ void carve_index(PatchIndex& ix, char* base, int64_t n, int p, int64_t nnz_upper
 // costs ~2.2x the ideal wavefronts.  One warp per (tile, column) ranks the
 // elements inside their quad (warp ballots) and orders the run by relative
 // position inside the quad (a proportional interleave: each group of 8 repeats
-// a quad only as often as the quad counts force); runs longer than 256 read the
+// a quad only as often as the quad counts force); runs longer than 128 read the
 // quad-sorted run column-major out of 8 rows instead (linear cost).  The fill left each element's
 // CSR slot in x_csc, so csr_pos is repointed without searching; the values are
 // scattered afterwards.  Deterministic.
@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(kSpreadWarps * 32) k_csc_spread(const int64_t*
     const int rq = s_rq[w][i], q = rq & 7, r2 = 2 * (rq >> 3) + 1;
     const int cq = s_cnt[w][q];
     int j = 0;
-    if (len <= 256) {   // O(len^2) ranking: short runs
+    if (len <= 128) {   // O(len^2) ranking: short runs
       for (int k = 0; k < len; ++k) {
         const int rk = s_rq[w][k], qk = rk & 7, rk2 = 2 * (rk >> 3) + 1;
         const int lhs = rk2 * cq, rhs = r2 * s_cnt[w][qk];   // key_k < key_i  <=>  rk2 / cnt_qk < r2 / cq
