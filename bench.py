@@ -413,6 +413,12 @@ def run_gpu_arm(args):
                 "fp32": {"achieved_tflops": alg_flops / dur_s / 1e12, "peak_tflops_derived": 74.45,
                          "frac": alg_flops / dur_s / 1e12 / 74.45},
                 "phase_ms_per_epoch": dict(zip(names, per))}
+    # the whole sweep against its roofline floor (12*|Omega| flops at the
+    # FP32 peak, 15 B per update at the HBM peak), as in the per-config table
+    floor_ms = 1e3 * max(12.0 * pm.n_obs * k / (FP32_PEAK_TF * 1e12), 15.0 * n * k / (peaks["hbm_gbs"] * 1e9))
+    roofline["sweep"] = {"floor_ms": floor_ms, "ms": ms / args.steps, "frac": floor_ms / (ms / args.steps),
+                         "bound": "hbm" if 15.0 * n * k / (peaks["hbm_gbs"] * 1e9) > 12.0 * pm.n_obs * k /
+                         (FP32_PEAK_TF * 1e12) else "fp32"}
 
     # --- quality of the device result after the timed sweeps ----------------
     est = gb.compose_estimates(st)
