@@ -177,6 +177,7 @@ struct CodeConst {
 struct CodeThread {
   double sq_w;
   float sq_w8;  // philox mode: sum S^2 over the current 8-atom group
+  int mc;       // lane j < 8: the warp's z count of atom kg + j in the current 8-atom group
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -256,8 +257,10 @@ __device__ __forceinline__ void code_one(const CompactArgs& a, const CodeConst& 
     else t.sq_w8 = fmaf(s_new, s_new, t.sq_w8);
     c.wrow[(k & 7) ^ c.wx] = w_new;
   }
-  const unsigned bal = __ballot_sync(0xffffffffu, z && own);
-  if (c.lane == 0 && bal) atomicAdd(&c.mcnt[k], __popc(bal));
+  // the warp's z count of atom k goes to lane k & 7's register; flushed to the
+  // CTA's shared counts once per 8-atom group (code_atoms)
+  const int nz = __popc(__ballot_sync(0xffffffffu, z && own));
+  if (c.lane == (k & 7)) t.mc += nz;
 }
 
 // Atoms [k0, k1) (k0 a multiple of 8) against the staged DT whose column 0 is
@@ -325,7 +328,10 @@ __device__ __forceinline__ void code_atoms(const CompactArgs& a, const CodeConst
       za = zna; zb = znb; sa = sna; sb = snb;
       zo += 2 * a.ld;
     }
-    // group done: the tile-blocked copy of w for the dictionary step, sum S^2
+    // group done: flush the z counts, the tile-blocked copy of w for the
+    // dictionary step, sum S^2
+    if (c.lane < 8 && t.mc) atomicAdd(&c.mcnt[kg + c.lane], t.mc);
+    t.mc = 0;
     if (c.live && c.g == 0) {
       if (MODE != kRngReplay) { t.sq_w += (double)t.sq_w8; t.sq_w8 = 0.0f; }
       float* wrow = c.wrow;
@@ -418,6 +424,7 @@ __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
   const int row_bytes = kp * 4;
   CodeThread t;
   t.sq_w8 = 0.0f;
+  t.mc = 0;
   const int per_blk = WC ? 32 / G : blockDim.x / G;
   const int64_t nblk = ceil_div(a.plist ? a.plist_n : a.n, per_blk);
   // blocks of patches are claimed dynamically (the launch may share the GPU with
