@@ -1354,7 +1354,7 @@ static void code_window_claim(int64_t n, int p, int k, int g, bool& ws, bool& wc
   code_dt_layout(p, k, &kc, &imgf, nullptr);
   const size_t per_cta = 228 * 1024 / 2 - 1024 - 512;
   ws = g == 1 && (size_t)imgf * 4 + (size_t)k * 8 + (size_t)(256 / g) * 9 * 4 > per_cta;
-  wc = g == 1 && kc >= k && !ws && n >= (1 << 20);   // small problems: CTA claiming (configs[0] +30 % otherwise)
+  wc = g == 1 && kc >= k && n >= (1 << 19);   // small problems: CTA claiming (configs[0] +30 % otherwise)
 }
 
 int code_launch_blocks(int cmax, int64_t n, int p, int k) {
@@ -1448,8 +1448,10 @@ int launch_code_compact(const CompactArgs& a_in, int mode, int& nblocks, cudaStr
   PB_CUDA_TRY(cudaMemsetAsync(a.blk_ctr, 0, sizeof(unsigned), st));
 #define PB_C(C, GG)                                                                                  \
   case C * 100 + GG: {                                                                               \
-    auto kern = ws ? (mode == kRngReplay ? k_code_compact<C, GG, kRngReplay, GG == 1, false>                    \
-                                         : k_code_compact<C, GG, kRngPhilox, GG == 1, false>)                  \
+    auto kern = ws && wc ? (mode == kRngReplay ? k_code_compact<C, GG, kRngReplay, GG == 1, GG == 1>           \
+                                               : k_code_compact<C, GG, kRngPhilox, GG == 1, GG == 1>)         \
+           : ws ? (mode == kRngReplay ? k_code_compact<C, GG, kRngReplay, GG == 1, false>                      \
+                                      : k_code_compact<C, GG, kRngPhilox, GG == 1, false>)                     \
            : wc ? (mode == kRngReplay ? k_code_compact<C, GG, kRngReplay, false, GG == 1>                      \
                                       : k_code_compact<C, GG, kRngPhilox, false, GG == 1>)                     \
                 : (mode == kRngReplay ? k_code_compact<C, GG, kRngReplay, false, false>                        \
