@@ -1354,7 +1354,7 @@ static void code_window_claim(int64_t n, int p, int k, int g, bool& ws, bool& wc
   code_dt_layout(p, k, &kc, &imgf, nullptr);
   const size_t per_cta = 228 * 1024 / 2 - 1024 - 512;
   ws = g == 1 && (size_t)imgf * 4 + (size_t)k * 8 + (size_t)(256 / g) * 9 * 4 > per_cta;
-  wc = g == 1 && kc >= k && n >= (1 << 19);   // small problems: CTA claiming (configs[0] +30 % otherwise)
+  wc = g == 1 && kc >= k && n >= (1 << 17);   // small problems: CTA claiming (configs[0] +30 % otherwise)
 }
 
 int code_launch_blocks(int cmax, int64_t n, int p, int k) {
