@@ -190,15 +190,13 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
     g.draws = d->rng_mode == PB_RNG_REPLAY ? d->atom_draws : nullptr;
     g.sc = sc; g.partials = ws.partials; g.reduced = ws.reduced; g.bar = ws.bar; g.max_blocks = kMaxDictBlocks;
     g.prof = g_dict_prof;
-    { const char* e = getenv("PB_DICT_DEBUG"); g.dbg = e ? atoi(e) : 0; }
+    g.dbg = PB_TUNE_INT("PB_DICT_DEBUG", 0);   // profiling bits exist in tuning builds only
     g.n = d->n; g.p = d->p; g.k = d->k; g.key0 = k0; g.key1 = k1;
     g.ld = c.ld;
     g.nnz = d->index->nnz;
     g.delta_g = ws.delta_g;   // atom shifts of the last updated block [8][P]
     g.seg_base = ix.seg_base;
-    { static double sc_env = -1.0;   // PB_DICT_SEG_COST: tuning override of the segment cost
-      if (sc_env < 0.0) { const char* e = getenv("PB_DICT_SEG_COST"); sc_env = e ? atof(e) : kDictSegCost; }
-      g.seg_cost = sc_env; }
+    g.seg_cost = PB_TUNE_DBL("PB_DICT_SEG_COST", kDictSegCost);
     if (d->resid_mode == PB_RESID_FROM_VALUES) {
       // Z*S == 0: every moment sum is 0 on every rank, the atoms are prior
       // redraws and the residual does not move (the first sweep of a cold
@@ -240,13 +238,21 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
     c2.plist_n = d->index->n_outliers;
     c2.block_sums = ws.block_sums + 2 * (size_t)nb1_expect;
     c2.blk_ctr = ws.ctr + 1;
-    static thread_local cudaStream_t side = nullptr;
-    static thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    if (!side) {
-      PB_CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-      PB_CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-      PB_CUDA_TRY(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    // side stream + fork/join events of the current device (one set per device
+    // ordinal and host thread: a stream belongs to the device it was created on)
+    static const int kMaxDev = 64;
+    static thread_local cudaStream_t sides[kMaxDev] = {};
+    static thread_local cudaEvent_t forks[kMaxDev] = {}, joins[kMaxDev] = {};
+    int dev = 0;
+    PB_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= kMaxDev) { set_error("device ordinal %d out of range", dev); return PB_EUNSUPPORTED; }
+    if (!sides[dev]) {
+      PB_CUDA_TRY(cudaStreamCreateWithFlags(&sides[dev], cudaStreamNonBlocking));
+      PB_CUDA_TRY(cudaEventCreateWithFlags(&forks[dev], cudaEventDisableTiming));
+      PB_CUDA_TRY(cudaEventCreateWithFlags(&joins[dev], cudaEventDisableTiming));
     }
+    cudaStream_t side = sides[dev];
+    cudaEvent_t ev_fork = forks[dev], ev_join = joins[dev];
     int nb1 = 0, nb2 = 0;
     PB_CUDA_TRY(cudaEventRecord(ev_fork, st));
     PB_CUDA_TRY(cudaStreamWaitEvent(side, ev_fork, 0));
@@ -410,11 +416,9 @@ int pb_build_index(pb_patch_index* pi, const uint8_t* observed, const float* val
   PB_CUDA_TRY(cudaMemcpyAsync(hist.data(), ix.hist, (size_t)(pi->p + 1) * 4, cudaMemcpyDeviceToHost, st));
   PB_CUDA_TRY(cudaStreamSynchronize(st));
   pi->cmax = cmax;
-  pi->split_count = getenv("PB_CODE_SPLIT_OFF") ? 0 : code_split_choose(hist.data(), pi->p, cmax);
-  if (const char* f = getenv("PB_CODE_SPLIT_AT")) {  // experiments: force the split threshold
-    const int t = atoi(f);
+  pi->split_count = PB_TUNE_FLAG("PB_CODE_SPLIT_OFF") ? 0 : code_split_choose(hist.data(), pi->p, cmax);
+  if (const int t = PB_TUNE_INT("PB_CODE_SPLIT_AT", 0))  // experiments: force the split threshold
     pi->split_count = (t > 0 && t < cmax) ? t : 0;
-  }
   pi->reserved = 0;
   pi->n_outliers = 0;
   if (pi->split_count > 0) {
@@ -452,14 +456,14 @@ int pb_dict_profile(int32_t enable, double* slots_ns_out) {
         for (int i = 0; i < kProfSlots; ++i) slots_ns_out[i] += (double)h[b * kProfSlots + i];
       }
       for (int i = 0; i < kProfSlots; ++i) slots_ns_out[i] /= nb ? nb : 1;
-      if (getenv("PB_DICT_PROF_CTAS")) {  // per-CTA element-phase and barrier-1 times (profiling aid)
+      if (PB_TUNE_FLAG("PB_DICT_PROF_CTAS")) {  // per-CTA element-phase and barrier-1 times (profiling aid)
         for (int b = 0; b < kMaxDictBlocks; ++b) {
           if (!h[b * kProfSlots + 2]) continue;
           fprintf(stderr, "cta %d elems %.4f tile_end %.4f sync1 %.4f\n", b, h[b * kProfSlots + 2] / 1e6,
                   h[b * kProfSlots + 3] / 1e6, h[b * kProfSlots + 6] / 1e6);
         }
       }
-      if (getenv("PB_DICT_PROF_DUMP")) {  // per-CTA spread of each slot (profiling aid)
+      if (PB_TUNE_FLAG("PB_DICT_PROF_DUMP")) {  // per-CTA spread of each slot (profiling aid)
         for (int i = 0; i < kProfSlots; ++i) {
           std::vector<double> v;
           for (int b = 0; b < kMaxDictBlocks; ++b)
@@ -585,7 +589,7 @@ int pb_problem_create(const pb_problem_desc* desc, pb_problem** out) {
   PB_A(frame, m) PB_A(mask, m) PB_A(values, p * n) PB_A(obs, p * n) PB_A(means, n) PB_A(counts, n)
   PB_A(atoms, k * p) PB_A(pi, k) PB_A(usage, k * ld) PB_A(weights, k * ld) PB_A(est, p * n) PB_A(recon, m)
   PB_A(m_count, k) PB_A(scalars, 1) PB_A(nobs_dev, 1) PB_A(out, m) PB_A(prev, m) PB_A(resid, m)
-  if (compose_tc_supported((int)p) && !getenv("PB_COMPOSE_TC_OFF")) PB_A(bpack, compose_tc_scratch_bytes((int)p, (int)k) / 4)
+  if (compose_tc_supported((int)p) && !PB_TUNE_FLAG("PB_COMPOSE_TC_OFF")) PB_A(bpack, compose_tc_scratch_bytes((int)p, (int)k) / 4)
   if (pr->grid.rank == 2 || pr->grid.rank == 3) {
     pr->panel_stride = pr->grid.rank == 3 ? pr->grid.tshape[2] : 1;
     pr->panel_px = m / pr->panel_stride;

@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "pb_tuning.cuh"
+
 #define PB_OK 0
 #define PB_ESHAPE -1
 #define PB_EVALUE -2

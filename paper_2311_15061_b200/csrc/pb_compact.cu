@@ -890,13 +890,13 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
     prefetched = false;
     __syncthreads();
     if (NSTAGE == 2 && t_lo < t_hi && !pf) {
-      if (threadIdx.x == 0 && !(a.dbg & 4)) issue(t_lo, seq & 1, blk);
+      if (threadIdx.x == 0 && !PB_DBG(a, 4)) issue(t_lo, seq & 1, blk);
     }
     for (int tile = t_lo; tile < t_hi; ++tile, ++seq) {
       const uint32_t st = NSTAGE == 2 ? (seq & 1) : 0;
       __syncthreads();   // previous tile fully consumed: its stage and cps buffer are free
       prof(0);
-      if (threadIdx.x == 0 && !(a.dbg & 4)) {
+      if (threadIdx.x == 0 && !PB_DBG(a, 4)) {
         if (NSTAGE == 1) { if (!(pf && tile == t_lo)) issue(tile, 0, blk); }
         else if (tile + 1 < t_hi) issue(tile + 1, st ^ 1, blk);
       }
@@ -906,12 +906,12 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
       const float* wcur = wbuf + (size_t)st * 2 * kTile * B;
       const uint32_t wcur_s = smem_u32(wcur), wprev_s = wcur_s + kTile * B * 4u;
       const int* cpt = cps + st * cpp;
-      if (!(a.dbg & 4)) mbar_wait(&mbar[st], (phase_bits >> st) & 1u);
+      if (!PB_DBG(a, 4)) mbar_wait(&mbar[st], (phase_bits >> st) & 1u);
       phase_bits ^= 1u << st;
       prof(1);
       const int m = (int)(re - rs);
       const int ws = (int)(rs - tb) + (int)((int64_t)m * wid / NW), we = (int)(rs - tb) + (int)((int64_t)m * (wid + 1) / NW);
-      if (ws < we && !(a.dbg & 8)) {
+      if (ws < we && !PB_DBG(a, 8)) {
         // Element phase of this warp's slice [ws, we).  The slice is cut into
         // segments that never cross a column end and hold at most kSegLen
         // elements; a ROUND gives one segment to each of the kGroups lane
@@ -1127,7 +1127,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
     // (no per-thread fence: the barrier's bar.sync + the master's gpu-scope
     // fence and release publish the CTA's partials, as in cooperative groups)
     prof(5);
-    if (a.dbg & 16) grid_sync(a.bar); else grid_sync_mono(a.bar + 2, bar_target);
+    if (PB_DBG(a, 16)) grid_sync(a.bar); else grid_sync_mono(a.bar + 2, bar_target);
     prof(6);
     // Cross-CTA reduction distributed by PIXEL: CTA c owns pixels c, c+G, ...;
     // one warp per (pixel, value) sums the G partials lane-strided then by a
@@ -1196,12 +1196,12 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
     if (a.split) return;  // split mode: the caller allreduces `reduced` across ranks, then k_dict_update
     // the next pass's first tile does not depend on the shifts: stage it now
     // (the owner scratch it overwrites is done) so it lands during the barrier
-    if (t_lo < t_hi && !(a.dbg & 4)) {
+    if (t_lo < t_hi && !PB_DBG(a, 4)) {
       if (threadIdx.x == 0) issue(t_lo, NSTAGE == 2 ? (seq & 1) : 0u, blk + 1);
       prefetched = true;
     }
     prof(10);
-    if (a.dbg & 16) grid_sync(a.bar); else grid_sync_mono(a.bar + 2, bar_target);
+    if (PB_DBG(a, 16)) grid_sync(a.bar); else grid_sync_mono(a.bar + 2, bar_target);
     prof(8);
     for (int t = threadIdx.x; t < B * p; t += blockDim.x) dprev[t] = __ldcg(a.delta_g + t);
     __syncthreads();
@@ -1346,8 +1346,10 @@ static double code_cost(int c, int g) {
 
 // Window layout and block claiming of a code-step launch (256 threads per CTA):
 // pitch-8 swizzled w windows when only they let two CTAs share an SM; warps
-// claim their own 32-patch blocks when D is staged whole with pitch-9 windows
-// (configs[0]/[2]/[4]: -4 %; with the pitch-8 windows of configs[1] +1.5 %).
+// claim their own 32-patch blocks whenever D is staged whole (either window
+// pitch) and the problem has at least 2^17 patches: configs[2]/[4] -4 %, and
+// combined with the pitch-8 windows configs[1] -7 % (v22: 2.12 -> 1.97 ms).
+// Covered at P = 100, K = 256, >= 2^17 patches by tests/test_gpu_scale.py.
 static void code_window_claim(int64_t n, int p, int k, int g, bool& ws, bool& wc) {
   int kc;
   int64_t imgf;
@@ -1493,16 +1495,14 @@ static int launch_dict_gram_b(DictGramArgs a, cudaStream_t st) {
   if (per_sm < 1) { set_error("dictionary step cannot be resident"); return PB_EUNSUPPORTED; }
   int blocks = sm_count_c() * per_sm;
   if (blocks > a.max_blocks) blocks = a.max_blocks;
-  static int cap = -1;   // PB_DICT_MAX_CTAS: grid cap for tuning experiments
-  if (cap < 0) { const char* e = getenv("PB_DICT_MAX_CTAS"); cap = e ? atoi(e) : 0; }
+  const int cap = PB_TUNE_INT("PB_DICT_MAX_CTAS", 0);   // grid cap for tuning experiments
   if (cap > 0 && blocks > cap) blocks = cap;
   {  // owner partials staged behind the owner scratch (inside the W staging area) when they fit
     using L = GramLayout<B>;
     const size_t npart = (size_t)(NW * 32) / L::NACC;
     const size_t scratch = ((size_t)(a.p + blocks - 1) / blocks * L::NACC + npart * L::NACC) * 8 + (size_t)B * 40;
     const size_t off = (scratch + 127) & ~(size_t)127;
-    static int nostage = -1;   // PB_DICT_NO_PSTAGE=1: owners read the partials from L2 (A/B)
-    if (nostage < 0) { const char* e = getenv("PB_DICT_NO_PSTAGE"); nostage = e ? atoi(e) : 0; }
+    const int nostage = PB_TUNE_INT("PB_DICT_NO_PSTAGE", 0);   // 1: owners read the partials from L2 (A/B)
     a.pstage_off = (!nostage && off + (size_t)blocks * L::NACC * 4 <= wbytes) ? (int)off : 0;
   }
   PB_CUDA_TRY(cudaMemsetAsync(a.bar, 0, 4 * sizeof(unsigned), st));
@@ -1514,8 +1514,7 @@ static int launch_dict_gram_b(DictGramArgs a, cudaStream_t st) {
 int launch_dict_gram(const DictGramArgs& a, cudaStream_t st) {
   // two 8-warp CTAs per SM (single-buffered staging) when they fit in shared
   // memory, else one 16-warp CTA with double-buffered staging
-  static int variant = -1;
-  if (variant < 0) { const char* e = getenv("PB_DICT_VARIANT"); variant = e ? atoi(e) : 0; }
+  const int variant = PB_TUNE_INT("PB_DICT_VARIANT", 0);
   if (variant != 1 && 2 * dict_gram_smem<8, kDictGroupLanes, kDictSegLen, 8, 1>(a.p, nullptr) <= 226 * 1024)
     return launch_dict_gram_b<8, kDictGroupLanes, kDictSegLen, 8, 1>(a, st);
   return launch_dict_gram_b<8, kDictGroupLanes, kDictSegLen, 16, 2>(a, st);

@@ -396,8 +396,7 @@ int launch_build_index(PatchIndex& ix, const uint8_t* obs, const float* values, 
   k_tile_fill<<<ix.ntiles, kFillThreads, 0, st>>>(obs, values, counts, ix.n, ix.p, ix.tile_base, ix.colptr, ix.e_loc,
                                            ix.x_csc, ix.rowptr, ix.csr_p, ix.csr_pos);
   {
-    static int spread = -1;   // PB_INDEX_NO_SPREAD=1: keep ascending patch order inside columns (A/B)
-    if (spread < 0) { const char* e = getenv("PB_INDEX_NO_SPREAD"); spread = (e && atoi(e)) ? 0 : 1; }
+    const int spread = !PB_TUNE_INT("PB_INDEX_NO_SPREAD", 0);   // 0: ascending patch order inside columns (A/B)
     if (spread)
       k_csc_spread<<<(unsigned)ceil_div((int64_t)ix.ntiles * ix.p, kSpreadWarps), kSpreadWarps * 32, 0, st>>>(
           ix.tile_base, ix.colptr, ix.ntiles, ix.p, ix.e_loc, (const uint32_t*)ix.x_csc, ix.csr_pos);

@@ -326,9 +326,7 @@ int launch_accumulate_atoms(bool resid, const float* values, const uint8_t* obs,
                             int accumulate, int64_t ld, cudaStream_t st) {
   if (ld < n) ld = n;
   if (!resid && compose_tc_supported(p)) {  // the dense contraction on the tensor cores (3xTF32)
-    static int use_tc = -1;
-    if (use_tc < 0) { const char* e = getenv("PB_COMPOSE_TC"); use_tc = e ? atoi(e) : 1; }
-    if (use_tc) return launch_compose_tc(usage, weights, ld, atoms, p, k_len, n, out, accumulate, st);
+    if (PB_TUNE_INT("PB_COMPOSE_TC", 1)) return launch_compose_tc(usage, weights, ld, atoms, p, k_len, n, out, accumulate, st);
   }
   int vpt, g;
   if (!pick_layout(p, vpt, g)) { set_error("patch size %d exceeds 2048", p); return PB_EUNSUPPORTED; }
