@@ -255,6 +255,27 @@ int pb_render_atlas(const float* atoms, const double* pi, int32_t k, int32_t ran
  *      pipeline.py:217-251).  Owns all device buffers. ---- */
 typedef struct pb_problem pb_problem;
 
+/* Host draw provider of a replay-mode problem (pb_problem_desc.replay = 1): the
+ * reference's keyed numpy streams (rng.py:25-32) evaluated by the caller; called
+ * from inside pb_problem_submit_frame on the calling thread.
+ *   PB_DRAW_PRIOR      (epoch 0)  out0 = prior atoms, K*P f64 row-major, stream (seed, 1)
+ *                                 scaled by 1/sqrt(P) (bpfa.py:121-122)
+ *   PB_DRAW_EPOCH      (epoch e)  out0 = atom normals K*P, stream (seed, 2, e, k) — NULL when
+ *                                 the dictionary is frozen; out1 / out2 = code uniforms /
+ *                                 normals K*N, stream (seed, 3, e, k) (bpfa.py:293-310)
+ *   PB_DRAW_POSTERIOR  (epoch e)  in m_counts (K), sums = {sum S^2, sum R^2, n_obs};
+ *                                 out0 = pi (K) from (seed, 4, e), out1 = {gamma_s, gamma_eps}
+ *                                 from (seed, 5, e), floors applied (bpfa.py:313-333)
+ * Return 0 on success; anything else aborts the frame with PB_EVALUE. */
+#define PB_DRAW_PRIOR 0
+#define PB_DRAW_EPOCH 1
+#define PB_DRAW_POSTERIOR 2
+typedef int (*pb_draw_fn)(void* ctx, int32_t stage, int64_t epoch, const int32_t* m_counts, const double* sums,
+                          double* out0, double* out1, double* out2);
+
+#define PB_INIT_PRIOR 0    /* bpfa.init_state(init_mode="prior") */
+#define PB_INIT_DATA 1     /* init_mode="data" (bpfa.py:126-134; Pipeline default, pipeline.py:52) */
+
 typedef struct pb_problem_desc {
   pb_grid_desc grid;
   int32_t num_atoms;
@@ -266,12 +287,20 @@ typedef struct pb_problem_desc {
   int32_t data_consistency;
   int32_t warm_start;
   int32_t average_last;
+  int32_t replay;        /* 0: device Philox draws (the fast path); 1: the reference streams from `draw` */
+  int32_t init_mode;     /* PB_INIT_*: cold start of the dictionary.  Data-mode atoms only survive
+                            the first dictionary step when the dictionary is frozen (SURVEY App. A
+                            Q1), so they are gathered on the device only then. */
+  pb_draw_fn draw;       /* replay mode only */
+  void* draw_ctx;
 } pb_problem_desc;
 
 int pb_problem_create(const pb_problem_desc* desc, pb_problem** out);
 int pb_problem_destroy(pb_problem* pr);
 /* One live frame: H2D frame (f64) + mask (uint8, cached when unchanged),
- * extract, epochs_per_frame warm-started sweeps (device RNG), compose, overlap-add,
+ * extract, epochs_per_frame warm-started sweeps (device Philox draws, or in replay
+ * mode the reference streams from desc.draw, one host round trip per epoch for
+ * the pi / gamma draws), compose, overlap-add,
  * data consistency, D2H reconstruction (f64).  Mirrors Pipeline.submit_frame's
  * hot slice (pipeline.py:224-251). */
 int pb_problem_submit_frame(pb_problem* pr, const double* frame_host, const uint8_t* mask_host,

@@ -63,10 +63,17 @@ class EpochDesc(ctypes.Structure):
                 ("allreduce", ALLREDUCE_FN), ("allreduce_ctx", c_vp)]
 
 
+PB_DRAW_PRIOR, PB_DRAW_EPOCH, PB_DRAW_POSTERIOR = 0, 1, 2
+PB_INIT_PRIOR, PB_INIT_DATA = 0, 1
+DRAW_FN = ctypes.CFUNCTYPE(c_i32, c_vp, c_i32, c_i64, ctypes.POINTER(c_i32), ctypes.POINTER(c_f64),
+                           ctypes.POINTER(c_f64), ctypes.POINTER(c_f64), ctypes.POINTER(c_f64))
+
+
 class ProblemDesc(ctypes.Structure):
     _fields_ = [("grid", GridDesc), ("num_atoms", c_i32), ("hyper", c_f64 * 6), ("seed", c_u64),
                 ("mean_subtract", c_i32), ("epochs_per_frame", c_i32), ("freeze_dict", c_i32),
-                ("data_consistency", c_i32), ("warm_start", c_i32), ("average_last", c_i32)]
+                ("data_consistency", c_i32), ("warm_start", c_i32), ("average_last", c_i32),
+                ("replay", c_i32), ("init_mode", c_i32), ("draw", DRAW_FN), ("draw_ctx", c_vp)]
 
 
 # name -> (restype, argtypes); exactly the functions include/pb200.h declares.

@@ -1,5 +1,6 @@
 // pb200 — C ABI (include/pb200.h) over the sm_100a kernels, plus the native
 // stateful "problem" used for the host-buffer live-frame path.
+#include <math.h>
 #include <stdarg.h>
 #include <stdlib.h>
 #include <stdio.h>
@@ -546,6 +547,12 @@ struct pb_problem {
   int64_t n_obs = 0;
   bool have_state = false;
   float last_ms = 0.f;
+  // replay mode (desc.replay): host draw staging (pinned) and device copies
+  double *h_atom = nullptr, *h_u = nullptr, *h_g = nullptr, *h_pi = nullptr;
+  double *d_atom = nullptr, *d_u = nullptr, *d_g = nullptr;
+  int32_t* h_m = nullptr;
+  pb_scalars* h_sc = nullptr;
+  int32_t epoch_host = 0;   // replay mode: the host owns the epoch counter
 };
 
 namespace {
@@ -565,6 +572,10 @@ int pb_problem_destroy(pb_problem* pr) {
                   pr->out, pr->prev, pr->resid, pr->panel, pr->masked, pr->bpack};
   for (void* b : bufs)
     if (b) cudaFree(b);
+  for (void* b : {(void*)pr->d_atom, (void*)pr->d_u, (void*)pr->d_g})
+    if (b) cudaFree(b);
+  for (void* b : {(void*)pr->h_atom, (void*)pr->h_u, (void*)pr->h_g, (void*)pr->h_pi, (void*)pr->h_m, (void*)pr->h_sc})
+    if (b) cudaFreeHost(b);
   if (pr->ev0) cudaEventDestroy(pr->ev0);
   if (pr->ev1) cudaEventDestroy(pr->ev1);
   if (pr->stream) cudaStreamDestroy(pr->stream);
@@ -578,6 +589,11 @@ int pb_problem_create(const pb_problem_desc* desc, pb_problem** out) {
   if (desc->epochs_per_frame < 1) { set_error("epochs_per_frame must be >= 1"); return PB_EVALUE; }
   for (int j = 0; j < 6; ++j)
     if (!(desc->hyper[j] > 0)) { set_error("hyperparameters must be > 0"); return PB_EVALUE; }
+  if (desc->replay && !desc->draw) { set_error("replay mode needs a draw provider"); return PB_EVALUE; }
+  if (desc->init_mode != PB_INIT_PRIOR && desc->init_mode != PB_INIT_DATA) {
+    set_error("unknown init mode %d", desc->init_mode);
+    return PB_EVALUE;
+  }
   pb_problem* pr = new pb_problem();
   pr->desc = *desc;
   int rc = make_grid(&desc->grid, pr->grid);
@@ -595,6 +611,19 @@ int pb_problem_create(const pb_problem_desc* desc, pb_problem** out) {
     pr->panel_px = m / pr->panel_stride;
     PB_A(panel, pr->panel_px) PB_A(masked, pr->panel_px)
   }
+  if (desc->replay) {  // the epoch's draws: K*P atom normals, K*N uniforms and normals
+    PB_A(d_atom, k * p) PB_A(d_u, k * n) PB_A(d_g, k * n)
+    if (cudaMallocHost((void**)&pr->h_atom, (size_t)k * p * 8) != cudaSuccess ||
+        cudaMallocHost((void**)&pr->h_u, (size_t)k * n * 8) != cudaSuccess ||
+        cudaMallocHost((void**)&pr->h_g, (size_t)k * n * 8) != cudaSuccess ||
+        cudaMallocHost((void**)&pr->h_pi, (size_t)k * 8) != cudaSuccess ||
+        cudaMallocHost((void**)&pr->h_m, (size_t)k * 4) != cudaSuccess ||
+        cudaMallocHost((void**)&pr->h_sc, sizeof(pb_scalars)) != cudaSuccess) {
+      set_error("pinned replay buffers: allocation failed");
+      pb_problem_destroy(pr);
+      return PB_ECUDA;
+    }
+  }
 #undef PB_A
   if (cudaStreamCreateWithFlags(&pr->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&pr->ev0) != cudaSuccess || cudaEventCreate(&pr->ev1) != cudaSuccess) {
@@ -607,9 +636,13 @@ int pb_problem_create(const pb_problem_desc* desc, pb_problem** out) {
 }
 
 static int problem_cold_init(pb_problem* pr) {
-  // init_state(prior) on device (bpfa.py:121-149): prior atoms, pi = a/(a+b),
-  // gammas at their prior means, Z = S = 0, epoch 0.  (Data-mode seeding only
-  // matters with freeze_dict; see infer() in bpfa.py of this package.)
+  // init_state on device (bpfa.py:104-152): prior atoms (device Philox, or the
+  // reference stream (seed, 1) in replay mode), data-mode seeding from the patches
+  // with the most observed elements when the dictionary is frozen (otherwise the
+  // first dictionary step redraws every atom from the prior before any use,
+  // SURVEY App. A Q1), pi = a/(a+b), gammas at their prior means, Z = S = 0,
+  // epoch 0.  An installed dictionary (install_dictionary, bpfa.py:355-376)
+  // replaces the atoms and pi.
   uint32_t k0, k1;
   device_key(pr->desc.seed, k0, k1);
   std::vector<double> pi(pr->k, pr->desc.hyper[0] / (pr->desc.hyper[0] + pr->desc.hyper[1]));
@@ -619,16 +652,72 @@ static int problem_cold_init(pb_problem* pr) {
     pi.swap(pr->pending_pi);
     PB_CUDA_TRY(cudaMemcpyAsync(pr->atoms, atoms.data(), atoms.size() * 4, cudaMemcpyHostToDevice, pr->stream));
   } else {
-    int rc = launch_prior_atoms(pr->atoms, pr->k, pr->p, k0, k1, pr->stream);
-    if (rc) return rc;
+    if (pr->desc.replay) {
+      if (pr->desc.draw(pr->desc.draw_ctx, PB_DRAW_PRIOR, 0, nullptr, nullptr, pr->h_atom, nullptr, nullptr)) {
+        set_error("replay draw provider failed (prior atoms)");
+        return PB_EVALUE;
+      }
+      atoms.resize((size_t)pr->k * pr->p);
+      for (size_t j = 0; j < atoms.size(); ++j) atoms[j] = (float)pr->h_atom[j];
+      PB_CUDA_TRY(cudaMemcpyAsync(pr->atoms, atoms.data(), atoms.size() * 4, cudaMemcpyHostToDevice, pr->stream));
+    } else {
+      int rc = launch_prior_atoms(pr->atoms, pr->k, pr->p, k0, k1, pr->stream);
+      if (rc) return rc;
+    }
+    if (pr->desc.init_mode == PB_INIT_DATA && pr->desc.freeze_dict) {
+      int rc = launch_data_atoms(pr->values, pr->counts, pr->n, pr->p, pr->k, pr->atoms, pr->stream);
+      if (rc) return rc;
+    }
   }
   PB_CUDA_TRY(cudaMemcpyAsync(pr->pi, pi.data(), pr->k * sizeof(double), cudaMemcpyHostToDevice, pr->stream));
   pb_scalars s{};
   s.gamma_s = fmax(pr->desc.hyper[2] / pr->desc.hyper[3], 1e-12);
   s.gamma_eps = fmax(pr->desc.hyper[4] / pr->desc.hyper[5], 1e-12);
   PB_CUDA_TRY(cudaMemcpyAsync(pr->scalars, &s, sizeof(s), cudaMemcpyHostToDevice, pr->stream));
-  PB_CUDA_TRY(cudaStreamSynchronize(pr->stream));  // s/pi live on this stack frame
+  PB_CUDA_TRY(cudaStreamSynchronize(pr->stream));  // s/pi/atoms live on this stack frame
   pr->have_state = true;
+  pr->epoch_host = 0;
+  return PB_OK;
+}
+
+// One replay-mode sweep of the problem: the reference's draws for this epoch
+// from the host provider (uploaded), the device sweep, then the pi / gamma draws
+// on the host from the epoch's usage counts and sums (bpfa.py:313-333) — the
+// same split as bpfa.gibbs_epoch(rng="numpy") of the Python API.
+static int replay_epoch(pb_problem* pr, pb_epoch_desc& d) {
+  cudaStream_t st = pr->stream;
+  const int64_t ep = (int64_t)pr->epoch_host + 1;
+  const size_t kp = (size_t)pr->k * pr->p, kn = (size_t)pr->k * pr->n;
+  const bool frozen = d.freeze_dict != 0;
+  if (pr->desc.draw(pr->desc.draw_ctx, PB_DRAW_EPOCH, ep, nullptr, nullptr, frozen ? nullptr : pr->h_atom, pr->h_u,
+                    pr->h_g)) {
+    set_error("replay draw provider failed (epoch %lld)", (long long)ep);
+    return PB_EVALUE;
+  }
+  if (!frozen) PB_CUDA_TRY(cudaMemcpyAsync(pr->d_atom, pr->h_atom, kp * 8, cudaMemcpyHostToDevice, st));
+  PB_CUDA_TRY(cudaMemcpyAsync(pr->d_u, pr->h_u, kn * 8, cudaMemcpyHostToDevice, st));
+  PB_CUDA_TRY(cudaMemcpyAsync(pr->d_g, pr->h_g, kn * 8, cudaMemcpyHostToDevice, st));
+  d.atom_draws = frozen ? nullptr : pr->d_atom;
+  d.code_u = pr->d_u;
+  d.code_g = pr->d_g;
+  int rc = run_epoch(&d, pr->m_count, st);
+  if (rc) return rc;
+  PB_CUDA_TRY(cudaMemcpyAsync(pr->h_m, pr->m_count, (size_t)pr->k * 4, cudaMemcpyDeviceToHost, st));
+  PB_CUDA_TRY(cudaMemcpyAsync(pr->h_sc, pr->scalars, sizeof(pb_scalars), cudaMemcpyDeviceToHost, st));
+  PB_CUDA_TRY(cudaStreamSynchronize(st));
+  double sums[3] = {pr->h_sc->sq_w, pr->h_sc->sq_r, (double)pr->n_obs};
+  double gam[2] = {0.0, 0.0};
+  if (pr->desc.draw(pr->desc.draw_ctx, PB_DRAW_POSTERIOR, ep, pr->h_m, sums, pr->h_pi, gam, nullptr)) {
+    set_error("replay draw provider failed (pi / gamma, epoch %lld)", (long long)ep);
+    return PB_EVALUE;
+  }
+  pr->h_sc->gamma_s = gam[0];
+  pr->h_sc->gamma_eps = gam[1];
+  pr->h_sc->epoch = (int32_t)ep;
+  pr->h_sc->diverged = !(isfinite(gam[0]) && isfinite(gam[1]) && isfinite(sums[1]));  // bpfa.py:335-342
+  PB_CUDA_TRY(cudaMemcpyAsync(pr->pi, pr->h_pi, (size_t)pr->k * 8, cudaMemcpyHostToDevice, st));
+  PB_CUDA_TRY(cudaMemcpyAsync(pr->scalars, pr->h_sc, sizeof(pb_scalars), cudaMemcpyHostToDevice, st));
+  pr->epoch_host = (int32_t)ep;
   return PB_OK;
 }
 
@@ -695,7 +784,7 @@ int pb_problem_submit_frame_ex(pb_problem* pr, const double* frame_host, const u
   pb_epoch_desc d{};
   d.n = n; d.ld = pr->ld; d.p = pr->p; d.k = pr->k;
   d.freeze_dict = pr->desc.freeze_dict;
-  d.rng_mode = PB_RNG_PHILOX;
+  d.rng_mode = pr->desc.replay ? PB_RNG_REPLAY : PB_RNG_PHILOX;
   d.seed = pr->desc.seed;
   d.n_obs = pr->n_obs;
   for (int j = 0; j < 6; ++j) d.hyper[j] = pr->desc.hyper[j];
@@ -706,7 +795,11 @@ int pb_problem_submit_frame_ex(pb_problem* pr, const double* frame_host, const u
   int tail = pr->desc.average_last < 1 ? 1 : (pr->desc.average_last > epochs ? epochs : pr->desc.average_last);
   for (int e = 0; e < epochs; ++e) {
     d.resid_mode = e == 0 ? PB_RESID_FROM_VALUES : PB_RESID_CARRY;  // codes were just reset
-    if ((rc = run_epoch(&d, pr->m_count, st))) return rc;
+    if (pr->desc.replay) {
+      if ((rc = replay_epoch(pr, d))) return rc;
+    } else if ((rc = run_epoch(&d, pr->m_count, st))) {
+      return rc;
+    }
     if (e >= epochs - tail) {
       if (pr->bpack)  // tensor-core compose with the problem's packed-D scratch
         rc = launch_compose_tc(pr->usage, pr->weights, pr->ld, pr->atoms, pr->p, pr->k, n, pr->est,

@@ -243,3 +243,68 @@ int launch_atlas(const float* atoms, const double* pi, int k, int rank, const in
 }
 
 }  // namespace pb
+
+namespace pb {
+
+// ---- data-mode dictionary seeding (bpfa.py:126-134) ------------------------
+// order = argsort(-counts, kind="stable"): a stable ascending radix sort of
+// (P - count, patch) pairs; atom j <- patch order[j], unit-normalized (norm in
+// f64), zero-norm candidates keep their prior atom; atoms past min(K, N) too.
+__global__ void k_seed_keys(const int32_t* counts, int64_t n, int p, uint32_t* keys, int32_t* idx) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = (uint32_t)(p - counts[i]);
+    idx[i] = (int32_t)i;
+  }
+}
+
+__global__ void __launch_bounds__(128) k_data_atoms(const float* values_pn, int64_t n, int p, const int32_t* order,
+                                                    float* atoms) {
+  __shared__ double part[4];
+  const int64_t i = order[blockIdx.x];
+  double ss = 0.0;
+  for (int q = threadIdx.x; q < p; q += blockDim.x) {
+    const double v = values_pn[(int64_t)q * n + i];
+    ss += v * v;
+  }
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  const double nrm = sqrt(part[0] + part[1] + part[2] + part[3]);
+  if (nrm > 0.0)
+    for (int q = threadIdx.x; q < p; q += blockDim.x)
+      atoms[(int64_t)blockIdx.x * p + q] = (float)((double)values_pn[(int64_t)q * n + i] / nrm);
+}
+
+int launch_data_atoms(const float* values_pn, const int32_t* counts, int64_t n, int p, int k, float* atoms,
+                      cudaStream_t st) {
+  if (n < 1 || k < 1) return PB_OK;
+  if (n >= ((int64_t)1 << 31)) { set_error("data-mode seeding supports < 2^31 patches"); return PB_EUNSUPPORTED; }
+  const int take = (int)(k < n ? k : n);
+  int bits = 1;
+  while ((1 << bits) <= p) ++bits;
+  uint32_t *kin = nullptr, *kout = nullptr;
+  int32_t *iin = nullptr, *iout = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  PB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kin, kout, iin, iout, (int)n, 0, bits, st));
+  char* buf = nullptr;
+  const size_t al = 256, nb = ((size_t)n * 4 + al - 1) / al * al;
+  PB_CUDA_TRY(cudaMallocAsync((void**)&buf, 4 * nb + tmp_bytes, st));
+  kin = (uint32_t*)buf; kout = (uint32_t*)(buf + nb); iin = (int32_t*)(buf + 2 * nb); iout = (int32_t*)(buf + 3 * nb);
+  tmp = buf + 4 * nb;
+  int64_t g = (n + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  k_seed_keys<<<(unsigned)g, 256, 0, st>>>(counts, n, p, kin, iin);
+  int rc = PB_OK;
+  if (cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, iin, iout, (int)n, 0, bits, st) != cudaSuccess) {
+    set_error("data-mode seeding sort failed");
+    rc = PB_ECUDA;
+  } else {
+    k_data_atoms<<<take, 128, 0, st>>>(values_pn, n, p, iout, atoms);
+    if (cudaGetLastError() != cudaSuccess) { set_error("k_data_atoms launch failed"); rc = PB_ECUDA; }
+  }
+  cudaFreeAsync(buf, st);
+  return rc;
+}
+
+}  // namespace pb

@@ -20,6 +20,10 @@ struct LiveFinishArgs {
 };
 
 int launch_live_finish(const LiveFinishArgs& a, cudaStream_t st);
+// bpfa.py:126-134 data-mode seeding: atoms[j] <- unit-normalized values of the
+// j-th patch by (observed count desc, index asc); zero-norm / surplus atoms untouched
+int launch_data_atoms(const float* values_pn, const int32_t* counts, int64_t n, int p, int k, float* atoms,
+                      cudaStream_t st);
 // sampling.py:184-207 on device; status 1 = all-zero residual (uniform draw)
 int adaptive_mask(const double* resid, int64_t m, int64_t budget, int64_t n_exploit, uint32_t k0, uint32_t k1,
                   uint64_t frame_index, uint8_t* mask, int* status, cudaStream_t st);

@@ -40,7 +40,13 @@ class LiveProblem:
 
     def __init__(self, shape, patch_spec: PatchSpec, hyperparams: Hyperparams | None = None, seed: int = 0,
                  epochs_per_frame: int = 2, freeze_dict: bool = False, data_consistency: bool = False,
-                 warm_start: bool = True, average_last: int = 1, mean_subtract: bool | None = None):
+                 warm_start: bool = True, average_last: int = 1, mean_subtract: bool | None = None,
+                 init_mode: str = "data", rng: str = "philox"):
+        """``rng="philox"``: device draws (the fast path).  ``rng="numpy"``: replay
+        mode — the native problem consumes the reference's own keyed streams
+        (rng.py:25-32; bpfa.py:121-122, 293-333), drawn on the host by a callback
+        the library invokes once per epoch (plus once for the pi / gamma draws),
+        so a frame reproduces Pipeline.submit_frame's draws exactly."""
         self.shape = tuple(int(m) for m in shape)
         patch_spec.validate_for(self.shape)
         hp = hyperparams or Hyperparams()
@@ -59,6 +65,17 @@ class LiveProblem:
         d.data_consistency = int(bool(data_consistency))
         d.warm_start = int(bool(warm_start))
         d.average_last = int(average_last)
+        if init_mode not in ("data", "prior"):
+            raise ValueError(f"unknown init mode {init_mode!r}")
+        d.init_mode = _lib.PB_INIT_DATA if init_mode == "data" else _lib.PB_INIT_PRIOR
+        self._draw = None
+        if rng == "numpy":
+            self._draw = _lib.DRAW_FN(_replay_provider(int(seed), hp, spec_n(patch_spec, self.shape),
+                                                       patch_spec.patch_size))
+            d.replay = 1
+            d.draw = self._draw
+        elif rng != "philox":
+            raise ValueError(f"unknown rng mode {rng!r}")
         self._lib = _lib.load()
         self._h = ctypes.c_void_p()
         _lib.check(self._lib.pb_problem_create(ctypes.byref(d), ctypes.byref(self._h)))
@@ -149,6 +166,61 @@ class LiveProblem:
         sc = _lib.Scalars()
         _lib.check(self._lib.pb_problem_get_dictionary(self._h, atoms.ctypes.data, pi.ctypes.data, ctypes.byref(sc)))
         return atoms, pi, sc
+
+
+def spec_n(spec: PatchSpec, shape):
+    return int(spec.num_patches(shape))
+
+
+def _replay_provider(seed: int, hp: Hyperparams, n: int, p: int):
+    """The reference's draws for the native replay mode (pb_draw_fn)."""
+    import math
+    import traceback
+
+    from .bpfa import PRECISION_FLOOR
+    from .rng import DOMAIN_ATOM, DOMAIN_CODE, DOMAIN_GAMMA, DOMAIN_INIT, DOMAIN_PI, keyed_rng
+
+    k = hp.num_atoms
+
+    def arr(ptr, shape):
+        return np.ctypeslib.as_array(ptr, shape=shape)
+
+    def fn(ctx, stage, epoch, m_counts, sums, out0, out1, out2):
+        try:
+            if stage == _lib.PB_DRAW_PRIOR:                     # bpfa.py:121-122
+                a = arr(out0, (k, p))
+                a[:] = keyed_rng(seed, DOMAIN_INIT).standard_normal((k, p)) / math.sqrt(p)
+            elif stage == _lib.PB_DRAW_EPOCH:                   # bpfa.py:304, 258-259
+                if out0:
+                    a = arr(out0, (k, p))
+                    for j in range(k):
+                        keyed_rng(seed, DOMAIN_ATOM, epoch, j).standard_normal(out=a[j])
+                u, g = arr(out1, (k, n)), arr(out2, (k, n))
+                for j in range(k):
+                    r = keyed_rng(seed, DOMAIN_CODE, epoch, j)
+                    r.random(out=u[j])
+                    r.standard_normal(out=g[j])
+            elif stage == _lib.PB_DRAW_POSTERIOR:               # bpfa.py:313-333
+                m = arr(m_counts, (k,)).astype(np.float64)
+                sq_w, sq_r, n_obs = (float(x) for x in arr(sums, (3,)))
+                sh_a = hp.concentration_a / k + m
+                sh_b = hp.concentration_b * (k - 1) / k + n - m
+                arr(out0, (k,))[:] = keyed_rng(seed, DOMAIN_PI, epoch).beta(
+                    np.maximum(sh_a, PRECISION_FLOOR), np.maximum(sh_b, PRECISION_FLOOR))
+                g5 = keyed_rng(seed, DOMAIN_GAMMA, epoch)
+                gs = max(g5.gamma(hp.weight_shape + 0.5 * n * k, 1.0 / (hp.weight_rate + 0.5 * sq_w)),
+                         PRECISION_FLOOR)
+                ge = max(g5.gamma(hp.noise_shape + 0.5 * n_obs, 1.0 / (hp.noise_rate + 0.5 * sq_r)),
+                         PRECISION_FLOOR)
+                arr(out1, (2,))[:] = (gs, ge)
+            else:
+                return 1
+            return 0
+        except Exception:  # noqa: BLE001 — reported to C as a failure code
+            traceback.print_exc()
+            return 1
+
+    return fn
 
 
 def adaptive_mask(residual, ratio: float, exploit_fraction: float = 0.5, seed: int = 0, frame_index: int = 0):

@@ -128,3 +128,53 @@ def test_live_sequence_replay_matches_reference(golden, cuda_device):
         ref = g[f"f{t}_recon"]
         assert abs(psnr(rec, frame) - psnr(ref, frame)) <= 0.05, t
         assert np.abs(rec - ref).max() <= 1e-3, (t, np.abs(rec - ref).max())
+
+
+def test_native_replay_matches_reference_pipeline(golden, cuda_device):
+    """The NATIVE live path (pb_problem_submit_frame, host buffers) in replay
+    mode against the reference Pipeline's 3 warm-started frames
+    (tests/golden/live.npz: Pipeline defaults — init "data", 2 epochs/frame,
+    DC off): per-frame reconstruction within 1e-3 and PSNR within 0.05 dB."""
+    from paper_2311_15061_b200.live import LiveProblem
+
+    g = golden("live.npz")
+    shape = g["f0_frame"].shape
+    with LiveProblem(shape, pp.PatchSpec((6, 6)), gb.Hyperparams(num_atoms=8), seed=0, epochs_per_frame=2,
+                     rng="numpy") as lp:
+        for t in range(3):
+            frame, mask = g[f"f{t}_frame"], g[f"f{t}_mask"]
+            rec = lp.submit_frame(frame, mask).reconstruction
+            ref = g[f"f{t}_recon"]
+            assert abs(psnr(rec, frame) - psnr(ref, frame)) <= 0.05, t
+            assert np.abs(rec - ref).max() <= 1e-3, (t, np.abs(rec - ref).max())
+            atoms, _, sc = lp.dictionary()
+            assert np.abs(atoms - g[f"f{t}_atoms"]).max() <= 1e-4
+            assert sc.epoch == 2 * (t + 1)
+
+
+def test_native_frozen_data_init_matches_oracle(cuda_device):
+    """freeze_dict without an installed dictionary: the native cold
+    start seeds the atoms from the K patches with the most observed elements
+    (bpfa.py:126-134, on device) and keeps them; replay mode then reproduces the
+    oracle's frozen inference."""
+    from oracle import bpfa as ob
+    from oracle import patches as op
+    from paper_2311_15061_b200.live import LiveProblem
+
+    img = inputs.synthetic_texture((40, 44), seed=3)
+    mask = inputs.make_mask(img.shape, 0.3, "uniform-random", 3)
+    k = 10
+    opm = op.extract_patches(img, mask, (6, 6), (), True)
+    hp = ob.Hyper(num_atoms=k)
+    ost = ob.init_state(opm, hp, 5, "data")
+    want_atoms = ost.atoms.copy()
+    ost, oest = ob.infer(opm, hp, 3, 5, freeze_dict=True, state=ost)
+    orec = op.reconstitute(opm, oest)
+    for rng in ("numpy", "philox"):
+        with LiveProblem(img.shape, pp.PatchSpec((6, 6)), gb.Hyperparams(num_atoms=k), seed=5, epochs_per_frame=3,
+                         freeze_dict=True, rng=rng) as lp:
+            rec = lp.submit_frame(img, mask).reconstruction
+            atoms, _, _ = lp.dictionary()
+        assert np.abs(atoms - want_atoms).max() <= 1e-6, rng   # data-seeded and frozen
+        if rng == "numpy":
+            assert np.abs(rec - orec).max() <= 1e-3

@@ -1,0 +1,69 @@
+"""End-to-end reconstruction quality against the reference on identical inputs
+(north_star correctness check 3; SURVEY §8c "PSNR within a stated ±0.1 dB, SSIM
+within ±0.002").
+
+The reference's PSNR / SSIM come from tests/golden/quality.json, produced by
+running patchbeam itself on the same frames, masks and seeds
+(tests/golden/make_quality.py; cases in tests/golden/quality_cases.py):
+
+* replay mode (the reference's own draw streams, free-running): the device run
+  of seed 0 must land within ±0.05 dB PSNR / ±0.001 SSIM of the reference's
+  seed-0 run — configs[0] in full through the Python API, configs[2] (3 live
+  512x512 frames) through the NATIVE problem (pb_problem_submit_frame), and the
+  configs[1] crop;
+* Philox mode (device draws — a different random stream of the same sampler):
+  the mean over seeds 0, 1, 2 (and frames) must lie within ±0.1 dB PSNR /
+  ±0.002 SSIM of the reference's mean over the same seeds.
+"""
+
+import json
+import os
+import sys
+
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.join(HERE, "golden"))
+
+from quality_cases import SEEDS, reference_summary, run_device  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+TOL_REPLAY_PSNR, TOL_REPLAY_SSIM = 0.05, 0.001
+TOL_MEAN_PSNR, TOL_MEAN_SSIM = 0.1, 0.002
+
+
+@pytest.fixture(scope="module")
+def qref():
+    return json.load(open(os.path.join(HERE, "golden", "quality.json")))
+
+
+@pytest.mark.parametrize("name", ["cfg0", "cfg2", "cfg1crop"])
+def test_replay_quality_matches_reference_seed0(qref, cuda_device, name):
+    p_ref, s_ref = reference_summary(qref, name)
+    got = np.array(run_device(name, SEEDS[0], rng="numpy"))
+    print(name, "replay psnr", got[:, 0], "ref", p_ref[0], "ssim", got[:, 1], "ref", s_ref[0])
+    assert np.abs(got[:, 0] - p_ref[0]).max() <= TOL_REPLAY_PSNR
+    assert np.abs(got[:, 1] - s_ref[0]).max() <= TOL_REPLAY_SSIM
+
+
+@pytest.mark.parametrize("name", ["cfg0", "cfg2", "cfg1crop"])
+def test_philox_quality_mean_over_seeds_matches_reference(qref, cuda_device, name):
+    p_ref, s_ref = reference_summary(qref, name)
+    got = np.array([run_device(name, s, rng="philox") for s in SEEDS])   # (seeds, frames, 2)
+    print(name, "philox psnr", got[..., 0].mean(), "ref", p_ref.mean(), "ssim", got[..., 1].mean(), "ref",
+          s_ref.mean())
+    assert abs(got[..., 0].mean() - p_ref.mean()) <= TOL_MEAN_PSNR
+    assert abs(got[..., 1].mean() - s_ref.mean()) <= TOL_MEAN_SSIM
+
+
+def test_replay_reconstruction_configs0_matches_reference(cuda_device):
+    """The seed-0 configs[0] reconstruction itself (data consistency on), free-running
+    replay over all 10 epochs: max |difference| small (f32 vs f64 arithmetic;
+    a rare near-tie Z flip moves a few pixels)."""
+    ref = np.load(os.path.join(HERE, "golden", "quality_cfg0_s0.npz"))["recon"]
+    _, recs = run_device("cfg0", 0, rng="numpy", return_recon=True)
+    d = np.abs(recs[0] - ref)
+    print("cfg0 replay recon: max", d.max(), "p99.9", np.quantile(d, 0.999))
+    assert np.quantile(d, 0.999) <= 1e-3
