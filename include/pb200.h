@@ -131,7 +131,8 @@ typedef struct pb_patch_index {
   void* buffer;     /* device buffer of pb_index_bytes(n, p, nnz) bytes */
   int32_t split_count;  /* set by pb_build_index: the code step runs patches with more
                            observed elements in a second, wider launch (0 = one launch) */
-  int32_t reserved;
+  int32_t split_request; /* input: 0 = automatic split choice (cost model), > 0 forces this
+                           threshold (when below cmax), < 0 never splits */
   int64_t n_outliers;   /* patches above split_count */
 } pb_patch_index;
 

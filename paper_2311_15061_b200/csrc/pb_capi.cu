@@ -417,10 +417,11 @@ int pb_build_index(pb_patch_index* pi, const uint8_t* observed, const float* val
   PB_CUDA_TRY(cudaMemcpyAsync(hist.data(), ix.hist, (size_t)(pi->p + 1) * 4, cudaMemcpyDeviceToHost, st));
   PB_CUDA_TRY(cudaStreamSynchronize(st));
   pi->cmax = cmax;
-  pi->split_count = PB_TUNE_FLAG("PB_CODE_SPLIT_OFF") ? 0 : code_split_choose(hist.data(), pi->p, cmax);
-  if (const int t = PB_TUNE_INT("PB_CODE_SPLIT_AT", 0))  // experiments: force the split threshold
-    pi->split_count = (t > 0 && t < cmax) ? t : 0;
-  pi->reserved = 0;
+  const int req = pi->split_request != 0 ? pi->split_request
+                  : PB_TUNE_FLAG("PB_CODE_SPLIT_OFF") ? -1 : PB_TUNE_INT("PB_CODE_SPLIT_AT", 0);
+  if (req > 0) pi->split_count = req < cmax ? req : 0;   // forced threshold
+  else if (req < 0) pi->split_count = 0;                 // never split
+  else pi->split_count = code_split_choose(hist.data(), pi->p, cmax);
   pi->n_outliers = 0;
   if (pi->split_count > 0) {
     if ((rc = launch_outliers(ix, counts, pi->split_count, st))) return rc;

@@ -125,6 +125,9 @@ class PatchMatrix:
     mean_subtracted: bool = False
     n_obs: int = 0
     _cache: dict = field(default_factory=dict, repr=False)
+    # code-step split of the observed-element index (pb_patch_index.split_request):
+    # 0 automatic, > 0 forced threshold, < 0 never
+    split_request: int = 0
 
     @property
     def num_patches(self):
@@ -169,6 +172,7 @@ class PatchMatrix:
             n, p = self.num_patches, self.patch_size
             nb = int(_lib.load().pb_index_bytes(n, p, self.n_obs))
             ix = _lib.PatchIndex(n, p, 0, self.n_obs, 0, None)
+            ix.split_request = int(self.split_request)
             buf = torch.empty((max(nb, 1),), dtype=torch.uint8, device=self.values_pn.device)
             ix.buffer = buf.data_ptr()
             _lib.call("pb_build_index", ctypes.byref(ix), _ptr(self.observed_pn), _ptr(self.values_pn),

@@ -9,7 +9,7 @@ replay, the reference's draw streams) or the reference's stated behaviour:
 * a fully observed frame: replay parity;
 * the split code step (a narrow launch for most patches and, concurrently on
   a side stream, a wide launch over the listed outlier patches), forced via
-  PB_CODE_SPLIT_AT with many and with few outliers: replay parity.
+  pb_patch_index.split_request with many and with few outliers: replay parity.
 """
 
 import numpy as np
@@ -26,8 +26,12 @@ from test_gpu_sweep import _compare_epoch, _pm_pair, _upload
 pytestmark = pytest.mark.gpu
 
 
-def _replay(img, mask, patch, ms, k, seed, epochs):
+def _replay(img, mask, patch, ms, k, seed, epochs, split=0):
     pm, opm = _pm_pair(img, mask, patch, ms)
+    if split:   # force the split code step (pb_patch_index.split_request)
+        pm.split_request = split
+        ix = pm.index()
+        assert ix.split_count == split and ix.n_outliers > 0
     hp = gb.Hyperparams(num_atoms=k)
     st = ob.init_state(opm, ob.Hyper(num_atoms=k), seed, init_mode="prior")
     n = opm.values.shape[0]
@@ -71,15 +75,11 @@ def test_empty_mask_sweep(cuda_device):
 
 
 @pytest.mark.parametrize("split", [8, 16])
-def test_split_code_step_replay(cuda_device, monkeypatch, split):
-    monkeypatch.setenv("PB_CODE_SPLIT_AT", str(split))
+def test_split_code_step_replay(cuda_device, split):
     rng = np.random.default_rng(15)
     img = rng.random((40, 41))
     mask = rng.random(img.shape) < 0.3   # 6x6 patches: ~11 observed, max ~20
-    pm, _ = _pm_pair(img, mask, (6, 6), True)
-    ix = pm.index()
-    assert ix.split_count == split and ix.n_outliers > 0
-    assert _replay(img, mask, (6, 6), True, 10, 3, 2) <= 4
+    assert _replay(img, mask, (6, 6), True, 10, 3, 2, split=split) <= 4
 
 
 def test_chunked_dictionary_staging_replay(cuda_device):
