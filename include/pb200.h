@@ -252,6 +252,21 @@ int pb_atlas_shape(int32_t k, int32_t rank, const int32_t* patch_shape, int64_t*
 int pb_render_atlas(const float* atoms, const double* pi, int32_t k, int32_t rank, const int32_t* patch_shape,
                     double* canvas, uint8_t* canvas_u8, void* stream);
 
+/* ---- entry-point steps (cli.py / bpfa.py) on device ---- */
+/* cli.py:195-212 _normalize_observed: frame (f64, M) -> out (f64, M, may alias
+ * frame) mapped to [0, 1] from the observed values only (mask uint8); identity
+ * when they already lie in [0, 1] or none is observed; a constant observed set
+ * maps observed elements to 0.  scale_out / offset_out (host) as the reference
+ * returns them.  Synchronizes `stream`. */
+int pb_normalize_observed(const double* frame, const uint8_t* mask, int64_t m, double* out, double* scale_out,
+                          double* offset_out, void* stream);
+/* bpfa.py:417-458 transfer_dictionary tiling: dst (K, src_p*repeat) f32 where each
+ * source element is repeated `repeat` = prod(extra trailing patch dims) times,
+ * renormalized to unit norm when `normalize` (zero atoms stay zero); normalize = 0
+ * with repeat = 1 copies bitwise (equal patch shapes).  Device pointers. */
+int pb_transfer_atoms(const float* src, int32_t k, int32_t src_p, int32_t repeat, int32_t normalize, float* dst,
+                      void* stream);
+
 /* ---- stateful problem (C-ABI with HOST buffers; the live submit_frame slice,
  *      pipeline.py:217-251).  Owns all device buffers. ---- */
 typedef struct pb_problem pb_problem;
@@ -323,12 +338,21 @@ int pb_problem_residual_map(pb_problem* pr, double* host_out);
 int pb_problem_adaptive_mask(pb_problem* pr, double ratio, double exploit_fraction, uint64_t seed,
                              int64_t frame_index, uint8_t* mask_host, int32_t* status_out);
 /* Adopt a dictionary (Pipeline._install_dictionary, pipeline.py:145-167): atoms
- * (K,P) f32 and pi (K) of THIS problem's K and P (reshape first with
- * bpfa.transfer_dictionary).  Before the first frame it is pending and seeds the
- * cold start (install_dictionary semantics, bpfa.py:355-376: precisions at the
- * prior means); afterwards it replaces the dictionary and keeps the precisions
- * and the epoch counter.  freeze: 0/1 sets freeze_dict, -1 keeps it. */
-int pb_problem_install_dictionary(pb_problem* pr, const float* atoms_host, const double* pi_host, int32_t freeze);
+ * (K,P) f32 and pi (K) host arrays of THIS problem's P (reshape first with
+ * bpfa.transfer_dictionary / pb_transfer_atoms) and any atom count K (the
+ * problem's K-dependent buffers are re-sized).  Before the first frame it is
+ * pending and seeds the cold start (install_dictionary semantics,
+ * bpfa.py:355-376: precisions at the prior means); afterwards it replaces the
+ * dictionary and keeps the precisions and the epoch counter.  freeze: 0/1 sets
+ * freeze_dict, -1 keeps it. */
+int pb_problem_install_dictionary(pb_problem* pr, const float* atoms_host, const double* pi_host, int32_t k,
+                                  int32_t freeze);
+/* Pipeline.transfer_between (pipeline.py:294-304) on the device: src's current
+ * dictionary (or its pending install) reshaped for dst by the transfer_dictionary
+ * rules (bpfa.py:417-458, pb_transfer_atoms) and installed into dst as above.
+ * PB_EVALUE for src == dst or a source without state; PB_ESHAPE for
+ * incompatible patch shapes. */
+int pb_problem_transfer_dictionary(pb_problem* src, pb_problem* dst, int32_t freeze);
 /* The problem's current dictionary atlas as a uint8 wire panel (host buffer of
  * pb_atlas_shape's size). */
 int pb_problem_render_atlas(pb_problem* pr, uint8_t* canvas_u8_host);

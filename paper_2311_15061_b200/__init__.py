@@ -18,7 +18,8 @@ from .bpfa import (  # noqa: F401
     install_dictionary,
     transfer_dictionary,
 )
-from .live import LiveFrame, LiveProblem, adaptive_mask  # noqa: F401
+from .entry import inpaint, learn, normalize_observed  # noqa: F401
+from .live import LiveFrame, LiveProblem, adaptive_mask, transfer_between  # noqa: F401
 from .patches import (  # noqa: F401
     CoverageError,
     PatchMatrix,

@@ -115,7 +115,10 @@ SIGNATURES = {
                                          ctypes.POINTER(c_i32)]),
     "pb_adaptive_mask": (c_i32, [c_vp, c_i64, ctypes.c_double, ctypes.c_double, ctypes.c_uint64, c_i64, c_vp,
                                  ctypes.POINTER(c_i32), c_vp]),
-    "pb_problem_install_dictionary": (c_i32, [c_vp, c_vp, c_vp, c_i32]),
+    "pb_problem_install_dictionary": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32]),
+    "pb_problem_transfer_dictionary": (c_i32, [c_vp, c_vp, c_i32]),
+    "pb_normalize_observed": (c_i32, [c_vp, c_vp, c_i64, c_vp, ctypes.POINTER(c_f64), ctypes.POINTER(c_f64), c_vp]),
+    "pb_transfer_atoms": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp]),
     "pb_problem_render_atlas": (c_i32, [c_vp, c_vp]),
     "pb_atlas_shape": (c_i32, [c_i32, c_i32, c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
     "pb_render_atlas": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),

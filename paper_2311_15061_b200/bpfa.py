@@ -412,29 +412,41 @@ def infer(pm: PatchMatrix, hp: Hyperparams, epochs: int, seed: int, freeze_dict:
 
 
 def transfer_dictionary(src: Dictionary, dst_patch_shape, dst_tensor_shape=None) -> Dictionary:
-    """bpfa.py:417-458 (host-side reshaping; out of the hot path)."""
-    src = src.to_host()
+    """bpfa.py:417-458: re-shape a dictionary for a destination problem.
+
+    Equal patch shapes copy the atoms bitwise; a destination patch shape that
+    extends the source's with extra trailing dimensions (which must span the
+    destination tensor) re-uses each source atom across every slice of them,
+    tiled and renormalized — on the device (pb_transfer_atoms).  Host atoms give
+    a host (f64) dictionary, device atoms a device (f32) one."""
     dst = tuple(int(b) for b in dst_patch_shape)
     sshape = tuple(src.patch_shape)
-    if dst == sshape:
-        return src.copy()
     ds, dd = len(sshape), len(dst)
-    if dd <= ds or dst[:ds] != sshape:
-        raise ShapeError(f"cannot transfer atoms of shape {sshape} to patch shape {dst}")
-    extra = dst[ds:]
-    if dst_tensor_shape is not None:
-        if len(dst_tensor_shape) != dd:
-            raise ShapeError("destination tensor rank does not match its patch shape")
-        for i, b in enumerate(extra, start=ds):
-            if b != dst_tensor_shape[i]:
-                raise ShapeError(f"transfer dimension {i} must span the destination tensor")
-    k = src.num_atoms
-    tiled = np.broadcast_to(src.atoms.reshape((k,) + sshape + (1,) * len(extra)),
-                            (k,) + sshape + extra).reshape(k, -1).copy()
-    norms = np.sqrt((tiled * tiled).sum(axis=1))
-    ok = norms > 0
-    tiled[ok] /= norms[ok, None]
-    return Dictionary(tiled, src.pi.copy(), dst)
+    repeat, normalize = 1, 0
+    if dst != sshape:
+        if dd <= ds or dst[:ds] != sshape:
+            raise ShapeError(f"cannot transfer atoms of shape {sshape} to patch shape {dst}")
+        extra = dst[ds:]
+        if dst_tensor_shape is not None:
+            if len(dst_tensor_shape) != dd:
+                raise ShapeError("destination tensor rank does not match its patch shape")
+            for i, b in enumerate(extra, start=ds):
+                if b != dst_tensor_shape[i]:
+                    raise ShapeError(f"transfer dimension {i} must span the destination tensor "
+                                     f"({b} != {dst_tensor_shape[i]})")
+        repeat, normalize = int(np.prod(extra)), 1
+    on_dev = isinstance(src.atoms, torch.Tensor)
+    if not normalize:
+        return src.copy()
+    a = src.atoms if on_dev else torch.as_tensor(np.asarray(src.atoms, dtype=np.float32))
+    a = a.to(device="cuda", dtype=torch.float32).contiguous()
+    k, sp = a.shape
+    out = torch.empty((k, sp * repeat), dtype=torch.float32, device=a.device)
+    _lib.call("pb_transfer_atoms", _ptr(a), k, sp, repeat, normalize, _ptr(out), _stream())
+    if on_dev:
+        pi = src.pi.clone() if isinstance(src.pi, torch.Tensor) else torch.as_tensor(np.asarray(src.pi), device="cuda")
+        return Dictionary(out, pi, dst)
+    return Dictionary(out.double().cpu().numpy(), np.array(src.pi, dtype=np.float64, copy=True), dst)
 
 
 # --- posterior helpers (bpfa.py:189-235), via the fine-grained seam kernels ----

@@ -15,6 +15,10 @@
 #include "pb_compose_tc.cuh"
 
 namespace pb {
+int launch_transfer_atoms(const float* src, int k, int src_p, int repeat, int normalize, float* dst, cudaStream_t st);
+}
+
+namespace pb {
 
 // ---- error state ----------------------------------------------------------
 static thread_local char g_err[1024] = "";
@@ -764,6 +768,13 @@ int pb_problem_submit_frame_ex(pb_problem* pr, const double* frame_host, const u
       PB_CUDA_TRY(cudaMalloc(&pr->index.buffer, ixb));
       pr->ix_cap = ixb;
     }
+    pr->index.n = n; pr->index.p = pr->p; pr->index.nnz = pr->n_obs;
+    if ((rc = pb_build_index(&pr->index, pr->obs, pr->values, pr->counts, st))) return rc;
+    pr->index_valid = true;
+  } else {
+    if ((rc = pb_index_refresh_values(&pr->index, pr->values, pr->counts, st))) return rc;
+  }
+  {  // epoch workspace for this mask's observed count and the current K
     const size_t wsb = pb_epoch_workspace_bytes(n, pr->p, pr->k, pr->n_obs);
     if (wsb > pr->ws_cap) {
       if (pr->ws) cudaFree(pr->ws);
@@ -771,11 +782,6 @@ int pb_problem_submit_frame_ex(pb_problem* pr, const double* frame_host, const u
       PB_CUDA_TRY(cudaMalloc(&pr->ws, wsb));
       pr->ws_cap = wsb;
     }
-    pr->index.n = n; pr->index.p = pr->p; pr->index.nnz = pr->n_obs;
-    if ((rc = pb_build_index(&pr->index, pr->obs, pr->values, pr->counts, st))) return rc;
-    pr->index_valid = true;
-  } else {
-    if ((rc = pb_index_refresh_values(&pr->index, pr->values, pr->counts, st))) return rc;
   }
   if (!pr->have_state || !pr->desc.warm_start) {
     if ((rc = problem_cold_init(pr))) return rc;
@@ -874,8 +880,52 @@ int pb_problem_render_atlas(pb_problem* pr, uint8_t* canvas_u8_host) {
   return rc;
 }
 
-int pb_problem_install_dictionary(pb_problem* pr, const float* atoms_host, const double* pi_host, int32_t freeze) {
+// Re-size every K-dependent buffer of a problem (a dictionary with another atom
+// count was installed: Pipeline._install_dictionary rebuilds the state with
+// moved.num_atoms, pipeline.py:158-167).  Codes are reset each frame anyway.
+static int problem_set_k(pb_problem* pr, int k) {
+  if (k == pr->k) return PB_OK;
+  if (k < 1) { set_error("num_atoms must be >= 1"); return PB_EVALUE; }
+  PB_CUDA_TRY(cudaStreamSynchronize(pr->stream));
+  void* dev[] = {pr->atoms, pr->pi, pr->usage, pr->weights, pr->m_count, pr->bpack, pr->ws,
+                 pr->d_atom, pr->d_u, pr->d_g};
+  for (void* b : dev)
+    if (b) cudaFree(b);
+  void* host[] = {pr->h_atom, pr->h_u, pr->h_g, pr->h_pi, pr->h_m};
+  for (void* b : host)
+    if (b) cudaFreeHost(b);
+  pr->atoms = nullptr; pr->pi = nullptr; pr->usage = nullptr; pr->weights = nullptr; pr->m_count = nullptr;
+  pr->bpack = nullptr; pr->ws = nullptr; pr->ws_cap = 0;
+  pr->d_atom = pr->d_u = pr->d_g = nullptr;
+  pr->h_atom = pr->h_u = pr->h_g = pr->h_pi = nullptr;
+  pr->h_m = nullptr;
+  pr->k = k;
+  pr->desc.num_atoms = k;
+  const int64_t n = pr->n, p = pr->p, ld = pr->ld;
+  int rc = PB_OK;
+#define PB_R(ptr, cnt) if ((rc = dalloc(&pr->ptr, (size_t)(cnt)))) return rc;
+  PB_R(atoms, (int64_t)k * p) PB_R(pi, k) PB_R(usage, (int64_t)k * ld) PB_R(weights, (int64_t)k * ld) PB_R(m_count, k)
+  if (compose_tc_supported((int)p) && !PB_TUNE_FLAG("PB_COMPOSE_TC_OFF")) PB_R(bpack, compose_tc_scratch_bytes((int)p, k) / 4)
+  if (pr->desc.replay) {
+    PB_R(d_atom, (int64_t)k * p) PB_R(d_u, (int64_t)k * n) PB_R(d_g, (int64_t)k * n)
+    if (cudaMallocHost((void**)&pr->h_atom, (size_t)k * p * 8) != cudaSuccess ||
+        cudaMallocHost((void**)&pr->h_u, (size_t)k * n * 8) != cudaSuccess ||
+        cudaMallocHost((void**)&pr->h_g, (size_t)k * n * 8) != cudaSuccess ||
+        cudaMallocHost((void**)&pr->h_pi, (size_t)k * 8) != cudaSuccess ||
+        cudaMallocHost((void**)&pr->h_m, (size_t)k * 4) != cudaSuccess) {
+      set_error("pinned replay buffers: allocation failed");
+      return PB_ECUDA;
+    }
+  }
+#undef PB_R
+  return PB_OK;
+}
+
+int pb_problem_install_dictionary(pb_problem* pr, const float* atoms_host, const double* pi_host, int32_t k,
+                                  int32_t freeze) {
   if (!pr || !atoms_host || !pi_host) { set_error("null argument"); return PB_EVALUE; }
+  int rc = problem_set_k(pr, k);
+  if (rc) return rc;
   if (freeze == 0 || freeze == 1) pr->desc.freeze_dict = freeze;
   const size_t kp = (size_t)pr->k * pr->p;
   if (!pr->have_state) {  // pending until the first frame (pipeline.py:155-157)
@@ -889,6 +939,71 @@ int pb_problem_install_dictionary(pb_problem* pr, const float* atoms_host, const
   PB_CUDA_TRY(cudaMemcpyAsync(pr->pi, pi_host, (size_t)pr->k * 8, cudaMemcpyHostToDevice, pr->stream));
   PB_CUDA_TRY(cudaStreamSynchronize(pr->stream));  // host buffers may be released on return
   return PB_OK;
+}
+
+int pb_problem_transfer_dictionary(pb_problem* src, pb_problem* dst, int32_t freeze) {
+  if (!src || !dst) { set_error("null argument"); return PB_EVALUE; }
+  if (src == dst) { set_error("cannot transfer a dictionary onto itself"); return PB_EVALUE; }
+  const bool pending = !src->have_state && !src->pending_atoms.empty();
+  if (!src->have_state && !pending) { set_error("source problem has no trained state yet"); return PB_EVALUE; }
+  // bpfa.transfer_dictionary shape rules (bpfa.py:431-449): equal patch shapes, or the
+  // destination extends the source with trailing dimensions that span its tensor
+  const pb::Grid &gs = src->grid, &gd = dst->grid;
+  int repeat = 1, normalize = 0;
+  bool same = gs.rank == gd.rank;
+  for (int i = 0; same && i < gs.rank; ++i) same = gs.bshape[i] == gd.bshape[i];
+  if (!same) {
+    bool ok = gd.rank > gs.rank;
+    for (int i = 0; ok && i < gs.rank; ++i) ok = gs.bshape[i] == gd.bshape[i];
+    if (!ok) { set_error("cannot transfer atoms between these patch shapes"); return PB_ESHAPE; }
+    for (int i = gs.rank; i < gd.rank; ++i) {
+      if (gd.bshape[i] != gd.tshape[i]) {
+        set_error("transfer dimension %d must span the destination tensor (%d != %lld)", i, gd.bshape[i],
+                  (long long)gd.tshape[i]);
+        return PB_ESHAPE;
+      }
+      repeat *= gd.bshape[i];
+    }
+    normalize = 1;
+  }
+  const int k = src->k, ps = src->p;
+  int rc = problem_set_k(dst, k);
+  if (rc) return rc;
+  if (freeze == 0 || freeze == 1) dst->desc.freeze_dict = freeze;
+  cudaStream_t st = dst->stream;
+  float* tmp_src = nullptr;
+  const float* s_atoms = src->atoms;
+  std::vector<double> pi_h;
+  if (pending) {  // the source's dictionary is still a pending install (host copies)
+    PB_CUDA_TRY(cudaMallocAsync((void**)&tmp_src, (size_t)k * ps * 4, st));
+    PB_CUDA_TRY(cudaMemcpyAsync(tmp_src, src->pending_atoms.data(), (size_t)k * ps * 4, cudaMemcpyHostToDevice, st));
+    s_atoms = tmp_src;
+    pi_h = src->pending_pi;
+  } else {
+    PB_CUDA_TRY(cudaStreamSynchronize(src->stream));   // the source's sweeps are done (snapshot)
+  }
+  float* out = dst->atoms;
+  if (!dst->have_state) PB_CUDA_TRY(cudaMallocAsync((void**)&out, (size_t)k * dst->p * 4, st));
+  rc = launch_transfer_atoms(s_atoms, k, ps, repeat, normalize, out, st);
+  if (!rc && !dst->have_state) {  // pending until the destination's first frame (pipeline.py:155-157)
+    dst->pending_atoms.resize((size_t)k * dst->p);
+    dst->pending_pi.resize(k);
+    if (cudaMemcpyAsync(dst->pending_atoms.data(), out, (size_t)k * dst->p * 4, cudaMemcpyDeviceToHost, st) ||
+        (pending ? false : cudaMemcpyAsync(dst->pending_pi.data(), src->pi, (size_t)k * 8, cudaMemcpyDeviceToHost, st)))
+      { set_error("transfer copy failed"); rc = PB_ECUDA; }
+    if (pending) dst->pending_pi = pi_h;
+  } else if (!rc) {  // replace the dictionary; precisions and epoch carry over (pipeline.py:158-167)
+    if (pending) {
+      if (cudaMemcpyAsync(dst->pi, pi_h.data(), (size_t)k * 8, cudaMemcpyHostToDevice, st)) rc = PB_ECUDA;
+    } else if (cudaMemcpyAsync(dst->pi, src->pi, (size_t)k * 8, cudaMemcpyDeviceToDevice, st)) {
+      rc = PB_ECUDA;
+    }
+    if (rc) set_error("transfer copy failed");
+  }
+  if (tmp_src) cudaFreeAsync(tmp_src, st);
+  if (!dst->have_state && out) cudaFreeAsync(out, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess && !rc) { set_error("transfer failed"); rc = PB_ECUDA; }
+  return rc;
 }
 
 int pb_problem_residual_map(pb_problem* pr, double* host_out) {

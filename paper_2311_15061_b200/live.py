@@ -138,14 +138,19 @@ class LiveProblem:
     def install_dictionary(self, dictionary, freeze: bool | None = None) -> None:
         """Pipeline._install_dictionary (pipeline.py:145-167): the dictionary is
         reshaped to this problem's patch shape (bpfa.transfer_dictionary,
-        bpfa.py:417-458); codes reset; pending until the first frame."""
+        bpfa.py:417-458, on device); codes reset; any atom count (the problem's
+        K-dependent buffers are re-sized); pending until the first frame."""
         moved = transfer_dictionary(dictionary, self.patch_shape, self.shape)
-        if moved.num_atoms != self.num_atoms:
-            raise ShapeError(f"dictionary has {moved.num_atoms} atoms, the problem {self.num_atoms}")
-        atoms = np.ascontiguousarray(np.asarray(moved.atoms, dtype=np.float32))
-        pi = np.ascontiguousarray(np.asarray(moved.pi, dtype=np.float64))
+        atoms = np.ascontiguousarray(_host(moved.atoms, np.float32))
+        pi = np.ascontiguousarray(_host(moved.pi, np.float64))
         _lib.check(self._lib.pb_problem_install_dictionary(self._h, atoms.ctypes.data, pi.ctypes.data,
-                                                           -1 if freeze is None else int(bool(freeze))), _VALUE)
+                                                           atoms.shape[0], -1 if freeze is None else int(bool(freeze))),
+                   _VALUE)
+        self.num_atoms = atoms.shape[0]
+
+    def transfer_from(self, src: "LiveProblem", freeze: bool = False) -> None:
+        """Pipeline.transfer_between(src, self) (pipeline.py:294-304), device to device."""
+        transfer_between(src, self, freeze)
 
     def snapshot_dictionary(self) -> Dictionary:
         """Pipeline.snapshot_dictionary (pipeline.py:280-286), on the host."""
@@ -166,6 +171,21 @@ class LiveProblem:
         sc = _lib.Scalars()
         _lib.check(self._lib.pb_problem_get_dictionary(self._h, atoms.ctypes.data, pi.ctypes.data, ctypes.byref(sc)))
         return atoms, pi, sc
+
+
+def _host(x, dtype):
+    import torch
+
+    return (x.detach().cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)).astype(dtype)
+
+
+def transfer_between(src: LiveProblem, dst: LiveProblem, freeze: bool = False) -> None:
+    """Pipeline.transfer_between (pipeline.py:294-304): install src's current
+    dictionary into dst (reshaped by the transfer_dictionary rules on the device;
+    dst codes reset; dst keeps its precisions and epoch counter)."""
+    _lib.check(_lib.load().pb_problem_transfer_dictionary(src._h, dst._h, int(bool(freeze))),
+               {_lib.PB_EVALUE: ValueError, _lib.PB_ESHAPE: ShapeError})
+    dst.num_atoms = src.num_atoms
 
 
 def spec_n(spec: PatchSpec, shape):

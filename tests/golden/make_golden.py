@@ -283,6 +283,61 @@ def atlases(pb):
     np.savez_compressed(os.path.join(OUT, "atlas.npz"), **out)
 
 
+def entry_cases(pb):
+    """The CLI entry flows' steps (cli.py): _normalize_observed cases, an inpaint
+    of an out-of-range frame (cmd_inpaint's steps), a learn over two images
+    (cmd_learn's steps), and a transfer_dictionary onto an extended patch shape."""
+    from patchbeam import bpfa
+    from patchbeam.cli import _normalize_observed
+    from patchbeam.patches import PatchMatrix, PatchSpec, apply_data_consistency, extract_patches, reconstitute
+    from patchbeam.sampling import SamplerSpec, make_mask
+
+    rng = np.random.default_rng(606)
+    out = {}
+    frames = [rng.random((9, 11)),                                   # already in [0, 1]: identity
+              rng.random((9, 11)) * 7.0 - 2.0,                       # affine
+              np.full((9, 11), 3.5),                                 # constant observed values
+              rng.random((9, 11)) * 4.0 + 1.0]                       # mask empty -> identity
+    masks = [rng.random((9, 11)) < 0.4, rng.random((9, 11)) < 0.4, rng.random((9, 11)) < 0.4,
+             np.zeros((9, 11), bool)]
+    frames[1][~masks[1]] = 1e6                                       # unobserved garbage must not matter
+    for i, (f, m) in enumerate(zip(frames, masks)):
+        g, sc, off = _normalize_observed(f, m)
+        out[f"n{i}_frame"], out[f"n{i}_mask"], out[f"n{i}_out"] = f, m, g
+        out[f"n{i}_scale_offset"] = np.array([sc, off])
+    # inpaint (cli.py:247-274): normalize -> extract (mean-sub) -> infer -> OLA -> DC
+    img = rng.random((30, 28)) * 5.0 + 10.0
+    mask = make_mask(SamplerSpec(kind="uniform-random", ratio=0.3, seed=3), img.shape)
+    f, sc, off = _normalize_observed(img, mask)
+    pm = extract_patches(f, mask, PatchSpec((5, 5)), mean_subtract=True)
+    st, est = bpfa.infer(pm, bpfa.Hyperparams(num_atoms=12), epochs=3, seed=4)
+    rec = apply_data_consistency(reconstitute(pm, est), f, mask, True)
+    out.update(inp_img=img, inp_mask=mask, inp_recon=rec, inp_scale_offset=np.array([sc, off]),
+               inp_atoms=st.dictionary.atoms)
+    # learn (cli.py:342-386): masks keyed by seed + i, concatenated patch matrices, infer
+    imgs = [rng.random((20, 22)), rng.random((18, 25))]
+    seed, ratio = 5, 0.35
+    parts = []
+    for i, im in enumerate(imgs):
+        mk = make_mask(SamplerSpec(ratio=ratio, seed=seed + i), im.shape)
+        parts.append(extract_patches(im, mk, PatchSpec((4, 4)), mean_subtract=True))
+    cat = PatchMatrix(values=np.concatenate([q.values for q in parts]),
+                      observed=np.concatenate([q.observed for q in parts]),
+                      origins=np.concatenate([q.origins for q in parts]),
+                      means=np.concatenate([q.means for q in parts]),
+                      tensor_shape=parts[0].tensor_shape, spec=PatchSpec((4, 4)), mean_subtracted=True)
+    st, _ = bpfa.infer(cat, bpfa.Hyperparams(num_atoms=7), epochs=3, seed=seed)
+    out.update(learn_img0=imgs[0], learn_img1=imgs[1], learn_atoms=st.dictionary.atoms, learn_pi=st.dictionary.pi,
+               learn_n=np.asarray(cat.num_patches))
+    # transfer_dictionary onto an extended patch shape (bpfa.py:417-458)
+    src = bpfa.Dictionary(rng.standard_normal((5, 12)).astype(np.float32).astype(np.float64),
+                          rng.uniform(0, 1, 5), (3, 4))
+    src.atoms[2] = 0.0
+    moved = bpfa.transfer_dictionary(src, (3, 4, 3), (10, 12, 3))
+    out.update(tr_src=src.atoms, tr_pi=src.pi, tr_out=moved.atoms)
+    np.savez_compressed(os.path.join(OUT, "entry.npz"), **out)
+
+
 def main():
     pb = _import_reference()
     import numba
@@ -290,7 +345,7 @@ def main():
     only = sys.argv[1:]
     for name, fn in (("extract", extraction_cases), ("traj", trajectories), ("masks", masks), ("live", live),
                      ("posterior", posterior), ("live_tail", live_tail), ("dicts", dict_files),
-                     ("atlas", atlases)):
+                     ("atlas", atlases), ("entry", entry_cases)):
         if not only or name in only:
             fn(pb)
     meta = {"python": platform.python_version(), "numpy": np.__version__,

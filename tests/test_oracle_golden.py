@@ -148,3 +148,13 @@ def test_live_pipeline_sequence_bit_exact(golden):
         st, est = ob.infer(pm, hp, 2, 0, state=st)
         assert np.array_equal(op.reconstitute(pm, est), g[f"f{t}_recon"]), t
         assert np.array_equal(st.atoms, g[f"f{t}_atoms"]), t
+
+
+def test_oracle_normalize_observed_matches_reference(golden):
+    from oracle.cli import normalize_observed
+
+    g = golden("entry.npz")
+    for i in range(4):
+        out, sc, off = normalize_observed(g[f"n{i}_frame"], g[f"n{i}_mask"])
+        assert np.array_equal(out, g[f"n{i}_out"]), i
+        assert (sc, off) == tuple(g[f"n{i}_scale_offset"]), i
