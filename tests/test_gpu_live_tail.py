@@ -19,7 +19,7 @@ from paper_2311_15061_b200 import _lib
 from paper_2311_15061_b200 import inputs
 from paper_2311_15061_b200.bpfa import Hyperparams
 from paper_2311_15061_b200.live import LiveProblem, adaptive_mask
-from paper_2311_15061_b200.patches import PatchSpec
+from paper_2311_15061_b200.patches import PatchSpec, ShapeError
 
 pytestmark = pytest.mark.gpu
 
@@ -135,8 +135,10 @@ def test_install_dictionary_pending_and_live(cuda_device, tmp_path):
         lp.submit_frame(frames[1], mask)
         atoms2, _, sc2 = lp.dictionary()
         assert sc2.epoch == 4 and not np.array_equal(atoms2, atoms)
-        with pytest.raises(Exception):
-            lp.install_dictionary(Dictionary(np.zeros((5, 36)), np.full(5, 0.5), (6, 6)))
+        lp.install_dictionary(Dictionary(np.zeros((5, 36)), np.full(5, 0.5), (6, 6)))   # another K: re-sized
+        assert lp.num_atoms == 5 and lp.dictionary()[0].shape == (5, 36)
+        with pytest.raises(ShapeError):
+            lp.install_dictionary(Dictionary(np.zeros((5, 25)), np.full(5, 0.5), (5, 5)))
 
 
 def test_atlas_on_device_matches_reference(golden, cuda_device):
