@@ -134,6 +134,8 @@ typedef struct pb_patch_index {
   int32_t split_request; /* input: 0 = automatic split choice (cost model), > 0 forces this
                            threshold (when below cmax), < 0 never splits */
   int64_t n_outliers;   /* patches above split_count */
+  int64_t nnz_ell;      /* set by pb_build_index: positions of the dictionary step's ELL wave
+                           layout (nnz + padding; the residual workspace holds this many) */
 } pb_patch_index;
 
 size_t pb_index_bytes(int64_t n, int32_t p, int64_t nnz);

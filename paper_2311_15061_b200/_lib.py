@@ -47,7 +47,8 @@ class Scalars(ctypes.Structure):
 
 class PatchIndex(ctypes.Structure):
     _fields_ = [("n", c_i64), ("p", c_i32), ("ntiles", c_i32), ("nnz", c_i64), ("cmax", c_i32),
-                ("buffer", c_vp), ("split_count", c_i32), ("split_request", c_i32), ("n_outliers", c_i64)]
+                ("buffer", c_vp), ("split_count", c_i32), ("split_request", c_i32), ("n_outliers", c_i64),
+                ("nnz_ell", c_i64)]
 
 
 ALLREDUCE_FN = ctypes.CFUNCTYPE(c_i32, c_vp, c_vp, c_i64, c_i32, c_vp)

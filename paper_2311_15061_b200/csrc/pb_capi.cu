@@ -71,7 +71,7 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 static size_t ws_bytes(int64_t n, int p, int k, int64_t nnz, EpochWs* ws, char* base) {
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return base ? base + o : nullptr; };
-  char* r = take((size_t)nnz * 4);
+  char* r = take((size_t)ell_cap(n, nnz) * 4);   // residual in the ELL wave order
   const size_t wtb = (size_t)ceil_div(n, kTile) * ceil_div(k, kWB) * kTile * kWB * 4;
   char* wt = take(wtb);
   char* pa = take(dict_gram_partials_bytes(p, kMaxDictBlocks));
@@ -173,11 +173,13 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
   phase_mark(kPhResid, st);
   int rc = PB_OK;
   if (d->resid_mode == PB_RESID_RECOMPUTE) {
-    rc = launch_resid_compact(c, st);                    // residual_full (bpfa.py:297)
+    // residual_full (bpfa.py:297) on the observed positions; the ELL padding is 0
+    PB_CUDA_TRY(cudaMemsetAsync(ws.r_csc, 0, (size_t)d->index->nnz_ell * 4, st));
+    rc = launch_resid_compact(c, st);
   } else if (d->resid_mode == PB_RESID_FROM_VALUES) {    // Z*S == 0  =>  R = X
     // (the tile-blocked code copy W is not cleared: the prior-draw dictionary
     // step below does not read it and the code step rewrites all of it)
-    if (cudaMemcpyAsync(ws.r_csc, ix.x_csc, (size_t)d->index->nnz * 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
+    if (cudaMemcpyAsync(ws.r_csc, ix.x_csc, (size_t)d->index->nnz_ell * 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
       set_error("residual copy failed");
       rc = PB_ECUDA;
     }
@@ -189,7 +191,8 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
   phase_mark(kPhDict, st);
   if (!d->freeze_dict) {
     DictGramArgs g{};
-    g.tile_base = ix.tile_base; g.colptr = ix.colptr; g.e_loc = ix.e_loc; g.ntiles = ix.ntiles;
+    g.ell_base = ix.ell_base; g.wave_base = ix.wave_base; g.wave_off = ix.wave_off; g.wave_meta = ix.wave_meta;
+    g.wave_col = ix.wave_col; g.e_ell = ix.e_ell; g.ntiles = ix.ntiles;
     g.wt = ws.wt; g.nblk8 = c.nblk8;
     g.r_csc = ws.r_csc; g.usage = d->usage; g.weights = d->weights; g.atoms = d->atoms;
     g.draws = d->rng_mode == PB_RNG_REPLAY ? d->atom_draws : nullptr;
@@ -200,8 +203,6 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
     g.ld = c.ld;
     g.nnz = d->index->nnz;
     g.delta_g = ws.delta_g;   // atom shifts of the last updated block [8][P]
-    g.seg_base = ix.seg_base;
-    g.seg_cost = PB_TUNE_DBL("PB_DICT_SEG_COST", kDictSegCost);
     if (d->resid_mode == PB_RESID_FROM_VALUES) {
       // Z*S == 0: every moment sum is 0 on every rank, the atoms are prior
       // redraws and the residual does not move (the first sweep of a cold
@@ -405,7 +406,10 @@ size_t pb_index_bytes(int64_t n, int32_t p, int64_t nnz) {
 int pb_build_index(pb_patch_index* pi, const uint8_t* observed, const float* values, const int32_t* counts,
                    void* stream) {
   if (!pi || !pi->buffer) { set_error("null index"); return PB_EVALUE; }
-  if (pi->nnz >= (int64_t)1 << 31) { set_error("too many observed elements for 32-bit positions"); return PB_EUNSUPPORTED; }
+  if (ell_cap(pi->n, pi->nnz) >= (int64_t)1 << 32) {
+    set_error("too many observed elements for 32-bit positions");
+    return PB_EUNSUPPORTED;
+  }
   PatchIndex ix;
   index_view(pi, ix);
   pi->ntiles = ix.ntiles;
@@ -419,6 +423,7 @@ int pb_build_index(pb_patch_index* pi, const uint8_t* observed, const float* val
   int32_t cmax = 0;
   PB_CUDA_TRY(cudaMemcpyAsync(&cmax, ix.cmax_dev, 4, cudaMemcpyDeviceToHost, st));
   PB_CUDA_TRY(cudaMemcpyAsync(hist.data(), ix.hist, (size_t)(pi->p + 1) * 4, cudaMemcpyDeviceToHost, st));
+  PB_CUDA_TRY(cudaMemcpyAsync(&pi->nnz_ell, ix.ell_base + ix.ntiles, 8, cudaMemcpyDeviceToHost, st));
   PB_CUDA_TRY(cudaStreamSynchronize(st));
   pi->cmax = cmax;
   const int req = pi->split_request != 0 ? pi->split_request

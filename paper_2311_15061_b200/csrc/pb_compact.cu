@@ -667,7 +667,6 @@ __device__ __forceinline__ uint64_t gtimer() {
 //   registers, and transpose-reduce them at the end of the segment.  Segments
 //   wholly owned by one warp add straight into the CTA accumulator; the (at
 //   most two) boundary segments go to per-warp slots merged in warp order.
-constexpr int kTbCache = 1024;  // tile bases cached in shared memory per CTA
 
 // The B sequential atom draws of one block from the reduced moments (f64):
 //   C_j += sum_{l<j} G_jl o delta_l;  lambda = P + geps*A_j;  mu = geps*(C_j + d_j*A_j)/lambda;
@@ -757,455 +756,517 @@ __device__ __forceinline__ void atom_block_update(const double* red, int p, int 
 }
 
 constexpr double kTileVisitCost = 3000.0;  // element-equivalents of one tile visit (work split)
-constexpr int kDictGroupLanes = 16;  // lanes per segment group in the element phase (8: +3 % at configs[1])
-constexpr int kDictSegLen = 256;   // max elements of one segment (a multiple of the group size)
-static_assert(kDictSegLen == kSegCountLen, "the cost model counts segments of the element phase");
+// Byte stride of one staged W block in shared memory: the tile's kTile x 8
+// floats, then the all-zero row kEllZeroRow that the ELL padding points to.
+constexpr uint32_t kWStride = (uint32_t)kTile * kWB * 4 + 128;
+constexpr int kEllPf = 6;   // elements in flight per lane in the element phase
 
-// NW warps per CTA, NSTAGE staging buffers (2: the next tile is bulk-copied
-// while this one is processed; 1: two CTAs share an SM and cover each other's
-// copy and barrier waits).
-template <int B, int kGroupLanes, int kSegLen, int NW, int NSTAGE>
-__global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) {
-  using L = GramLayout<B>;
-  static_assert(NW * 2 <= 32, "at most one boundary slot per lane");
-  extern __shared__ __align__(16) unsigned char smraw[];
-  const int p = a.p;
-  static_assert(B == kWB, "the tile-blocked code copy W holds blocks of kWB atoms");
-  // [stage][cur|prev][kTile*B] staging of the tile-blocked code copy (async bulk copies),
-  // aliased by red64 in the update phase
-  float* wbuf = (float*)smraw;
-  float* acc = (float*)(smraw + a.wbytes);               // p * NACC
-  float* slots = acc + (size_t)p * L::NACC;              // NW * 2 * NACC
-  int* slot_col = (int*)(slots + NW * 2 * L::NACC);      // NW * 2
-  const int cpp = colptr_pitch(p);
-  int* cps = slot_col + NW * 2;                          // NSTAGE * cpp (tile colptr, bulk-copied)
-  int64_t* tbs = (int64_t*)(cps + NSTAGE * cpp);        // kTbCache tile bases of this CTA
-  float* dold = (float*)(tbs + kTbCache);                // B * p
-  float* dprev = dold + B * p;                           // B * p
-  double* red64 = (double*)smraw;                        // p * NACC (aliases the staging)
-  __shared__ __align__(8) uint64_t mbar[3];   // [0..1] staging stages, [2] owner partials
-  if (threadIdx.x == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
-    mbar_init(&mbar[2], 1);
+// One ELL wave (pb_index.cu) as seen by a lane: its run's column, the wave's
+// run length, log2 of the lanes per column, and the lane's first position.
+struct EllWave {
+  int lw, lg, col;
+  int64_t base;
+};
+
+__device__ __forceinline__ EllWave ell_header(const DictGramArgs& a, int64_t wv, int64_t tile_ell, int lane) {
+  EllWave h;
+  const int meta = a.wave_meta[wv];
+  h.lw = meta & 0xFF;
+  h.lg = meta >> 8;
+  h.col = a.wave_col[wv * 32 + lane];
+  h.base = tile_ell + a.wave_off[wv] + lane;
+  return h;
+}
+
+// the first kEllPf positions of a wave's run in flight
+__device__ __forceinline__ void ell_prefetch(const DictGramArgs& a, const EllWave& h, uint32_t (&ib)[kEllPf],
+                                             float (&rb)[kEllPf], uint64_t pol) {
+#pragma unroll
+  for (int d = 0; d < kEllPf; ++d) {
+    ib[d] = kEllZeroRow;
+    rb[d] = 0.0f;
+    if (d < h.lw) { ib[d] = ldg_hint(a.e_ell + h.base + d * 32, pol); rb[d] = ldg_hint(a.r_csc + h.base + d * 32, pol); }
   }
-  uint32_t pphase = 0;  // parity of mbar[2]
-  unsigned bar_target = 0;  // grid_sync_mono: arrivals expected so far
-  // owner reads: shared memory when staged, else L2 (ld.cg)
-  auto ld_part = [&](const float* q) -> float { return a.pstage_off ? *q : __ldcg(q); };
-  __syncthreads();
-  uint32_t phase_bits = 0;   // parity of each stage's mbarrier
-  uint32_t seq = 0;          // running tile-visit counter -> stage = seq & 1
+}
 
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const double geps = a.sc->gamma_eps;
-  const int epoch = a.sc->epoch + 1;
-  const int nblk = (a.k + B - 1) / B;
-  const int64_t nnz = a.tile_base[a.ntiles];
-  // CTA element ranges balance elements + kTileVisitCost per tile visited (each
-  // visit pays the staging, barriers and boundary merge): boundary c sits where
-  // the prefix cost C(e) = e + kTileVisitCost * (tiles started up to e) reaches
-  // c/G of the total; a boundary falling in a tile's visit cost snaps to the
-  // tile start.  Static and deterministic.
-  // A segment (a column run of <= kSegLen elements) adds a fixed round cost
-  // (transpose reduction, segment carve, first-load latency): kSegCost element
-  // equivalents, spread linearly over the tile's elements.
-  const double seg_cost = a.seg_base ? a.seg_cost : 0.0;
-  auto cost_at = [&](int t) {
-    return (double)a.tile_base[t] + kTileVisitCost * t + (seg_cost > 0.0 ? seg_cost * (double)a.seg_base[t] : 0.0);
+// Element phase of one ELL wave: the lane walks its run of column h.col (stride
+// 32, coalesced), applies the previous block's shifts to the residual and
+// accumulates the block's Gram / moment sums in registers.  Padding positions
+// point at the zero W row and carry r = 0: no per-element tests.
+template <bool HP, bool HC>
+__device__ __forceinline__ void ell_elements(const DictGramArgs& a, const EllWave& h, uint32_t wcur_s, uint32_t wprev_s,
+                                             const float2 (&dl2)[kWB / 2], float (&v)[GramLayout<kWB>::NP],
+                                             uint32_t (&ib)[kEllPf], float (&rb)[kEllPf], uint64_t pol) {
+  using L = GramLayout<kWB>;
+  constexpr int B = kWB;
+  const uint16_t* ep = a.e_ell + h.base;
+  float* rp = a.r_csc + h.base;
+  const int lw = h.lw;
+  for (int j0 = 0; j0 < lw; j0 += kEllPf) {
+#pragma unroll
+    for (int d = 0; d < kEllPf; ++d) {
+      const int j = j0 + d;
+      if (j >= lw) break;
+      const uint32_t il = ib[d];
+      float r = rb[d];
+      if (j + kEllPf < lw) {
+        ib[d] = ldg_hint(ep + (j + kEllPf) * 32, pol);
+        rb[d] = ldg_hint(rp + (j + kEllPf) * 32, pol);
+      }
+      const uint32_t wo[2] = {il, il ^ 16u};
+      if constexpr (HP) {  // r += w_prev . delta  (packed pairs, two independent chains)
+        float2 sh[B / 4];
+#pragma unroll
+        for (int q = 0; q < B / 4; ++q) {
+          const float4 w4 = lds128(wprev_s + wo[q]);
+          sh[q] = __fmul2_rn(make_float2(w4.x, w4.y), dl2[2 * q]);
+          sh[q] = __ffma2_rn(make_float2(w4.z, w4.w), dl2[2 * q + 1], sh[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < B / 4; ++q) r += sh[q].x + sh[q].y;
+        stg_hint(rp + j * 32, r, pol);
+      }
+      if constexpr (HC) {
+        float wc[B];
+#pragma unroll
+        for (int q = 0; q < B / 4; ++q) {
+          const float4 w4 = lds128(wcur_s + wo[q]);
+          wc[4 * q + 0] = w4.x; wc[4 * q + 1] = w4.y; wc[4 * q + 2] = w4.z; wc[4 * q + 3] = w4.w;
+        }
+        const float2 rr2 = make_float2(r, r);
+#pragma unroll
+        for (int q = 0; q < B / 2; ++q) pfma(v, q, make_float2(wc[2 * q], wc[2 * q + 1]), rr2);  // C
+#pragma unroll
+        for (int jj = 0; jj < B; ++jj) {   // Gram pairs (G_jj,2m, G_jj,2m+1)
+          const float2 wj = make_float2(wc[jj], wc[jj]);
+#pragma unroll
+          for (int m = 0; 2 * m <= jj; ++m) pfma(v, L::gidx(jj, 2 * m) / 2, wj, make_float2(wc[2 * m], wc[2 * m + 1]));
+        }
+      }
+    }
+  }
+}
+
+// The R = 2^lg runs of each column (lanes [R*g, R*g + R)) combine their sums
+// (transpose reduction inside the group) and add the column's totals to the
+// accumulator; each column sits in exactly one wave per tile.
+__device__ __forceinline__ void ell_flush(float (&v)[GramLayout<kWB>::NP], int lg, int col, int lane, float* acc) {
+  using L = GramLayout<kWB>;
+  auto flush = [&](auto s_c) {
+    constexpr int S = decltype(s_c)::value;
+    constexpr int SG = S > 16 ? 16 : S;
+    if constexpr (SG > 1) group_transpose_reduce<L::NP, SG>(v, lane & (SG - 1));
+    constexpr int R = L::NP / SG;
+    if constexpr (S == 32) {
+#pragma unroll
+      for (int q = 0; q < R; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], 16);
+    }
+    int vb = 0;
+    {
+      int cnt = L::NP;
+#pragma unroll
+      for (int o = SG / 2; o >= 1; o >>= 1) { cnt >>= 1; if (lane & o) vb += cnt; }
+    }
+    if (col != 0xFFFF && (S < 32 || lane < 16)) {
+      float* dst = acc + col * L::NACC + vb;
+#pragma unroll
+      for (int q = 0; q < R; ++q)
+        if (vb + q < L::NACC) dst[q] += v[q];
+    }
   };
+  switch (lg) {
+    case 0: flush(std::integral_constant<int, 1>{}); break;
+    case 1: flush(std::integral_constant<int, 2>{}); break;
+    case 2: flush(std::integral_constant<int, 4>{}); break;
+    case 3: flush(std::integral_constant<int, 8>{}); break;
+    case 4: flush(std::integral_constant<int, 16>{}); break;
+    default: flush(std::integral_constant<int, 32>{}); break;
+  }
+}
+
+// The CTA's wave range [w_lo, w_hi) and tiles [t_lo, t_hi): ELL positions +
+// kTileVisitCost per tile visited balanced over the grid (static, deterministic),
+// boundaries snapped to wave starts.
+__device__ __forceinline__ void ell_cta_range(const DictGramArgs& a, int64_t& w_lo, int64_t& w_hi, int& t_lo,
+                                              int& t_hi) {
+  const double total_cost = (double)a.ell_base[a.ntiles] + kTileVisitCost * a.ntiles;
+  auto cost_at = [&](int t) { return (double)a.ell_base[t] + kTileVisitCost * t; };
   auto boundary = [&](int c) -> int64_t {
     if (c <= 0) return 0;
-    if (c >= (int)gridDim.x) return nnz;
-    const double target = cost_at(a.ntiles) * c / gridDim.x;
+    if (c >= (int)gridDim.x) return a.wave_base[a.ntiles];
+    const double target = total_cost * c / gridDim.x;
     int lo = 0, hi = a.ntiles - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
       if (cost_at(mid) <= target) lo = mid; else hi = mid - 1;
     }
     const double over = target - cost_at(lo) - kTileVisitCost;
-    const int64_t el = a.tile_base[lo + 1] - a.tile_base[lo];
-    const double work = cost_at(lo + 1) - cost_at(lo) - kTileVisitCost;   // elements + segment costs of tile lo
-    const int64_t e = a.tile_base[lo] + (over > 0.0 && work > 0.0 ? (int64_t)(over * (double)el / work) : 0);
-    return min(e, a.tile_base[lo + 1]);
+    const int64_t w0 = a.wave_base[lo], w1 = a.wave_base[lo + 1];
+    if (over <= 0.0 || w1 == w0) return w0;
+    int64_t wl = w0, wh = w1 - 1;   // last wave starting at or before `over`
+    while (wl < wh) {
+      const int64_t mid = (wl + wh + 1) >> 1;
+      if ((double)a.wave_off[mid] <= over) wl = mid; else wh = mid - 1;
+    }
+    return wl;
   };
-  const int64_t e_lo = boundary(blockIdx.x), e_hi = boundary(blockIdx.x + 1);
-  // tiles overlapping [e_lo, e_hi): t_lo = last tile starting <= e_lo
-  int t_lo = 0, t_hi = 0;
-  {
+  w_lo = boundary(blockIdx.x);
+  w_hi = boundary(blockIdx.x + 1);
+  t_lo = 0;
+  t_hi = 0;
+  if (w_hi > w_lo) {
     int lo = 0, hi = a.ntiles - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (a.tile_base[mid] <= e_lo) lo = mid; else hi = mid - 1;
+      if (a.wave_base[mid] <= w_lo) lo = mid; else hi = mid - 1;
     }
     t_lo = lo;
     t_hi = t_lo;
-    while (t_hi < a.ntiles && a.tile_base[t_hi] < e_hi) ++t_hi;
-    if (e_hi <= e_lo) t_hi = t_lo;
+    while (t_hi < a.ntiles && a.wave_base[t_hi] < w_hi) ++t_hi;
   }
-  const bool tb_cached = t_hi - t_lo + 1 <= kTbCache;
-  if (tb_cached)
-    for (int t = threadIdx.x; t <= t_hi - t_lo; t += blockDim.x) tbs[t] = a.tile_base[t_lo + t];
-  __syncthreads();
-  auto tile_start = [&](int t) { return tb_cached ? tbs[t - t_lo] : a.tile_base[t]; };
-  uint64_t t_mark = a.prof ? gtimer() : 0;
-  auto prof = [&](int slot) {
-    if (a.prof && threadIdx.x == 0) {
-      const uint64_t now = gtimer();
-      a.prof[blockIdx.x * kProfSlots + slot] += now - t_mark;
-      t_mark = now;
-    }
-  };
+}
 
+// Cross-CTA reduction distributed by PIXEL (after grid barrier 1): CTA c owns
+// pixels c, c+G, ...; each value of a pixel is summed over the G per-CTA
+// partials in a fixed order (f64, deterministic) and the owner performs that
+// pixel's B sequential atom draws right away (pixels are independent).
+template <int NW>
+__device__ __forceinline__ void dict_owner_phase(const DictGramArgs& a, unsigned char* smraw, uint64_t* pbar,
+                                                 uint32_t& pphase, int k0, int nb, double geps, int epoch,
+                                                 const float* dold, float* dprev) {
+  using L = GramLayout<kWB>;
+  constexpr int B = kWB;
+  const int p = a.p;
+  double* red64 = (double*)smraw;                        // p * NACC (aliases the staging)
+  auto ld_part = [&](const float* q) -> float { return a.pstage_off ? *q : __ldcg(q); };
+  const int npl = blockIdx.x < (unsigned)p ? (p - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  constexpr int NPART = (NW * 32) / L::NACC;   // threads per value
+  double* part64 = red64 + (size_t)((p + gridDim.x - 1) / gridDim.x) * L::NACC;  // [NPART][NACC] scratch
+  AtomPre* pre = (AtomPre*)(part64 + NPART * L::NACC);                          // [B]
+  float* pstage = (float*)(smraw + a.pstage_off);
+  for (int i = 0; i < npl; ++i) {
+    const int pe = blockIdx.x + i * gridDim.x;
+    const float* pix = a.partials + (size_t)pe * gridDim.x * L::NACC;
+    if (a.pstage_off) {   // one bulk copy of the pixel's partials (contiguous, L2-resident)
+      if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async;" ::: "memory");   // generic-proxy partials -> async-proxy read
+        const uint32_t bytes = gridDim.x * L::NACC * 4u;
+        mbar_expect_tx(pbar, bytes);
+        bulk_copy_g2s(pstage, pix, bytes, pbar);
+      }
+      mbar_wait(pbar, pphase);
+      pphase ^= 1u;
+    }
+    if (threadIdx.x < NPART * L::NACC) {
+      const int q = threadIdx.x % L::NACC, part = threadIdx.x / L::NACC;
+      const float* src = (a.pstage_off ? (const float*)pstage : pix) + q;
+      double acc16[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) acc16[u] = 0.0;
+      int b = part;
+      for (; b + 15 * NPART < (int)gridDim.x; b += 16 * NPART) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) acc16[u] += (double)ld_part(src + (size_t)(b + u * NPART) * L::NACC);
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u)  // tail: at most 15 more partials, still independent
+        if (b + u * NPART < (int)gridDim.x) acc16[u] += (double)ld_part(src + (size_t)(b + u * NPART) * L::NACC);
+#pragma unroll
+      for (int h = 8; h >= 1; h >>= 1)
+#pragma unroll
+        for (int u = 0; u < h; ++u) acc16[u] += acc16[u + h];
+      part64[part * L::NACC + q] = acc16[0];
+    }
+    __syncthreads();
+    if (threadIdx.x < L::NACC) {
+      double sum = 0.0;
+      for (int u = 0; u < NPART; ++u) sum += part64[u * L::NACC + threadIdx.x];
+      red64[(size_t)i * L::NACC + threadIdx.x] = sum;
+      if (a.split) a.reduced[(size_t)pe * L::NACC + threadIdx.x] = sum;
+    }
+    __syncthreads();
+    if (a.split) continue;
+    if ((int)threadIdx.x < nb)   // the parallel part of the B draws
+      pre[threadIdx.x] = atom_pre<B>(red64 + (size_t)i * L::NACC, threadIdx.x, pe, p, k0, geps, epoch, a.draws,
+                                     a.key0, a.key1, dold);
+    __syncthreads();
+    if (threadIdx.x == 0)
+      atom_pixel_update<B>(red64 + (size_t)i * L::NACC, pe, p, k0, nb, geps, epoch, a.draws, a.key0, a.key1, dold,
+                           a.atoms, dprev, a.delta_g, pre);
+    __syncthreads();
+  }
+}
+
+// Dictionary step (ELL element order), persistent and cooperative: one 16-warp
+// CTA per SM with two tile stages.  The warps walk the CTA's waves round-robin
+// ACROSS tiles (no CTA barrier per tile): stage s holds every other tile; a
+// warp waits on a stage's fill mbarrier before its first wave of that tile and,
+// once past the tile, counts itself out on the stage; the last warp out issues
+// the bulk copies of the tile two ahead into the freed stage.  Column sums of
+// even and odd tiles go to two accumulators (warps are at most one tile apart,
+// so a column is never flushed by two warps at once), summed in fixed order at
+// the end of the pass.  The next wave's first elements are loaded before the
+// current wave's flush.
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
+  using L = GramLayout<kWB>;
+  constexpr int B = kWB;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int p = a.p;
+  // [stage 0: cur | prev][stage 1: cur | prev] (each block + its zero row), aliased
+  // by the owner scratch in the update phase; then acc[2][p*NACC], dold, dprev
+  float* acc0 = (float*)(smraw + a.wbytes);
+  float* acc1 = acc0 + (size_t)p * L::NACC;
+  float* dold = acc1 + (size_t)p * L::NACC;
+  float* dprev = dold + B * p;
+  __shared__ __align__(8) uint64_t mbar[3];   // [0..1] stage fills, [2] owner partials
+  __shared__ int done[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    mbar_init(&mbar[2], 1);
+    done[0] = done[1] = 0;
+  }
+  uint32_t pphase = 0;
+  int fills0 = 0, fills1 = 0;   // fills of stage 0 / 1 completed in earlier passes (mbarrier parities)
+  unsigned bar_target = 0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const double geps = a.sc->gamma_eps;
+  const int epoch = a.sc->epoch + 1;
+  const int nblk = (a.k + B - 1) / B;
+  int64_t w_lo, w_hi;
+  int t_lo, t_hi;
+  ell_cta_range(a, w_lo, w_hi, t_lo, t_hi);
+  const int ntile = t_hi - t_lo;
+  const uint32_t sbase = smem_u32(smraw);
   if (a.split && a.blk_begin > 0) {  // split mode: the previous pass's shifts come from global memory
     for (int t = threadIdx.x; t < B * p; t += blockDim.x) dprev[t] = a.delta_g[t];
   }
-  // async staging: bulk-copy a tile's W blocks (current, previous) of pass `bk` into a stage
   const uint64_t pol_last = l2_policy_evict_last(), pol_first = l2_policy_evict_first();
-  auto issue = [&](int tile, uint32_t stage, int bk) {
+  // bulk-copy tile t_lo + u's W blocks of pass `bk` into stage u & 1
+  auto issue = [&](int u, int bk) {
+    const int s = u & 1, tile = t_lo + u;
+    unsigned char* dst = smraw + (size_t)s * 2 * kWStride;
     fence_proxy_async();
     const bool hc = bk < nblk, hp = bk > 0;
-    const uint32_t bytes = (hc ? kTile * B * 4u : 0u) + (hp ? kTile * B * 4u : 0u) + cpp * 4u;
-    mbar_expect_tx(&mbar[stage], bytes);
-    bulk_copy_g2s(cps + stage * cpp, a.colptr + (int64_t)tile * cpp, cpp * 4u, &mbar[stage]);
-    float* dst = wbuf + (size_t)stage * 2 * kTile * B;
-    if (hc) bulk_copy_g2s(dst, a.wt + ((int64_t)tile * a.nblk8 + bk) * kTile * B, kTile * B * 4u, &mbar[stage]);
+    mbar_expect_tx(&mbar[s], (hc ? kTile * B * 4u : 0u) + (hp ? kTile * B * 4u : 0u));
+    if (hc) {
+      if (a.w_evict_first)
+        bulk_copy_g2s_hint(dst, a.wt + ((int64_t)tile * a.nblk8 + bk) * kTile * B, kTile * B * 4u, &mbar[s], pol_first);
+      else
+        bulk_copy_g2s(dst, a.wt + ((int64_t)tile * a.nblk8 + bk) * kTile * B, kTile * B * 4u, &mbar[s]);
+    }
     if (hp)  // last use of the previous block
-      bulk_copy_g2s_hint(dst + kTile * B, a.wt + ((int64_t)tile * a.nblk8 + bk - 1) * kTile * B, kTile * B * 4u,
-                         &mbar[stage], pol_first);
+      bulk_copy_g2s_hint(dst + kWStride, a.wt + ((int64_t)tile * a.nblk8 + bk - 1) * kTile * B, kTile * B * 4u,
+                         &mbar[s], pol_first);
   };
   bool prefetched = false;
   for (int blk = a.split ? a.blk_begin : 0; blk <= (a.split ? a.blk_begin : nblk); ++blk) {
     const bool has_cur = blk < nblk, has_prev = blk > 0;
     const int k0 = blk * B;
     const int nb = has_cur ? min(B, a.k - k0) : 0;
-    const int kp0 = k0 - B;
-    const int nbp = has_prev ? min(B, a.k - kp0) : 0;
+    for (int t = threadIdx.x; t < 2 * p * L::NACC; t += blockDim.x) acc0[t] = 0.0f;
+    for (int t = threadIdx.x; t < B * p; t += blockDim.x) {
+      const int j = t / p, pe = t - j * p;
+      dold[t] = j < nb ? a.atoms[(int64_t)(k0 + j) * p + pe] : 0.0f;
+    }
+    if (threadIdx.x < 16) {   // the zero rows behind the four blocks (the owner phase overwrote them)
+      const int blkno = threadIdx.x >> 2, part = threadIdx.x & 3;
+      *(float2*)(smraw + blkno * kWStride + kEllZeroRow + part * 8) = make_float2(0.f, 0.f);
+    }
+    if (threadIdx.x == 0 && !prefetched) {
+      if (ntile > 0) issue(0, blk);
+      if (ntile > 1) issue(1, blk);
+    }
+    prefetched = false;
+    __syncthreads();
+    // ---- element phase: this warp's waves w_lo + wid, + NW, ... ----
+    // Every warp visits every tile of the CTA in order: wait for the stage's
+    // fill, its waves of the tile, count out (the last warp out refills the stage
+    // with the tile two ahead).  Waiting on every fill in order keeps each
+    // stage's mbarrier parity unambiguous.
+    {
+      auto fill_parity = [&](int uu) { return (uint32_t)(((uu & 1) ? fills1 : fills0) + (uu >> 1)) & 1u; };
+      auto tile_of = [&](int64_t w, int from) {
+        int t = from;
+        while (t + 1 < ntile && a.wave_base[t_lo + t + 1] <= w) ++t;
+        return t;
+      };
+      int64_t wv = w_lo + wid;
+      bool have = wv < w_hi;
+      int wu = 0;              // tile (relative) of the next wave
+      uint32_t ib[kEllPf];
+      float rb[kEllPf];
+      EllWave h{};
+      if (have) {
+        wu = tile_of(wv, 0);
+        h = ell_header(a, wv, a.ell_base[t_lo + wu], lane);
+        ell_prefetch(a, h, ib, rb, pol_last);
+      }
+      for (int u = 0; u < ntile; ++u) {
+        mbar_wait(&mbar[u & 1], fill_parity(u));
+        const uint32_t wcur_s = sbase + (uint32_t)(u & 1) * 2 * kWStride, wprev_s = wcur_s + kWStride;
+        float* acc = (u & 1) ? acc1 : acc0;
+        while (have && wu == u) {
+          float2 dl2[B / 2];
+          const bool live = h.col != 0xFFFF;
+#pragma unroll
+          for (int j = 0; j < B / 2; ++j)
+            dl2[j] = (has_prev && live) ? make_float2(dprev[2 * j * p + h.col], dprev[(2 * j + 1) * p + h.col])
+                                        : make_float2(0.f, 0.f);
+          float v[L::NP];
+#pragma unroll
+          for (int q = 0; q < L::NP; ++q) v[q] = 0.0f;
+          if (has_prev && has_cur) ell_elements<true, true>(a, h, wcur_s, wprev_s, dl2, v, ib, rb, pol_last);
+          else if (has_cur) ell_elements<false, true>(a, h, wcur_s, wprev_s, dl2, v, ib, rb, pol_last);
+          else ell_elements<true, false>(a, h, wcur_s, wprev_s, dl2, v, ib, rb, pol_last);
+          const int lg_c = h.lg, col_c = h.col;
+          // the next wave's header and first elements go in flight before the flush
+          wv += NW;
+          have = wv < w_hi;
+          if (have) {
+            wu = tile_of(wv, wu);
+            h = ell_header(a, wv, a.ell_base[t_lo + wu], lane);
+            ell_prefetch(a, h, ib, rb, pol_last);
+          }
+          if (has_cur) ell_flush(v, lg_c, col_c, lane, acc);
+        }
+        // count out of tile u; the last warp out refills its stage with tile u + 2
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_block();
+          const int s = u & 1;
+          if (atomicAdd(&done[s], 1) == NW - 1) {
+            done[s] = 0;
+            if (u + 2 < ntile) issue(u + 2, blk);
+          }
+        }
+      }
+      fills0 += (ntile + 1) >> 1;
+      fills1 += ntile >> 1;
+    }
+    if (!has_cur) break;
+    __syncthreads();
+    // pixel-major partials [pixel][CTA][NACC] (even + odd tile sums, fixed order)
+    for (int t = threadIdx.x; t < p * L::NACC; t += blockDim.x) {
+      const int pe = t / L::NACC, q = t - pe * L::NACC;
+      a.partials[((size_t)pe * gridDim.x + blockIdx.x) * L::NACC + q] = acc0[t] + acc1[t];
+    }
+    if (PB_DBG(a, 16)) grid_sync(a.bar); else grid_sync_mono(a.bar + 2, bar_target);
+    dict_owner_phase<NW>(a, smraw, &mbar[2], pphase, k0, nb, geps, epoch, dold, dprev);
+    if (a.split) return;  // split mode: the caller allreduces `reduced` across ranks, then k_dict_update
+    // the next pass's first tiles do not depend on the shifts: stage them now
+    // (the owner scratch they overwrite is done) so they land during the barrier
+    if (threadIdx.x == 0) {
+      if (ntile > 0) issue(0, blk + 1);
+      if (ntile > 1) issue(1, blk + 1);
+    }
+    prefetched = true;
+    if (PB_DBG(a, 16)) grid_sync(a.bar); else grid_sync_mono(a.bar + 2, bar_target);
+    for (int t = threadIdx.x; t < B * p; t += blockDim.x) dprev[t] = __ldcg(a.delta_g + t);
+    __syncthreads();
+  }
+}
+
+// Single-stage variant (large patches, where two stages and two accumulators do
+// not fit): NW warps, the CTA's tiles one at a time, the tile's waves
+// round-robin over the warps, a CTA barrier per tile.
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) {
+  using L = GramLayout<kWB>;
+  constexpr int B = kWB;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int p = a.p;
+  float* acc = (float*)(smraw + a.wbytes);               // p * NACC
+  float* dold = acc + (size_t)p * L::NACC;               // B * p
+  float* dprev = dold + B * p;                           // B * p
+  __shared__ __align__(8) uint64_t mbar[2];   // [0] staging, [1] owner partials
+  const uint32_t wcur_s = smem_u32(smraw), wprev_s = wcur_s + kWStride;
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+  }
+  uint32_t pphase = 0, sphase = 0;
+  unsigned bar_target = 0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const double geps = a.sc->gamma_eps;
+  const int epoch = a.sc->epoch + 1;
+  const int nblk = (a.k + B - 1) / B;
+  int64_t w_lo, w_hi;
+  int t_lo, t_hi;
+  ell_cta_range(a, w_lo, w_hi, t_lo, t_hi);
+  if (a.split && a.blk_begin > 0) {
+    for (int t = threadIdx.x; t < B * p; t += blockDim.x) dprev[t] = a.delta_g[t];
+  }
+  const uint64_t pol_last = l2_policy_evict_last(), pol_first = l2_policy_evict_first();
+  auto issue = [&](int tile, int bk) {
+    fence_proxy_async();
+    const bool hc = bk < nblk, hp = bk > 0;
+    mbar_expect_tx(&mbar[0], (hc ? kTile * B * 4u : 0u) + (hp ? kTile * B * 4u : 0u));
+    if (hc) bulk_copy_g2s(smraw, a.wt + ((int64_t)tile * a.nblk8 + bk) * kTile * B, kTile * B * 4u, &mbar[0]);
+    if (hp)
+      bulk_copy_g2s_hint(smraw + kWStride, a.wt + ((int64_t)tile * a.nblk8 + bk - 1) * kTile * B, kTile * B * 4u,
+                         &mbar[0], pol_first);
+  };
+  bool prefetched = false;
+  for (int blk = a.split ? a.blk_begin : 0; blk <= (a.split ? a.blk_begin : nblk); ++blk) {
+    const bool has_cur = blk < nblk, has_prev = blk > 0;
+    const int k0 = blk * B;
+    const int nb = has_cur ? min(B, a.k - k0) : 0;
     for (int t = threadIdx.x; t < p * L::NACC; t += blockDim.x) acc[t] = 0.0f;
     for (int t = threadIdx.x; t < B * p; t += blockDim.x) {
       const int j = t / p, pe = t - j * p;
       dold[t] = j < nb ? a.atoms[(int64_t)(k0 + j) * p + pe] : 0.0f;
     }
-    const bool pf = prefetched;   // this pass's first tile was issued at the end of the previous pass
-    prefetched = false;
-    __syncthreads();
-    if (NSTAGE == 2 && t_lo < t_hi && !pf) {
-      if (threadIdx.x == 0 && !PB_DBG(a, 4)) issue(t_lo, seq & 1, blk);
+    if (threadIdx.x < 8) {   // the zero rows behind both blocks (the owner phase overwrote them)
+      const int blkno = threadIdx.x >> 2, part = threadIdx.x & 3;
+      *(float2*)(smraw + blkno * kWStride + kEllZeroRow + part * 8) = make_float2(0.f, 0.f);
     }
-    for (int tile = t_lo; tile < t_hi; ++tile, ++seq) {
-      const uint32_t st = NSTAGE == 2 ? (seq & 1) : 0;
-      __syncthreads();   // previous tile fully consumed: its stage and cps buffer are free
-      prof(0);
-      if (threadIdx.x == 0 && !PB_DBG(a, 4)) {
-        if (NSTAGE == 1) { if (!(pf && tile == t_lo)) issue(tile, 0, blk); }
-        else if (tile + 1 < t_hi) issue(tile + 1, st ^ 1, blk);
+    const bool pf = prefetched;
+    prefetched = false;
+    for (int tile = t_lo; tile < t_hi; ++tile) {
+      __syncthreads();   // previous tile fully consumed (and the zero rows written)
+      if (threadIdx.x == 0 && !(pf && tile == t_lo)) issue(tile, blk);
+      const int64_t wa = max(w_lo, a.wave_base[tile]), wb = min(w_hi, a.wave_base[tile + 1]);
+      const int64_t tile_ell = a.ell_base[tile];
+      mbar_wait(&mbar[0], sphase);
+      sphase ^= 1u;
+      for (int64_t wv = wa + wid; wv < wb; wv += NW) {
+        const EllWave h = ell_header(a, wv, tile_ell, lane);
+        uint32_t ib[kEllPf];
+        float rb[kEllPf];
+        ell_prefetch(a, h, ib, rb, pol_last);
+        float2 dl2[B / 2];
+        const bool live = h.col != 0xFFFF;
+#pragma unroll
+        for (int j = 0; j < B / 2; ++j)
+          dl2[j] = (has_prev && live) ? make_float2(dprev[2 * j * p + h.col], dprev[(2 * j + 1) * p + h.col])
+                                      : make_float2(0.f, 0.f);
+        float v[L::NP];
+#pragma unroll
+        for (int q = 0; q < L::NP; ++q) v[q] = 0.0f;
+        if (has_prev && has_cur) ell_elements<true, true>(a, h, wcur_s, wprev_s, dl2, v, ib, rb, pol_last);
+        else if (has_cur) ell_elements<false, true>(a, h, wcur_s, wprev_s, dl2, v, ib, rb, pol_last);
+        else ell_elements<true, false>(a, h, wcur_s, wprev_s, dl2, v, ib, rb, pol_last);
+        if (has_cur) ell_flush(v, h.lg, h.col, lane, acc);
       }
-      if (lane == 0) { slot_col[wid * 2] = -1; slot_col[wid * 2 + 1] = -1; }
-      const int64_t tb = tile_start(tile);
-      const int64_t rs = max(tb, e_lo), re = min(tile_start(tile + 1), e_hi);
-      const float* wcur = wbuf + (size_t)st * 2 * kTile * B;
-      const uint32_t wcur_s = smem_u32(wcur), wprev_s = wcur_s + kTile * B * 4u;
-      const int* cpt = cps + st * cpp;
-      if (!PB_DBG(a, 4)) mbar_wait(&mbar[st], (phase_bits >> st) & 1u);
-      phase_bits ^= 1u << st;
-      prof(1);
-      const int m = (int)(re - rs);
-      const int ws = (int)(rs - tb) + (int)((int64_t)m * wid / NW), we = (int)(rs - tb) + (int)((int64_t)m * (wid + 1) / NW);
-      if (ws < we && !PB_DBG(a, 8)) {
-        // Element phase of this warp's slice [ws, we).  The slice is cut into
-        // segments that never cross a column end and hold at most kSegLen
-        // elements; a ROUND gives one segment to each of the kGroups lane
-        // groups (kGroupLanes lanes each, striding the segment).  The Gram /
-        // moment sums of a round are reduced inside each lane group (3 shuffle
-        // levels instead of 5 per column), groups that share a column are
-        // combined in group order, and the head group adds the totals to the
-        // CTA accumulator (or the warp's boundary slot) — fixed order, so
-        // deterministic.
-        constexpr int S = kGroupLanes, NG = 32 / kGroupLanes;
-        const int grp = lane / S, sub = lane % S;
-        int col = 0;
-        {
-          int lo = 0, hi = p - 1;
-          while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (cpt[mid] <= ws) lo = mid; else hi = mid - 1; }
-          col = lo;
-        }
-        const int c_first = col;
-        int pos = ws;
-        // segment length: when the slice spans fewer columns than groups, cut it
-        // into whole rounds of NG equal segments (<= kSegLen); otherwise the
-        // column ends already give enough segments
-        int c_last = 0;
-        {
-          int lo = c_first, hi = p - 1;
-          while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (cpt[mid] <= we - 1) lo = mid; else hi = mid - 1; }
-          c_last = lo;
-        }
-        int seg_len = kSegLen;
-        if (c_last - c_first + 1 < NG) {
-          const int n_rounds = (we - ws + NG * kSegLen - 1) / (NG * kSegLen);
-          seg_len = ((we - ws + NG * n_rounds - 1) / (NG * n_rounds) + S - 1) / S * S;
-        }
-        for (int q = lane; q < 2 * L::NACC; q += 32) slots[wid * 2 * L::NACC + q] = 0.0f;
-        __syncwarp();
-        // carve the next NG segments (warp-uniform) and put the first kPf
-        // elements of this lane's segment in flight
-        constexpr int kPf = 6;   // elements in flight per lane (2: 2.7x slower; 8: spills)
-        const uint16_t* eloc_t = a.e_loc + tb;
-        float* r_t = a.r_csc + tb;
-        int ms = 0, mt = 0, mc = -1, its = 0;
-        int ilb[kPf];
-        float rb[kPf];
-        auto carve = [&]() {
-          int max_len = 0;
-          ms = 0; mt = 0; mc = -1;
-#pragma unroll
-          for (int g = 0; g < NG; ++g) {
-            int s = we, t = we, cg = -1;
-            if (pos < we) {
-              while (cpt[col + 1] <= pos) ++col;  // skip empty columns
-              s = pos;
-              t = min(min(we, cpt[col + 1]), pos + seg_len);
-              cg = col;
-              pos = t;
-            }
-            max_len = max(max_len, t - s);
-            if (g == grp) { ms = s; mt = t; mc = cg; }
-          }
-          its = (max_len + S - 1) / S;
-#pragma unroll
-          for (int d = 0; d < kPf; ++d) {
-            const int e = ms + sub + d * S;
-            ilb[d] = 0;
-            rb[d] = 0.0f;
-            if (e < mt) { ilb[d] = ldg_hint(eloc_t + e, pol_last); rb[d] = ldg_hint(r_t + e, pol_last); }
-          }
-        };
-        carve();
-        while (true) {
-          float2 dl2[B / 2];
-#pragma unroll
-          for (int j = 0; j < B / 2; ++j)
-            dl2[j] = (has_prev && mc >= 0) ? make_float2(dprev[2 * j * p + mc], dprev[(2 * j + 1) * p + mc])
-                                           : make_float2(0.0f, 0.0f);
-          float v[L::NP];
-#pragma unroll
-          for (int q = 0; q < L::NP; ++q) v[q] = 0.0f;
-          // lane-private cursors: element ec, its residual slot rc, kPf*S ahead in flight
-          int ec = ms + sub;
-          float* rc = r_t + ec;
-          const uint16_t* ecp = eloc_t + ec;
-          // the pass's block flags are compile-time inside the element loop
-          auto elements = [&](auto hp_c, auto hc_c) {
-            constexpr bool HP = decltype(hp_c)::value, HC = decltype(hc_c)::value;
-            for (int it = 0; it < its; it += kPf) {
-#pragma unroll
-              for (int d = 0; d < kPf; ++d) {
-                if (it + d >= its) break;
-                const int il = ilb[d];
-                float r = rb[d];
-                if (ec + kPf * S < mt) { ilb[d] = ldg_hint(ecp + kPf * S, pol_last); rb[d] = ldg_hint(rc + kPf * S, pol_last); }
-                if (ec < mt) {
-                  const uint32_t wo[2] = {(uint32_t)il, (uint32_t)il ^ 16u};  // e_loc holds w_row_off
-                  if constexpr (HP) {  // r += w_prev . delta  (packed pairs, two independent chains)
-                    float2 sh[B / 4];
-#pragma unroll
-                    for (int h = 0; h < B / 4; ++h) {
-                      const float4 w4 = lds128(wprev_s + wo[h]);
-                      sh[h] = __fmul2_rn(make_float2(w4.x, w4.y), dl2[2 * h]);
-                      sh[h] = __ffma2_rn(make_float2(w4.z, w4.w), dl2[2 * h + 1], sh[h]);
-                    }
-#pragma unroll
-                    for (int h = 0; h < B / 4; ++h) r += sh[h].x + sh[h].y;
-                    stg_hint(rc, r, pol_last);
-                  }
-                  if constexpr (HC) {
-                    float wc[B];
-#pragma unroll
-                    for (int h = 0; h < B / 4; ++h) {
-                      const float4 w4 = lds128(wcur_s + wo[h]);
-                      wc[4 * h + 0] = w4.x; wc[4 * h + 1] = w4.y; wc[4 * h + 2] = w4.z; wc[4 * h + 3] = w4.w;
-                    }
-                    const float2 rr2 = make_float2(r, r);
-#pragma unroll
-                    for (int h = 0; h < B / 2; ++h) pfma(v, h, make_float2(wc[2 * h], wc[2 * h + 1]), rr2);  // C
-#pragma unroll
-                    for (int j = 0; j < B; ++j) {   // Gram pairs (G_j,2m, G_j,2m+1)
-                      const float2 wj = make_float2(wc[j], wc[j]);
-#pragma unroll
-                      for (int m = 0; 2 * m <= j; ++m)
-                        pfma(v, L::gidx(j, 2 * m) / 2, wj, make_float2(wc[2 * m], wc[2 * m + 1]));
-                    }
-                  }
-                }
-                ec += S;
-                rc += S;
-                ecp += S;
-              }
-            }
-          };
-          if (has_prev && has_cur) elements(std::true_type{}, std::true_type{});
-          else if (has_cur) elements(std::false_type{}, std::true_type{});
-          else elements(std::true_type{}, std::false_type{});
-          const int mc_done = mc;
-          const bool more = pos < we;
-          if (more) carve();  // next round's loads overlap this round's reduction
-          if (has_cur) {
-            // reduce inside the lane group: lane `sub` ends with values [base, base + NP/S)
-            group_transpose_reduce<L::NP, S>(v, sub);
-            constexpr int R = L::NP / S;
-            int base = 0;
-            {
-              int cnt = L::NP;
-#pragma unroll
-              for (int o = S / 2; o >= 1; o >>= 1) { cnt >>= 1; if (sub & o) base += cnt; }
-            }
-            // combine groups of the same column: segmented doubling sum toward
-            // the run's first group (columns are non-decreasing across groups)
-#pragma unroll
-            for (int k = 1; k < NG; k <<= 1) {
-              const int cn = __shfl_down_sync(0xffffffffu, mc_done, k * S);
-              const bool join = grp + k < NG && cn == mc_done && mc_done >= 0;
-#pragma unroll
-              for (int q = 0; q < R; ++q) {
-                const float o = __shfl_down_sync(0xffffffffu, v[q], k * S);
-                v[q] += join ? o : 0.0f;
-              }
-            }
-            const int c_prev = __shfl_up_sync(0xffffffffu, mc_done, S);
-            const bool head = mc_done >= 0 && (grp == 0 || c_prev != mc_done);
-            if (head) {
-              const bool exclusive = cpt[mc_done] >= ws && cpt[mc_done + 1] <= we;
-              const int slot = wid * 2 + (mc_done == c_first ? 0 : 1);
-              float* dst = exclusive ? acc + mc_done * L::NACC : slots + slot * L::NACC;
-#pragma unroll
-              for (int q = 0; q < R; ++q)
-                if (base + q < L::NACC) dst[base + q] += v[q];
-              if (!exclusive && sub == 0) slot_col[slot] = mc_done;
-            }
-          }
-          if (!more) break;
-        }
-      }
-      prof(2);
-      __syncthreads();
-      prof(3);
-      // merge the boundary segments in warp order (deterministic): the valid
-      // slots have non-decreasing columns, so each column is a run of slots;
-      // warp h merges the h-th run (every warp derives the runs by ballot)
-      if (has_cur) {
-        const int col = lane < NW * 2 ? slot_col[lane] : -1;
-        const unsigned vm = __ballot_sync(0xffffffffu, col >= 0);
-        const unsigned before = vm & ((1u << lane) - 1u);
-        const int prev_col = __shfl_sync(0xffffffffu, col, before ? 31 - __clz(before) : 0);
-        const unsigned hm = __ballot_sync(0xffffffffu, col >= 0 && (!before || prev_col != col));
-        for (int h = wid; h < __popc(hm); h += NW) {
-          unsigned m = hm;
-          for (int i = 0; i < h; ++i) m &= m - 1u;
-          const int hs = __ffs(m) - 1;
-          const int c = __shfl_sync(0xffffffffu, col, hs);
-          for (int q = lane; q < L::NACC; q += 32) {
-            float sum = acc[c * L::NACC + q];
-            for (int s2 = hs; s2 < NW * 2; ++s2) {
-              const int c2 = slot_col[s2];
-              if (c2 == c) sum += slots[s2 * L::NACC + q];
-              else if (c2 > c) break;
-            }
-            acc[c * L::NACC + q] = sum;
-          }
-        }
-      }
-      prof(4);
     }
     if (!has_cur) break;
     __syncthreads();
-    // pixel-major partials [pixel][CTA][NACC]: an owner stages all of its
-    // pixel's partials with one bulk copy
     for (int t = threadIdx.x; t < p * L::NACC; t += blockDim.x) {
       const int pe = t / L::NACC, q = t - pe * L::NACC;
       a.partials[((size_t)pe * gridDim.x + blockIdx.x) * L::NACC + q] = acc[t];
     }
-    // (no per-thread fence: the barrier's bar.sync + the master's gpu-scope
-    // fence and release publish the CTA's partials, as in cooperative groups)
-    prof(5);
     if (PB_DBG(a, 16)) grid_sync(a.bar); else grid_sync_mono(a.bar + 2, bar_target);
-    prof(6);
-    // Cross-CTA reduction distributed by PIXEL: CTA c owns pixels c, c+G, ...;
-    // one warp per (pixel, value) sums the G partials lane-strided then by a
-    // fixed shuffle tree (f64, deterministic), and the owner performs that
-    // pixel's B sequential atom draws right away (pixels are independent).
-    const int npl = blockIdx.x < (unsigned)p ? (p - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-    constexpr int NPART = (NW * 32) / L::NACC;   // threads per value
-    double* part64 = red64 + (size_t)((p + gridDim.x - 1) / gridDim.x) * L::NACC;  // [NPART][NACC] scratch
-    AtomPre* pre = (AtomPre*)(part64 + NPART * L::NACC);                          // [B]
-    // the pixel's G x NACC partials staged in shared memory behind the scratch
-    float* pstage = (float*)(smraw + a.pstage_off);
-    for (int i = 0; i < npl; ++i) {
-      const int pe = blockIdx.x + i * gridDim.x;
-      const float* pix = a.partials + (size_t)pe * gridDim.x * L::NACC;
-      if (a.pstage_off) {   // one bulk copy of the pixel's partials (contiguous, L2-resident)
-        if (threadIdx.x == 0) {
-          asm volatile("fence.proxy.async;" ::: "memory");   // generic-proxy partials -> async-proxy read
-          const uint32_t bytes = gridDim.x * L::NACC * 4u;
-          mbar_expect_tx(&mbar[2], bytes);
-          bulk_copy_g2s(pstage, pix, bytes, &mbar[2]);
-        }
-        mbar_wait(&mbar[2], pphase);
-        pphase ^= 1u;
-      }
-      if (threadIdx.x < NPART * L::NACC) {
-        // value q over partials b = part, part + NPART, ...: 16 independent chains
-        const int q = threadIdx.x % L::NACC, part = threadIdx.x / L::NACC;
-        const float* src = (a.pstage_off ? (const float*)pstage : pix) + q;
-        double acc16[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) acc16[u] = 0.0;
-        int b = part;
-        for (; b + 15 * NPART < (int)gridDim.x; b += 16 * NPART) {
-#pragma unroll
-          for (int u = 0; u < 16; ++u) acc16[u] += (double)ld_part(src + (size_t)(b + u * NPART) * L::NACC);
-        }
-#pragma unroll
-        for (int u = 0; u < 16; ++u)  // tail: at most 15 more partials, still independent
-          if (b + u * NPART < (int)gridDim.x) acc16[u] += (double)ld_part(src + (size_t)(b + u * NPART) * L::NACC);
-#pragma unroll
-        for (int h = 8; h >= 1; h >>= 1)
-#pragma unroll
-          for (int u = 0; u < h; ++u) acc16[u] += acc16[u + h];
-        part64[part * L::NACC + q] = acc16[0];
-      }
-      __syncthreads();
-      if (threadIdx.x < L::NACC) {
-        double sum = 0.0;
-        for (int u = 0; u < NPART; ++u) sum += part64[u * L::NACC + threadIdx.x];
-        red64[(size_t)i * L::NACC + threadIdx.x] = sum;
-        if (a.split) a.reduced[(size_t)pe * L::NACC + threadIdx.x] = sum;
-      }
-      __syncthreads();
-      if (a.split) continue;
-      prof(11);
-      if ((int)threadIdx.x < nb)   // the parallel part of the B draws
-        pre[threadIdx.x] = atom_pre<B>(red64 + (size_t)i * L::NACC, threadIdx.x, pe, p, k0, geps, epoch, a.draws,
-                                       a.key0, a.key1, dold);
-      __syncthreads();
-      if (threadIdx.x == 0)
-        atom_pixel_update<B>(red64 + (size_t)i * L::NACC, pe, p, k0, nb, geps, epoch, a.draws, a.key0, a.key1, dold,
-                             a.atoms, dprev, a.delta_g, pre);
-      __syncthreads();
-    }
-    prof(7);
-    if (a.split) return;  // split mode: the caller allreduces `reduced` across ranks, then k_dict_update
-    // the next pass's first tile does not depend on the shifts: stage it now
-    // (the owner scratch it overwrites is done) so it lands during the barrier
-    if (t_lo < t_hi && !PB_DBG(a, 4)) {
-      if (threadIdx.x == 0) issue(t_lo, NSTAGE == 2 ? (seq & 1) : 0u, blk + 1);
+    dict_owner_phase<NW>(a, smraw, &mbar[1], pphase, k0, nb, geps, epoch, dold, dprev);
+    if (a.split) return;
+    if (t_lo < t_hi) {
+      if (threadIdx.x == 0) issue(t_lo, blk + 1);
       prefetched = true;
     }
-    prof(10);
     if (PB_DBG(a, 16)) grid_sync(a.bar); else grid_sync_mono(a.bar + 2, bar_target);
-    prof(8);
     for (int t = threadIdx.x; t < B * p; t += blockDim.x) dprev[t] = __ldcg(a.delta_g + t);
     __syncthreads();
-    prof(9);
   }
 }
 
@@ -1471,24 +1532,26 @@ int launch_code_compact(const CompactArgs& a_in, int mode, int& nblocks, cudaStr
   return PB_OK;
 }
 
-template <int B, int GL, int SL, int NW, int NSTAGE>
+template <int NW>
 static size_t dict_gram_smem(int p, size_t* wbytes_out) {
-  using L = GramLayout<B>;
-  const size_t wbytes = std::max((size_t)NSTAGE * 2 * kTile * B * 4, (size_t)p * L::NACC * 8);
+  using L = GramLayout<kWB>;
+  const size_t wbytes = std::max((size_t)2 * kWStride, (size_t)p * L::NACC * 8);
   if (wbytes_out) *wbytes_out = wbytes;
-  return wbytes + (size_t)p * L::NACC * 4 + (size_t)NW * 2 * L::NACC * 4 + NW * 2 * 4 +
-         (size_t)NSTAGE * colptr_pitch(p) * 4 + (size_t)kTbCache * 8 + (size_t)2 * B * p * 4;
+  return wbytes + (size_t)p * L::NACC * 4 + (size_t)2 * kWB * p * 4;
 }
 
-template <int B, int GL, int SL, int NW, int NSTAGE>
+static size_t dict_ell2_smem(int p, size_t* wbytes_out);
+
+template <int NW, bool TWO>
 static int launch_dict_gram_b(DictGramArgs a, cudaStream_t st) {
+  constexpr int B = kWB;
   const int th = NW * 32;
   if (a.ld % 4) { set_error("usage/weights row pitch must be a multiple of 4 (got %lld)", (long long)a.ld); return PB_EVALUE; }
   size_t wbytes = 0;
-  const size_t smem = dict_gram_smem<B, GL, SL, NW, NSTAGE>(a.p, &wbytes);
+  const size_t smem = TWO ? dict_ell2_smem(a.p, &wbytes) : dict_gram_smem<NW>(a.p, &wbytes);
   a.wbytes = (int)wbytes;
   if (smem > 225 * 1024) { set_error("patch size %d too large for the dictionary step", a.p); return PB_EUNSUPPORTED; }
-  auto kern = k_dict_gram<B, GL, SL, NW, NSTAGE>;
+  auto kern = TWO ? k_dict_ell2<NW> : k_dict_gram<NW>;
   PB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   PB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, th, smem));
@@ -1511,13 +1574,33 @@ static int launch_dict_gram_b(DictGramArgs a, cudaStream_t st) {
   return PB_OK;
 }
 
-int launch_dict_gram(const DictGramArgs& a, cudaStream_t st) {
-  // two 8-warp CTAs per SM (single-buffered staging) when they fit in shared
-  // memory, else one 16-warp CTA with double-buffered staging
+static size_t dict_ell2_smem(int p, size_t* wbytes_out) {
+  using L = GramLayout<kWB>;
+  const size_t wbytes = std::max((size_t)4 * kWStride, (size_t)p * L::NACC * 8);
+  if (wbytes_out) *wbytes_out = wbytes;
+  return wbytes + (size_t)2 * p * L::NACC * 4 + (size_t)2 * kWB * p * 4;
+}
+
+int launch_dict_gram(const DictGramArgs& a_in, cudaStream_t st) {
+  // one 16-warp CTA per SM with two tile stages (waves flow across tiles) when
+  // it fits in shared memory; else the single-stage variant
+  DictGramArgs a = a_in;
+  // both W blocks stream with evict_first: the residual and the element index
+  // (re-read every pass) keep L2 (configs[1] 3.41 -> 2.52 ms)
+  a.w_evict_first = PB_TUNE_INT("PB_DICT_W_EVICT", 1);
+  {
+    static bool l2_set = false;
+    const int persist = PB_TUNE_INT("PB_L2_PERSIST_MB", 0);
+    if (persist > 0 && !l2_set) {
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)persist << 20);
+      l2_set = true;
+    }
+  }
   const int variant = PB_TUNE_INT("PB_DICT_VARIANT", 0);
-  if (variant != 1 && 2 * dict_gram_smem<8, kDictGroupLanes, kDictSegLen, 8, 1>(a.p, nullptr) <= 226 * 1024)
-    return launch_dict_gram_b<8, kDictGroupLanes, kDictSegLen, 8, 1>(a, st);
-  return launch_dict_gram_b<8, kDictGroupLanes, kDictSegLen, 16, 2>(a, st);
+  if (variant == 0 && dict_ell2_smem(a.p, nullptr) <= 225 * 1024)
+    return launch_dict_gram_b<16, true>(a, st);
+  if (variant != 1 && 2 * dict_gram_smem<8>(a.p, nullptr) <= 226 * 1024) return launch_dict_gram_b<8, false>(a, st);
+  return launch_dict_gram_b<16, false>(a, st);
 }
 
 int launch_dict_update(const DictGramArgs& a, int blk, cudaStream_t st) {

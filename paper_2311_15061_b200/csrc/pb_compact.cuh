@@ -51,10 +51,13 @@ struct CompactArgs {
 };
 
 struct DictGramArgs {
-  // index (CSC view)
-  const int64_t* tile_base;
-  const int32_t* colptr;
-  const uint16_t* e_loc;
+  // index (ELL wave view, pb_index.cu)
+  const int64_t* ell_base;    // [ntiles + 1] ELL positions per tile (prefix)
+  const int64_t* wave_base;   // [ntiles + 1] waves per tile (prefix)
+  const uint32_t* wave_off;   // [waves] first position of the wave inside its tile
+  const uint16_t* wave_meta;  // [waves] Lw | log2(R) << 8
+  const uint16_t* wave_col;   // [waves][32] column of each lane (0xFFFF idle)
+  const uint16_t* e_ell;      // [nnz_ell] W-row byte offset of each position
   int ntiles;
   const float* wt;      // tile-blocked code copy [tile][k/8][patch][8]
   int nblk8;
@@ -79,8 +82,7 @@ struct DictGramArgs {
   int max_blocks;
   int wbytes;
   int pstage_off;       // byte offset of the staged owner partials in shared memory (0: read from L2)
-  const int64_t* seg_base;  // per-tile column-segment prefix (work-split cost model) or null
-  double seg_cost;          // element equivalents of one segment
+  int w_evict_first;    // the current block's W copy with an L2 evict_first policy too
   int64_t n;
   int64_t ld;           // row pitch of usage/weights (K, ld), ld >= n
   int64_t nnz;          // observed elements (host copy of tile_base[ntiles])
@@ -93,7 +95,6 @@ int launch_code_compact(const CompactArgs& a, int mode, int& nblocks, cudaStream
 // the code step's per-patch limit for the main launch from the count histogram (0 = no split)
 int code_split_choose(const int32_t* hist, int p, int cmax);
 int code_launch_blocks(int cmax, int64_t n, int p, int k);  // blocks of patches (= S^2/R^2 pairs) of a launch
-constexpr double kDictSegCost = 40.0;  // element equivalents of one element-phase segment (work split; live -5 %)
 int launch_dict_gram(const DictGramArgs& a, cudaStream_t st);
 // dictionary step on all-zero codes: prior redraw of every atom (bit-identical to launch_dict_gram on W == 0)
 int launch_dict_prior(const DictGramArgs& a, cudaStream_t st);

@@ -120,7 +120,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* wsum, int& total) {
 __global__ void __launch_bounds__(kFillThreads) k_tile_fill(
     const uint8_t* __restrict__ obs, const float* __restrict__ values, const int32_t* __restrict__ counts, int64_t n,
     int p, const int64_t* __restrict__ tile_base, int32_t* __restrict__ colptr, uint16_t* __restrict__ e_loc,
-    float* __restrict__ x_csc, int64_t* __restrict__ rowptr, uint16_t* __restrict__ csr_p,
+    uint32_t* __restrict__ slot_csc, int64_t* __restrict__ rowptr, uint16_t* __restrict__ csr_p,
     uint32_t* __restrict__ csr_pos) {
   static_assert(kTile == 2 * kFillThreads, "two patches per fill thread");
   __shared__ int wsum[33];
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kFillThreads) k_tile_fill(
     if (o0) {
       const int64_t pos = col + rank;
       e_loc[pos] = (uint16_t)w_row_off(l0);
-      ((uint32_t*)x_csc)[pos] = (uint32_t)(row0 + j0);   // CSR slot (k_csc_spread); values: k_scatter_x
+      slot_csc[pos] = (uint32_t)(row0 + j0);   // CSR slot (ELL transform); values: k_scatter_x
       csr_p[row0 + j0] = (uint16_t)pe;
       csr_pos[row0 + j0] = (uint32_t)pos;
       ++j0;
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kFillThreads) k_tile_fill(
     if (o1) {
       const int64_t pos = col + rank + o0;
       e_loc[pos] = (uint16_t)w_row_off(l0 + 1);
-      ((uint32_t*)x_csc)[pos] = (uint32_t)(row1 + j1);
+      slot_csc[pos] = (uint32_t)(row1 + j1);
       csr_p[row1 + j1] = (uint16_t)pe;
       csr_pos[row1 + j1] = (uint32_t)pos;
       ++j1;
@@ -184,8 +184,9 @@ int index_bytes(int64_t n, int p, int64_t nnz_upper, size_t* out) {
   a((size_t)(ntiles + 1) * 8);        // tile_base
   a((size_t)ntiles * colptr_pitch(p) * 4);    // colptr
   a((size_t)(n + 1) * 8);             // rowptr
-  a((size_t)nnz_upper * 2);           // e_loc
-  a((size_t)nnz_upper * 4);           // x_csc
+  const int64_t ecap = ell_cap(n, nnz_upper), wcap = wave_cap(n, p, nnz_upper);
+  a((size_t)nnz_upper * 2);           // e_loc (CSC)
+  a((size_t)ecap * 4);                // x_csc (ELL order)
   a((size_t)nnz_upper * 2);           // csr_p
   a((size_t)nnz_upper * 4);           // csr_pos
   a(64);                              // cmax + misc
@@ -195,6 +196,15 @@ int index_bytes(int64_t n, int p, int64_t nnz_upper, size_t* out) {
   a((size_t)(p + 2) * 4);             // histogram of observed counts
   a((size_t)ntiles * 4);              // tile_segs
   a((size_t)(ntiles + 1) * 8);        // seg_base
+  a((size_t)nnz_upper * 4);           // slot_csc
+  a((size_t)ecap * 2);                // e_ell
+  a((size_t)ntiles * 4);              // ell_tot
+  a((size_t)(ntiles + 1) * 8);        // ell_base
+  a((size_t)ntiles * 4);              // wave_tot
+  a((size_t)(ntiles + 1) * 8);        // wave_base
+  a((size_t)wcap * 4);                // wave_off
+  a((size_t)wcap * 2);                // wave_meta
+  a((size_t)wcap * 64);               // wave_col
   *out = b;
   return PB_OK;
 }
@@ -208,8 +218,9 @@ void carve_index(PatchIndex& ix, char* base, int64_t n, int p, int64_t nnz_upper
   ix.tile_base = (int64_t*)take((size_t)(ntiles + 1) * 8);
   ix.colptr = (int32_t*)take((size_t)ntiles * colptr_pitch(p) * 4);
   ix.rowptr = (int64_t*)take((size_t)(n + 1) * 8);
+  const int64_t ecap = ell_cap(n, nnz_upper), wcap = wave_cap(n, p, nnz_upper);
   ix.e_loc = (uint16_t*)take((size_t)nnz_upper * 2);
-  ix.x_csc = (float*)take((size_t)nnz_upper * 4);
+  ix.x_csc = (float*)take((size_t)ecap * 4);
   ix.csr_p = (uint16_t*)take((size_t)nnz_upper * 2);
   ix.csr_pos = (uint32_t*)take((size_t)nnz_upper * 4);
   ix.cmax_dev = (int32_t*)take(64);
@@ -219,101 +230,15 @@ void carve_index(PatchIndex& ix, char* base, int64_t n, int p, int64_t nnz_upper
   ix.hist = (int32_t*)take((size_t)(p + 2) * 4);
   ix.tile_segs = (int32_t*)take((size_t)ntiles * 4);
   ix.seg_base = (int64_t*)take((size_t)(ntiles + 1) * 8);
-}
-
-// Bank spreading of the CSC order (after k_tile_fill, before k_scatter_x).
-// The dictionary step's lanes gather each element's W row from shared memory
-// with 16-byte loads whose quarter-warps are 8 CONSECUTIVE elements of a column
-// run; rows land on one of 8 bank quads ((e_loc >> 4) & 7), so a random order
-// costs ~2.2x the ideal wavefronts.  One warp per (tile, column) ranks the
-// elements inside their quad (warp ballots) and orders the run by relative
-// position inside the quad (a proportional interleave: each group of 8 repeats
-// a quad only as often as the quad counts force); runs longer than 128 read the
-// quad-sorted run column-major out of 8 rows instead (linear cost).  The fill left each element's
-// CSR slot in x_csc, so csr_pos is repointed without searching; the values are
-// scattered afterwards.  Deterministic.
-constexpr int kSpreadWarps = 8;
-__global__ void __launch_bounds__(kSpreadWarps * 32) k_csc_spread(const int64_t* __restrict__ tile_base,
-                                                                  const int32_t* __restrict__ colptr, int ntiles, int p,
-                                                                  uint16_t* __restrict__ e_loc,
-                                                                  const uint32_t* __restrict__ slot_of,
-                                                                  uint32_t* __restrict__ csr_pos) {
-  __shared__ uint16_t s_e[kSpreadWarps][kTile];
-  __shared__ uint16_t s_rq[kSpreadWarps][kTile];   // rank inside the quad << 3 | quad
-  __shared__ int s_cnt[kSpreadWarps][8];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t job = (int64_t)blockIdx.x * kSpreadWarps + w;
-  if (job >= (int64_t)ntiles * p) return;
-  const int t = (int)(job / p), pe = (int)(job - (int64_t)t * p);
-  const int32_t* cp = colptr + (int64_t)t * colptr_pitch(p);
-  const int64_t base = tile_base[t] + cp[pe];
-  const int len = cp[pe + 1] - cp[pe];
-  if (len <= 8) return;
-  int cnt[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) cnt[q] = 0;
-  for (int i0 = 0; i0 < len; i0 += 32) {   // warp-uniform trip count: full-mask ballots
-    const int i = i0 + lane;
-    const bool live = i < len;
-    const uint16_t e = live ? e_loc[base + i] : 0;
-    if (live) s_e[w][i] = e;
-    const int q = (e >> 4) & 7;
-#pragma unroll
-    for (int b = 0; b < 8; ++b) cnt[b] += __popc(__ballot_sync(0xffffffffu, live && q == b));
-  }
-  __syncwarp();
-  int seen[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) seen[q] = 0;
-  for (int i0 = 0; i0 < len; i0 += 32) {
-    const int i = i0 + lane;
-    const bool live = i < len;
-    const uint16_t e = live ? s_e[w][i] : 0;
-    const int q = (e >> 4) & 7;
-    int r = 0;
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const unsigned m = __ballot_sync(0xffffffffu, live && q == b);
-      if (q == b) r = seen[b] + __popc(m & ((1u << lane) - 1u));   // stable rank inside the quad
-      seen[b] += __popc(m);
-    }
-    if (live) s_rq[w][i] = (uint16_t)((r << 3) | q);
-  }
-  __syncwarp();
-  if (lane < 8) {
-#pragma unroll
-    for (int b = 0; b < 8; ++b)
-      if (lane == b) s_cnt[w][b] = cnt[b];
-  }
-  __syncwarp();
-  // proportional interleave: element (q, r) sits at the relative position
-  // (r + 1/2) / cnt_q of its quad; the new order sorts those keys (ties by
-  // quad), so every quad is spread evenly and each group of 8 repeats a quad
-  // only as often as the counts force
-  for (int i = lane; i < len; i += 32) {
-    const int rq = s_rq[w][i], q = rq & 7, r2 = 2 * (rq >> 3) + 1;
-    const int cq = s_cnt[w][q];
-    int j = 0;
-    if (len <= 128) {   // O(len^2) ranking: short runs
-      for (int k = 0; k < len; ++k) {
-        const int rk = s_rq[w][k], qk = rk & 7, rk2 = 2 * (rk >> 3) + 1;
-        const int lhs = rk2 * cq, rhs = r2 * s_cnt[w][qk];   // key_k < key_i  <=>  rk2 / cnt_qk < r2 / cq
-        j += (lhs < rhs || (lhs == rhs && qk < q)) ? 1 : 0;
-      }
-    } else {            // long runs: the quad-sorted run read column-major out of 8 rows
-      int st = 0;
-      for (int b = 0; b < q; ++b) st += s_cnt[w][b];
-      const int sidx = st + (rq >> 3);
-      const int c = (len + 7) >> 3, nf = len / c, rem = len - nf * c;
-      const int row = sidx / c, col = sidx - row * c;
-      j = col * nf + min(col, rem) + row;
-    }
-    {
-      const uint16_t e = s_e[w][i];
-      e_loc[base + j] = e;
-      csr_pos[slot_of[base + i]] = (uint32_t)(base + j);
-    }
-  }
+  ix.slot_csc = (uint32_t*)take((size_t)nnz_upper * 4);
+  ix.e_ell = (uint16_t*)take((size_t)ecap * 2);
+  ix.ell_tot = (int32_t*)take((size_t)ntiles * 4);
+  ix.ell_base = (int64_t*)take((size_t)(ntiles + 1) * 8);
+  ix.wave_tot = (int32_t*)take((size_t)ntiles * 4);
+  ix.wave_base = (int64_t*)take((size_t)(ntiles + 1) * 8);
+  ix.wave_off = (uint32_t*)take((size_t)wcap * 4);
+  ix.wave_meta = (uint16_t*)take((size_t)wcap * 2);
+  ix.wave_col = (uint16_t*)take((size_t)wcap * 64);
 }
 
 // Column segments of each tile: sum over columns of ceil(len / kSegCountLen).
@@ -326,6 +251,164 @@ __global__ void k_tile_segs(const int32_t* __restrict__ colptr, int ntiles, int 
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) segs[t] = s;
+}
+
+
+// ---- ELL wave layout (the dictionary step's order) -------------------------
+// Per tile, every non-empty column c (n_c elements) is cut into R_c = pow2ceil(
+// ceil(n_c / kEllRun)) <= 32 runs of balanced length (<= len_c = ceil(n_c/R_c)).
+// Columns are ordered by (R desc, len desc, c) and packed into WAVES of 32 lane
+// runs: a column's runs occupy R_c consecutive lanes of one wave, every wave
+// holds columns of ONE R (a new wave starts where R changes), and the wave's run
+// length Lw is the longest of its runs.  Element j of lane l's run is stored at
+// wave_off + j*32 + l (coalesced for a warp walking the wave); positions past a
+// run's end are padding (W row kEllZeroRow, value 0).  In the dictionary step a
+// lane accumulates its run's Gram / moment sums in registers and the R lanes of
+// a column combine them once per wave (transpose reduction); each column sits in
+// exactly one wave per tile, so flushes never collide.  Deterministic.
+struct EllPlan {
+  int nw;          // waves of the tile
+  int64_t total;   // ELL positions of the tile
+};
+
+__device__ __forceinline__ int ell_runs(int n) {
+  if (n <= 0) return 0;
+  const int q = (n + kEllRun - 1) / kEllRun;
+  int r = 1;
+  while (r < q) r <<= 1;
+  return r < 32 ? r : 32;
+}
+
+// Block-wide plan of tile t in shared memory: s_w / s_l0 per column, s_wlen /
+// s_wlg / s_woff per wave.  Needs blockDim.x threads, p <= blockDim.x * 8.
+__device__ EllPlan ell_plan(const int32_t* __restrict__ cp, int p, int* s_key, int* s_ord, uint16_t* s_w,
+                            uint8_t* s_l0, uint8_t* s_wlen, uint8_t* s_wlg, uint32_t* s_woff) {
+  __shared__ EllPlan res;
+  for (int c = threadIdx.x; c < p; c += blockDim.x) {
+    const int n = cp[c + 1] - cp[c];
+    const int R = ell_runs(n);
+    int lg = 0;
+    while ((1 << lg) < R) ++lg;
+    const int len = R ? (n + R - 1) / R : 0;
+    s_key[c] = n == 0 ? 0x7FFFFFFF : (((5 - lg) << 16) | (kEllRun * 32 - len));
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < p; c += blockDim.x) {
+    const int kc = s_key[c];
+    int rank = 0;
+    for (int d = 0; d < p; ++d) {
+      const int kd = s_key[d];
+      rank += (kd < kc || (kd == kc && d < c)) ? 1 : 0;
+    }
+    s_ord[rank] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int lane = 0, w = -1, cur_lg = -1;
+    int64_t off = 0;
+    for (int i = 0; i < p; ++i) {
+      const int c = s_ord[i];
+      const int n = cp[c + 1] - cp[c];
+      if (n == 0) break;   // empty columns sort last
+      const int R = ell_runs(n);
+      int lg = 0;
+      while ((1 << lg) < R) ++lg;
+      const int len = (n + R - 1) / R;
+      if (w < 0 || lg != cur_lg || lane + R > 32) {   // open a new wave
+        if (w >= 0) off += 32 * (int64_t)s_wlen[w];
+        ++w;
+        lane = 0;
+        cur_lg = lg;
+        s_wlen[w] = 0;
+        s_wlg[w] = (uint8_t)lg;
+        s_woff[w] = (uint32_t)off;
+      }
+      s_w[c] = (uint16_t)w;
+      s_l0[c] = (uint8_t)lane;
+      if (len > s_wlen[w]) s_wlen[w] = (uint8_t)len;
+      lane += R;
+    }
+    if (w >= 0) off += 32 * (int64_t)s_wlen[w];
+    res.nw = w + 1;
+    res.total = off;
+  }
+  __syncthreads();
+  return res;
+}
+
+__host__ __device__ constexpr int ell_smem_bytes(int p) { return p * (4 + 4 + 2 + 1) + (p + 8) * (1 + 1 + 4) + 64; }
+
+__global__ void __launch_bounds__(256) k_ell_count(const int32_t* __restrict__ colptr, int p, int32_t* __restrict__ ell_tot,
+                                                   int32_t* __restrict__ wave_tot) {
+  extern __shared__ __align__(8) unsigned char es[];
+  int* s_key = (int*)es;
+  int* s_ord = s_key + p;
+  uint32_t* s_woff = (uint32_t*)(s_ord + p);
+  uint16_t* s_w = (uint16_t*)(s_woff + p + 8);
+  uint8_t* s_l0 = (uint8_t*)(s_w + p);
+  uint8_t* s_wlen = s_l0 + p;
+  uint8_t* s_wlg = s_wlen + p + 8;
+  const EllPlan pl = ell_plan(colptr + (int64_t)blockIdx.x * colptr_pitch(p), p, s_key, s_ord, s_w, s_l0, s_wlen,
+                              s_wlg, s_woff);
+  if (threadIdx.x == 0) {
+    ell_tot[blockIdx.x] = (int32_t)pl.total;
+    wave_tot[blockIdx.x] = pl.nw;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_ell_fill(const int64_t* __restrict__ tile_base, const int32_t* __restrict__ colptr,
+                                                  int p, const uint16_t* __restrict__ e_loc,
+                                                  const uint32_t* __restrict__ slot_csc,
+                                                  const int64_t* __restrict__ ell_base, const int64_t* __restrict__ wave_base,
+                                                  uint16_t* __restrict__ e_ell, float* __restrict__ x_ell,
+                                                  uint32_t* __restrict__ csr_pos, uint32_t* __restrict__ wave_off,
+                                                  uint16_t* __restrict__ wave_meta, uint16_t* __restrict__ wave_col) {
+  extern __shared__ __align__(8) unsigned char es[];
+  int* s_key = (int*)es;
+  int* s_ord = s_key + p;
+  uint32_t* s_woff = (uint32_t*)(s_ord + p);
+  uint16_t* s_w = (uint16_t*)(s_woff + p + 8);
+  uint8_t* s_l0 = (uint8_t*)(s_w + p);
+  uint8_t* s_wlen = s_l0 + p;
+  uint8_t* s_wlg = s_wlen + p + 8;
+  const int t = blockIdx.x;
+  const int32_t* cp = colptr + (int64_t)t * colptr_pitch(p);
+  const EllPlan pl = ell_plan(cp, p, s_key, s_ord, s_w, s_l0, s_wlen, s_wlg, s_woff);
+  const int64_t eb = ell_base[t], wb = wave_base[t], tb = tile_base[t];
+  // padding everywhere, then the real elements on top
+  for (int64_t i = threadIdx.x; i < pl.total; i += blockDim.x) {
+    e_ell[eb + i] = (uint16_t)kEllZeroRow;
+    x_ell[eb + i] = 0.0f;
+  }
+  for (int w = threadIdx.x; w < pl.nw; w += blockDim.x) {
+    wave_off[wb + w] = s_woff[w];
+    wave_meta[wb + w] = (uint16_t)(s_wlen[w] | (s_wlg[w] << 8));
+  }
+  for (int i = threadIdx.x; i < pl.nw * 32; i += blockDim.x) wave_col[(wb + i / 32) * 32 + (i & 31)] = 0xFFFFu;
+  __syncthreads();
+  for (int c = threadIdx.x; c < p; c += blockDim.x) {
+    const int n = cp[c + 1] - cp[c];
+    if (!n) continue;
+    const int R = ell_runs(n);
+    for (int r = 0; r < R; ++r) wave_col[(wb + s_w[c]) * 32 + s_l0[c] + r] = (uint16_t)c;
+  }
+  // elements: column of each tile element by binary search in the column pointers
+  const int nt = cp[p];
+  for (int e = threadIdx.x; e < nt; e += blockDim.x) {
+    int lo = 0, hi = p - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (cp[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    const int c = lo, n = cp[c + 1] - cp[c], q = e - cp[c];
+    const int R = ell_runs(n), base = n / R, rem = n % R;
+    int r, j;
+    if (q < rem * (base + 1)) { r = q / (base + 1); j = q - r * (base + 1); }
+    else { const int q2 = q - rem * (base + 1); r = rem + q2 / base; j = q2 - (r - rem) * base; }
+    const int64_t pos = eb + s_woff[s_w[c]] + (int64_t)j * 32 + s_l0[c] + r;
+    e_ell[pos] = e_loc[tb + e];
+    csr_pos[slot_csc[tb + e]] = (uint32_t)pos;
+  }
 }
 
 // Histogram of the per-patch observed counts (0..p): shared-memory bins per block.
@@ -394,14 +477,20 @@ int launch_build_index(PatchIndex& ix, const uint8_t* obs, const float* values, 
   k_tile_totals<<<ix.ntiles, 256, 0, st>>>(counts, ix.n, ix.tile_tot, ix.cmax_dev);
   k_tile_scan<<<1, 1024, 0, st>>>(ix.tile_tot, ix.ntiles, ix.tile_base);
   k_tile_fill<<<ix.ntiles, kFillThreads, 0, st>>>(obs, values, counts, ix.n, ix.p, ix.tile_base, ix.colptr, ix.e_loc,
-                                           ix.x_csc, ix.rowptr, ix.csr_p, ix.csr_pos);
-  {
-    const int spread = !PB_TUNE_INT("PB_INDEX_NO_SPREAD", 0);   // 0: ascending patch order inside columns (A/B)
-    if (spread)
-      k_csc_spread<<<(unsigned)ceil_div((int64_t)ix.ntiles * ix.p, kSpreadWarps), kSpreadWarps * 32, 0, st>>>(
-          ix.tile_base, ix.colptr, ix.ntiles, ix.p, ix.e_loc, (const uint32_t*)ix.x_csc, ix.csr_pos);
+                                           ix.slot_csc, ix.rowptr, ix.csr_p, ix.csr_pos);
+  // the ELL wave layout (the dictionary step's order): plan, prefix, fill
+  const size_t esm = ell_smem_bytes(ix.p);
+  if (esm > 48 * 1024) {
+    PB_CUDA_TRY(cudaFuncSetAttribute(k_ell_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm));
+    PB_CUDA_TRY(cudaFuncSetAttribute(k_ell_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm));
   }
-  // the observed values into the (final) CSC order
+  k_ell_count<<<ix.ntiles, 256, esm, st>>>(ix.colptr, ix.p, ix.ell_tot, ix.wave_tot);
+  k_tile_scan<<<1, 1024, 0, st>>>(ix.ell_tot, ix.ntiles, ix.ell_base);
+  k_tile_scan<<<1, 1024, 0, st>>>(ix.wave_tot, ix.ntiles, ix.wave_base);
+  k_ell_fill<<<ix.ntiles, 256, esm, st>>>(ix.tile_base, ix.colptr, ix.p, ix.e_loc, ix.slot_csc, ix.ell_base,
+                                          ix.wave_base, ix.e_ell, ix.x_csc, ix.csr_pos, ix.wave_off, ix.wave_meta,
+                                          ix.wave_col);
+  // the observed values into the ELL order
   k_scatter_x<<<(unsigned)ceil_div(ix.n, 256), 256, 0, st>>>(values, counts, ix.rowptr, ix.csr_p, ix.csr_pos, ix.n,
                                                              ix.x_csc);
   k_tile_segs<<<(unsigned)ceil_div(ix.ntiles, 8), 256, 0, st>>>(ix.colptr, ix.ntiles, ix.p, ix.tile_segs);

@@ -11,6 +11,17 @@ constexpr int kSegCountLen = 256;  // segment length of the dictionary step's el
 
 __host__ __device__ constexpr int colptr_pitch(int p) { return (p + 1 + 3) & ~3; }
 
+// ---- ELL wave layout of the dictionary step (see pb_index.cu) ----
+constexpr int kEllRun = 32;                 // max elements of one lane's run
+constexpr uint32_t kEllZeroRow = 32768u;    // W-row byte offset of the zero row behind each staged block
+// upper bounds of the ELL element and wave counts (padding included)
+__host__ __device__ inline int64_t ell_cap(int64_t n, int64_t nnz) {
+  return 2 * nnz + 6144 * ((n + kTile - 1) / kTile) + 1024;
+}
+__host__ __device__ inline int64_t wave_cap(int64_t n, int p, int64_t nnz) {
+  return ((n + kTile - 1) / kTile) * (8 + (2 * p + 31) / 32) + 2 * nnz / 1024 + 1;
+}
+
 // Byte offset of patch row il's first 16-byte chunk inside a tile block of the
 // code copy W ([kTile][kWB] floats); the second chunk is at (offset ^ 16).
 // Chunks are XOR-swizzled across each 128-byte line (4 rows) so gathers of
@@ -38,6 +49,16 @@ struct PatchIndex {
   int32_t* hist;        // [p + 1] histogram of the observed counts
   int32_t* tile_segs;   // [ntiles] column segments of each tile (columns cut every kSegCountLen elements)
   int64_t* seg_base;    // [ntiles + 1] prefix of tile_segs (the dictionary step's work-split cost model)
+  // ELL wave layout (the dictionary step's order; x_csc and the residual live in it)
+  uint32_t* slot_csc;   // [nnz] CSC scratch: CSR slot of each CSC element
+  uint16_t* e_ell;      // [ell_cap] W-row byte offset per ELL position (kEllZeroRow for padding)
+  int32_t* ell_tot;     // [ntiles] ELL positions of each tile (padding included)
+  int64_t* ell_base;    // [ntiles + 1]
+  int32_t* wave_tot;    // [ntiles] waves of each tile
+  int64_t* wave_base;   // [ntiles + 1] first global wave of each tile
+  uint32_t* wave_off;   // [waves] first ELL position of the wave, relative to its tile's ell_base
+  uint16_t* wave_meta;  // [waves] run length Lw | log2(lanes per column) << 8
+  uint16_t* wave_col;   // [waves][32] column of each lane's run (0xFFFF: idle lane)
 };
 
 int index_bytes(int64_t n, int p, int64_t nnz, size_t* out);
