@@ -392,22 +392,39 @@ __global__ void __launch_bounds__(256) k_ell_fill(const int64_t* __restrict__ ti
     const int R = ell_runs(n);
     for (int r = 0; r < R; ++r) wave_col[(wb + s_w[c]) * 32 + s_l0[c] + r] = (uint16_t)c;
   }
-  // elements: column of each tile element by binary search in the column pointers
-  const int nt = cp[p];
-  for (int e = threadIdx.x; e < nt; e += blockDim.x) {
-    int lo = 0, hi = p - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (cp[mid] <= e) lo = mid; else hi = mid - 1;
+  // elements, bank-spread: a column's elements form a sequence t = 0..n-1 with
+  // element t in run t % R at step t / R (lane lane0 + t % R).  Rows land on one
+  // of 8 shared-memory bank quads ((e >> 4) & 7); sequence slot t asks for quad
+  // (t + lane0) & 7 — at every step the 8 lanes of a quarter-warp then ask for 8
+  // different quads — and takes the next unused element of that quad, else of
+  // the quad with the most elements left.  One thread per column; deterministic.
+  for (int c = threadIdx.x; c < p; c += blockDim.x) {
+    const int n = cp[c + 1] - cp[c];
+    if (!n) continue;
+    const int R = ell_runs(n), l0 = s_l0[c];
+    const int64_t cb = tb + cp[c];
+    const int64_t wpos = eb + s_woff[s_w[c]] + l0;
+    int left[8], cur[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) { left[q] = 0; cur[q] = 0; }
+    for (int i = 0; i < n; ++i) ++left[(e_loc[cb + i] >> 4) & 7];
+    for (int t = 0; t < n; ++t) {
+      int q = (t + l0) & 7;
+      if (!left[q]) {
+        int best = 0;
+#pragma unroll
+        for (int b = 1; b < 8; ++b)
+          if (left[b] > left[best]) best = b;
+        q = best;
+      }
+      int i = cur[q];
+      while (((e_loc[cb + i] >> 4) & 7) != q) ++i;
+      cur[q] = i + 1;
+      --left[q];
+      const int64_t pos = wpos + (int64_t)(t / R) * 32 + (t % R);
+      e_ell[pos] = e_loc[cb + i];
+      csr_pos[slot_csc[cb + i]] = (uint32_t)pos;
     }
-    const int c = lo, n = cp[c + 1] - cp[c], q = e - cp[c];
-    const int R = ell_runs(n), base = n / R, rem = n % R;
-    int r, j;
-    if (q < rem * (base + 1)) { r = q / (base + 1); j = q - r * (base + 1); }
-    else { const int q2 = q - rem * (base + 1); r = rem + q2 / base; j = q2 - (r - rem) * base; }
-    const int64_t pos = eb + s_woff[s_w[c]] + (int64_t)j * 32 + s_l0[c] + r;
-    e_ell[pos] = e_loc[tb + e];
-    csr_pos[slot_csc[tb + e]] = (uint32_t)pos;
   }
 }
 
