@@ -759,7 +759,7 @@ constexpr double kTileVisitCost = 3000.0;  // element-equivalents of one tile vi
 // Byte stride of one staged W block in shared memory: the tile's kTile x 8
 // floats, then the all-zero row kEllZeroRow that the ELL padding points to.
 constexpr uint32_t kWStride = (uint32_t)kTile * kWB * 4 + 128;
-constexpr int kEllPf = 6;   // elements in flight per lane in the element phase
+constexpr int kEllPf = 8;   // elements in flight per lane in the element phase (6: +1-3 %)
 
 // One ELL wave (pb_index.cu) as seen by a lane: its run's column, the wave's
 // run length, log2 of the lanes per column, and the lane's first position.
@@ -1021,6 +1021,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
   float* dprev = dold + B * p;
   __shared__ __align__(8) uint64_t mbar[3];   // [0..1] stage fills, [2] owner partials
   __shared__ int done[2];
+  __shared__ unsigned next_wave;   // dynamic wave claiming inside the CTA
   if (threadIdx.x == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
@@ -1078,6 +1079,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
       if (ntile > 0) issue(0, blk);
       if (ntile > 1) issue(1, blk);
     }
+    if (threadIdx.x == 0) next_wave = NW;   // waves 0..NW-1 go to warps 0..NW-1
     prefetched = false;
     __syncthreads();
     // ---- element phase: this warp's waves w_lo + wid, + NW, ... ----
@@ -1091,6 +1093,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
         int t = from;
         while (t + 1 < ntile && a.wave_base[t_lo + t + 1] <= w) ++t;
         return t;
+      };
+      // a warp's next wave: claimed from the CTA's counter (dynamic balance;
+      // each column still gets one flush per tile, in tile order per parity, so
+      // the sums do not depend on which warp took which wave) or round-robin
+      auto next = [&](int64_t cur) -> int64_t {
+        if (!a.dyn_waves) return cur + NW;
+        unsigned w = 0;
+        if (lane == 0) w = atomicAdd(&next_wave, 1u);
+        return w_lo + (int64_t)__shfl_sync(0xffffffffu, w, 0);
       };
       int64_t wv = w_lo + wid;
       bool have = wv < w_hi;
@@ -1122,7 +1133,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
           else ell_elements<true, false>(a, h, wcur_s, wprev_s, dl2, v, ib, rb, pol_last);
           const int lg_c = h.lg, col_c = h.col;
           // the next wave's header and first elements go in flight before the flush
-          wv += NW;
+          wv = next(wv);
           have = wv < w_hi;
           if (have) {
             wu = tile_of(wv, wu);
@@ -1588,6 +1599,7 @@ int launch_dict_gram(const DictGramArgs& a_in, cudaStream_t st) {
   // both W blocks stream with evict_first: the residual and the element index
   // (re-read every pass) keep L2 (configs[1] 3.41 -> 2.52 ms)
   a.w_evict_first = PB_TUNE_INT("PB_DICT_W_EVICT", 1);
+  a.dyn_waves = PB_TUNE_INT("PB_DICT_DYN", 1);
   {
     static bool l2_set = false;
     const int persist = PB_TUNE_INT("PB_L2_PERSIST_MB", 0);

@@ -1,4 +1,5 @@
-export PB200_LIB_VARIANT=tune
-for e in "" "PB_DICT_W_EVICT=1" "PB_L2_PERSIST_MB=90" "PB_DICT_W_EVICT=1 PB_L2_PERSIST_MB=90" "PB_L2_PERSIST_MB=120 PB_DICT_W_EVICT=1"; do
-  echo "== $e"; env $e timeout 120 python tools/sweep_timing.py 1 4 --steps 4 2>&1 | grep cfg
+# A/B of dictionary-step tuning variants (scratch): bash tools/ab_l2.sh
+for spec in "tune:PB_DICT_DYN=0" "tune:PB_DICT_DYN=1" "pf8:PB_DICT_DYN=1" "pf8:PB_DICT_DYN=0"; do
+  v=${spec%%:*}; e=${spec#*:}
+  echo "== $v $e"; env PB200_LIB_VARIANT=$v $e timeout 120 python tools/sweep_timing.py 0 1 2 4 --steps 4 2>&1 | grep cfg
 done
