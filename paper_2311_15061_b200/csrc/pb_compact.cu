@@ -789,29 +789,69 @@ __device__ __forceinline__ void ell_prefetch(const DictGramArgs& a, const EllWav
   }
 }
 
+// compile-time loop: f(integral_constant<int, 0>) ... f(integral_constant<int, N-1>)
+template <int N, int I = 0, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    static_for<N, I + 1>(f);
+  }
+}
+
+// Loads / stores at a compile-time byte offset from a base register ([reg+imm]
+// addressing: no per-element address arithmetic in the unrolled element loop).
+template <int OFF>
+__device__ __forceinline__ uint16_t ldg_u16_off(const uint16_t* p, uint64_t pol) {
+  uint16_t v;
+  asm volatile("ld.global.L2::cache_hint.u16 %0, [%1+%3], %2;" : "=h"(v) : "l"(p), "l"(pol), "n"(OFF));
+  return v;
+}
+template <int OFF>
+__device__ __forceinline__ float ldg_f32_off(const float* p, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.L2::cache_hint.f32 %0, [%1+%3], %2;" : "=f"(v) : "l"(p), "l"(pol), "n"(OFF));
+  return v;
+}
+template <int OFF>
+__device__ __forceinline__ void stg_f32_off(float* p, float v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0+%3], %1, %2;" ::"l"(p), "f"(v), "l"(pol), "n"(OFF) : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ float4 lds128_off(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+%5];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr), "n"(OFF));
+  return v;
+}
+
 // Element phase of one ELL wave: the lane walks its run of column h.col (stride
 // 32, coalesced), applies the previous block's shifts to the residual and
 // accumulates the block's Gram / moment sums in registers.  Padding positions
-// point at the zero W row and carry r = 0: no per-element tests.
+// point at the zero W row and carry r = 0: no per-element tests beyond the
+// wave's length.  The previous block's W is staged kWStride bytes after the
+// current one.
 template <bool HP, bool HC>
-__device__ __forceinline__ void ell_elements(const DictGramArgs& a, const EllWave& h, uint32_t wcur_s, uint32_t wprev_s,
+__device__ __forceinline__ void ell_elements(const DictGramArgs& a, const EllWave& h, uint32_t wcur_s,
                                              const float2 (&dl2)[kWB / 2], float (&v)[GramLayout<kWB>::NP],
                                              uint32_t (&ib)[kEllPf], float (&rb)[kEllPf], uint64_t pol) {
   using L = GramLayout<kWB>;
   constexpr int B = kWB;
-  const uint16_t* ep = a.e_ell + h.base;
-  float* rp = a.r_csc + h.base;
+  const uint32_t wprev_s = wcur_s + kWStride;
+  // chunk base pointers (advanced once per kEllPf positions): the unrolled
+  // accesses below are [base + immediate]
+  const uint16_t* __restrict__ ep = a.e_ell + h.base;
+  float* __restrict__ rp = a.r_csc + h.base;
   const int lw = h.lw;
-  for (int j0 = 0; j0 < lw; j0 += kEllPf) {
+  for (int j0 = 0; j0 < lw; j0 += kEllPf, ep += kEllPf * 32, rp += kEllPf * 32) {
+    const int more = lw - j0 - kEllPf;   // positions left after this chunk
 #pragma unroll
     for (int d = 0; d < kEllPf; ++d) {
-      const int j = j0 + d;
-      if (j >= lw) break;
+      if (j0 + d >= lw) break;
       const uint32_t il = ib[d];
       float r = rb[d];
-      if (j + kEllPf < lw) {
-        ib[d] = ldg_hint(ep + (j + kEllPf) * 32, pol);
-        rb[d] = ldg_hint(rp + (j + kEllPf) * 32, pol);
+      if (d < more) {
+        ib[d] = __ldg(ep + (kEllPf + d) * 32);
+        rb[d] = rp[(kEllPf + d) * 32];
       }
       const uint32_t wo[2] = {il, il ^ 16u};
       if constexpr (HP) {  // r += w_prev . delta  (packed pairs, two independent chains)
@@ -824,7 +864,7 @@ __device__ __forceinline__ void ell_elements(const DictGramArgs& a, const EllWav
         }
 #pragma unroll
         for (int q = 0; q < B / 4; ++q) r += sh[q].x + sh[q].y;
-        stg_hint(rp + j * 32, r, pol);
+        rp[d * 32] = r;
       }
       if constexpr (HC) {
         float wc[B];
@@ -1128,9 +1168,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
           float v[L::NP];
 #pragma unroll
           for (int q = 0; q < L::NP; ++q) v[q] = 0.0f;
-          if (has_prev && has_cur) ell_elements<true, true>(a, h, wcur_s, wprev_s, dl2, v, ib, rb, pol_last);
-          else if (has_cur) ell_elements<false, true>(a, h, wcur_s, wprev_s, dl2, v, ib, rb, pol_last);
-          else ell_elements<true, false>(a, h, wcur_s, wprev_s, dl2, v, ib, rb, pol_last);
+          if (has_prev && has_cur) ell_elements<true, true>(a, h, wcur_s, dl2, v, ib, rb, pol_last);
+          else if (has_cur) ell_elements<false, true>(a, h, wcur_s, dl2, v, ib, rb, pol_last);
+          else ell_elements<true, false>(a, h, wcur_s, dl2, v, ib, rb, pol_last);
           const int lg_c = h.lg, col_c = h.col;
           // the next wave's header and first elements go in flight before the flush
           wv = next(wv);
@@ -1256,9 +1296,9 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
         float v[L::NP];
 #pragma unroll
         for (int q = 0; q < L::NP; ++q) v[q] = 0.0f;
-        if (has_prev && has_cur) ell_elements<true, true>(a, h, wcur_s, wprev_s, dl2, v, ib, rb, pol_last);
-        else if (has_cur) ell_elements<false, true>(a, h, wcur_s, wprev_s, dl2, v, ib, rb, pol_last);
-        else ell_elements<true, false>(a, h, wcur_s, wprev_s, dl2, v, ib, rb, pol_last);
+        if (has_prev && has_cur) ell_elements<true, true>(a, h, wcur_s, dl2, v, ib, rb, pol_last);
+        else if (has_cur) ell_elements<false, true>(a, h, wcur_s, dl2, v, ib, rb, pol_last);
+        else ell_elements<true, false>(a, h, wcur_s, dl2, v, ib, rb, pol_last);
         if (has_cur) ell_flush(v, h.lg, h.col, lane, acc);
       }
     }
