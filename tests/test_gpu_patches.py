@@ -151,11 +151,19 @@ def _carve(buf, n, p, nnz):
     """Mirror of carve_index (pb_index.cu) to read the index back for checking."""
     kt = 1024
     nt = -(-n // kt)
+    ecap = 2 * nnz + 6144 * nt + 1024                              # ell_cap
+    wcap = nt * (8 + (2 * p + 31) // 32) + 2 * nnz // 1024 + 1     # wave_cap
     out, off = {}, 0
     for name, cnt, dt in [("tile_tot", nt, np.int32), ("tile_base", nt + 1, np.int64),
                           ("colptr", nt * ((p + 1 + 3) & ~3), np.int32), ("rowptr", n + 1, np.int64),
-                          ("e_loc", nnz, np.uint16), ("x_csc", nnz, np.float32), ("csr_p", nnz, np.uint16),
-                          ("csr_pos", nnz, np.uint32)]:
+                          ("e_loc", nnz, np.uint16), ("x_csc", ecap, np.float32), ("csr_p", nnz, np.uint16),
+                          ("csr_pos", nnz, np.uint32), ("cmax", 16, np.int32), ("outliers", n, np.int32),
+                          ("out_tot", nt, np.int32), ("out_base", nt + 1, np.int64), ("hist", p + 2, np.int32),
+                          ("tile_segs", nt, np.int32), ("seg_base", nt + 1, np.int64),
+                          ("slot_csc", nnz, np.uint32), ("e_ell", ecap, np.uint16), ("ell_tot", nt, np.int32),
+                          ("ell_base", nt + 1, np.int64), ("wave_tot", nt, np.int32), ("wave_base", nt + 1, np.int64),
+                          ("wave_off", wcap, np.uint32), ("wave_meta", wcap, np.uint16),
+                          ("wave_col", wcap * 32, np.uint16)]:
         nb = cnt * np.dtype(dt).itemsize
         out[name] = buf[off:off + nb].view(dt)
         off += (nb + 255) & ~255
@@ -165,8 +173,15 @@ def _carve(buf, n, p, nnz):
 @pytest.mark.parametrize("shape,patch,ratio,kind", [((40, 45), (8, 8), 0.25, "uniform-random"),
                                                      ((70, 64), (8, 8), 0.25, "line-hop"),
                                                      ((50, 41), (10, 10), 0.1, "uniform-random"),
-                                                     ((12, 10, 6), (4, 3, 6), 0.3, "uniform-random")])
+                                                     ((12, 10, 6), (4, 3, 6), 0.3, "uniform-random"),
+                                                     ((300, 40), (10, 10), 0.1, "uniform-random")])
 def test_observed_element_index_exact(cuda_device, shape, patch, ratio, kind):
+    """The observed-element index (pb_index.cu) element by element: the CSR
+    view (ascending offsets per patch), and the dictionary step's ELL wave
+    layout — every observed element at exactly one position of its tile's
+    range, in a lane whose run belongs to its column, each column in one wave
+    per tile on R aligned lanes (uniform R per wave), padding pointing at the
+    zero W row with value 0, and bank-spread quarter-warp steps."""
     from paper_2311_15061_b200 import inputs
 
     rng = np.random.default_rng(0)
@@ -178,32 +193,64 @@ def test_observed_element_index_exact(cuda_device, shape, patch, ratio, kind):
     n, p = obs.shape
     assert ix.nnz == obs.sum() and ix.cmax == obs.sum(1).max()
     b = _carve(pm._cache["ix_buf"].cpu().numpy(), n, p, int(ix.nnz))
-    # CSR: per patch, ascending observed offsets; positions point at the same element in CSC
     rows, cols = np.nonzero(obs)          # row-major => ascending (i, p)
     assert np.array_equal(b["csr_p"].astype(np.int64), cols)
     assert np.array_equal(b["rowptr"][:n], np.concatenate([[0], np.cumsum(obs.sum(1))[:-1]]))
     pos = b["csr_pos"].astype(np.int64)
-    assert np.array_equal(np.sort(pos), np.arange(ix.nnz))
+    nell = int(b["ell_base"][-1])
+    assert nell == ix.nnz_ell and len(np.unique(pos)) == len(pos) and pos.max(initial=0) < nell
     tile = rows // 1024
-    assert np.array_equal(b["e_loc"][pos].astype(np.int64), _w_row_off(rows - tile * 1024))
+    assert np.array_equal(b["e_ell"][pos].astype(np.int64), _w_row_off(rows - tile * 1024))
     assert np.array_equal(b["x_csc"][pos], vals[rows, cols].astype(np.float32))
-    tb = b["tile_base"].astype(np.int64)
-    cp = b["colptr"].reshape(-1, (p + 1 + 3) & ~3)[:, :p + 1].astype(np.int64) + tb[:-1, None]  # tile-relative
-    assert np.all((pos >= cp[tile, cols]) & (pos < cp[tile, cols + 1]))
-    # CSC order inside a column: a bank-spread permutation of the column's
-    # patches (k_csc_spread) — every aligned 8-element group hits the W-row bank
-    # quads at least as evenly as ascending patch order would
-    worst_new = worst_asc = 0
-    for t in range(cp.shape[0]):
-        for pe in range(p):
-            e = b["e_loc"][cp[t, pe]:cp[t, pe + 1]].astype(np.int64)
-            seg = _w_row_index(e)
-            assert len(np.unique(seg)) == len(seg)
-            asc = _w_row_off(np.sort(seg))
-            for order, acc in ((e, "new"), (asc, "asc")):
-                m = sum(np.bincount((order[g:g + 8] >> 4) & 7, minlength=8).max() for g in range(0, len(order), 8))
-                if acc == "new":
-                    worst_new += m
-                else:
-                    worst_asc += m
-    assert worst_new <= worst_asc
+    eb, wb = b["ell_base"].astype(np.int64), b["wave_base"].astype(np.int64)
+    assert np.all((pos >= eb[tile]) & (pos < eb[tile + 1]))
+    pad = np.ones(nell, bool)
+    pad[pos] = False
+    assert np.all(b["e_ell"][:nell][pad] == 32768) and np.all(b["x_csc"][:nell][pad] == 0)
+    # wave of each element and its lane's column
+    woff, meta, wcol = b["wave_off"].astype(np.int64), b["wave_meta"].astype(np.int64), b["wave_col"].astype(np.int64)
+    rel = pos - eb[tile]
+    for t in np.unique(tile):
+        ws = np.arange(wb[t], wb[t + 1])
+        sel = tile == t
+        w = ws[np.searchsorted(woff[ws], rel[sel], side="right") - 1]
+        lane = (rel[sel] - woff[w]) % 32
+        step = (rel[sel] - woff[w]) // 32
+        assert np.all(step < (meta[w] & 0xFF))
+        assert np.array_equal(wcol[w * 32 + lane], cols[sel])
+        cols_seen = []
+        for wv in ws:
+            c = wcol[wv * 32:(wv + 1) * 32]
+            r = 1 << (meta[wv] >> 8)
+            for g in range(0, 32, r):
+                grp = c[g:g + r]
+                assert np.all(grp == grp[0]), (wv, g, grp)
+                if grp[0] != 0xFFFF:
+                    cols_seen.append(int(grp[0]))
+        assert len(cols_seen) == len(set(cols_seen))      # one wave per column per tile
+    # bank spreading: W-row bank quads inside each quarter-warp step (1 = conflict
+    # free) against the same runs filled in ascending patch order
+    def quarter_cost(blk):
+        cost = 0
+        for qtr in range(4):
+            e = blk[:, 8 * qtr: 8 * qtr + 8]
+            for jj in range(e.shape[0]):
+                q = (e[jj][e[jj] != 32768] >> 4) & 7
+                cost += np.bincount(q, minlength=8).max() if len(q) else 0
+        return cost
+
+    spread = ascending = 0
+    for t in range(len(wb) - 1):
+        for wv in range(wb[t], wb[t + 1]):
+            lw = int(meta[wv] & 0xFF)
+            blk = b["e_ell"][eb[t] + woff[wv]: eb[t] + woff[wv] + 32 * lw].astype(np.int64).reshape(lw, 32)
+            asc = np.full_like(blk, 32768)
+            r = 1 << (meta[wv] >> 8)
+            for g in range(0, 32, r):
+                el = blk[:, g:g + r].ravel()
+                el = _w_row_off(np.sort(_w_row_index(el[el != 32768])))
+                for k, e in enumerate(el):
+                    asc[k // r, g + k % r] = e
+            spread += quarter_cost(blk)
+            ascending += quarter_cost(asc)
+    assert spread <= ascending, (spread, ascending)
