@@ -789,6 +789,21 @@ __device__ __forceinline__ void ell_prefetch(const DictGramArgs& a, const EllWav
   }
 }
 
+// 16-byte shared load the compiler may schedule freely (not volatile): the
+// address must derive from a value produced after the mbarrier wait that
+// guards the staged data (see ell_stage_addr), so it cannot be hoisted above it
+__device__ __forceinline__ float4 lds128_nv(uint32_t addr) {
+  float4 v;
+  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+// the stage's shared address, re-derived after the mbarrier wait (opaque copy)
+__device__ __forceinline__ uint32_t ell_stage_addr(uint32_t a) {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %1;" : "=r"(r) : "r"(a) : "memory");
+  return r;
+}
+
 // compile-time loop: f(integral_constant<int, 0>) ... f(integral_constant<int, N-1>)
 template <int N, int I = 0, typename F>
 __device__ __forceinline__ void static_for(F&& f) {
@@ -830,6 +845,11 @@ __device__ __forceinline__ float4 lds128_off(uint32_t addr) {
 // point at the zero W row and carry r = 0: no per-element tests beyond the
 // wave's length.  The previous block's W is staged kWStride bytes after the
 // current one.
+#ifndef PB_ELL_LDS_VOLATILE
+#define LDS_W lds128_nv
+#else
+#define LDS_W lds128
+#endif
 template <bool HP, bool HC>
 __device__ __forceinline__ void ell_elements(const DictGramArgs& a, const EllWave& h, uint32_t wcur_s,
                                              const float2 (&dl2)[kWB / 2], float (&v)[GramLayout<kWB>::NP],
@@ -858,7 +878,7 @@ __device__ __forceinline__ void ell_elements(const DictGramArgs& a, const EllWav
         float2 sh[B / 4];
 #pragma unroll
         for (int q = 0; q < B / 4; ++q) {
-          const float4 w4 = lds128(wprev_s + wo[q]);
+          const float4 w4 = LDS_W(wprev_s + wo[q]);
           sh[q] = __fmul2_rn(make_float2(w4.x, w4.y), dl2[2 * q]);
           sh[q] = __ffma2_rn(make_float2(w4.z, w4.w), dl2[2 * q + 1], sh[q]);
         }
@@ -870,7 +890,7 @@ __device__ __forceinline__ void ell_elements(const DictGramArgs& a, const EllWav
         float wc[B];
 #pragma unroll
         for (int q = 0; q < B / 4; ++q) {
-          const float4 w4 = lds128(wcur_s + wo[q]);
+          const float4 w4 = LDS_W(wcur_s + wo[q]);
           wc[4 * q + 0] = w4.x; wc[4 * q + 1] = w4.y; wc[4 * q + 2] = w4.z; wc[4 * q + 3] = w4.w;
         }
         const float2 rr2 = make_float2(r, r);
@@ -1156,7 +1176,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
       }
       for (int u = 0; u < ntile; ++u) {
         mbar_wait(&mbar[u & 1], fill_parity(u));
-        const uint32_t wcur_s = sbase + (uint32_t)(u & 1) * 2 * kWStride, wprev_s = wcur_s + kWStride;
+        const uint32_t wcur_s = ell_stage_addr(sbase + (uint32_t)(u & 1) * 2 * kWStride);
         float* acc = (u & 1) ? acc1 : acc0;
         while (have && wu == u) {
           float2 dl2[B / 2];
@@ -1232,7 +1252,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
   float* dold = acc + (size_t)p * L::NACC;               // B * p
   float* dprev = dold + B * p;                           // B * p
   __shared__ __align__(8) uint64_t mbar[2];   // [0] staging, [1] owner partials
-  const uint32_t wcur_s = smem_u32(smraw), wprev_s = wcur_s + kWStride;
+  const uint32_t wcur_s = smem_u32(smraw);
   if (threadIdx.x == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
@@ -1282,6 +1302,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
       const int64_t tile_ell = a.ell_base[tile];
       mbar_wait(&mbar[0], sphase);
       sphase ^= 1u;
+      const uint32_t wst = ell_stage_addr(wcur_s);   // (loads of the stage stay behind the wait)
       for (int64_t wv = wa + wid; wv < wb; wv += NW) {
         const EllWave h = ell_header(a, wv, tile_ell, lane);
         uint32_t ib[kEllPf];
@@ -1296,9 +1317,9 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
         float v[L::NP];
 #pragma unroll
         for (int q = 0; q < L::NP; ++q) v[q] = 0.0f;
-        if (has_prev && has_cur) ell_elements<true, true>(a, h, wcur_s, dl2, v, ib, rb, pol_last);
-        else if (has_cur) ell_elements<false, true>(a, h, wcur_s, dl2, v, ib, rb, pol_last);
-        else ell_elements<true, false>(a, h, wcur_s, dl2, v, ib, rb, pol_last);
+        if (has_prev && has_cur) ell_elements<true, true>(a, h, wst, dl2, v, ib, rb, pol_last);
+        else if (has_cur) ell_elements<false, true>(a, h, wst, dl2, v, ib, rb, pol_last);
+        else ell_elements<true, false>(a, h, wst, dl2, v, ib, rb, pol_last);
         if (has_cur) ell_flush(v, h.lg, h.col, lane, acc);
       }
     }
