@@ -13,6 +13,8 @@
 // is a gather (one thread per output element, coverage computed analytically),
 // so it is deterministic and atomic-free; neighbouring output elements read
 // neighbouring patches at the same offset -> coalesced.  Both are HBM-bound.
+#include <algorithm>
+
 #include "pb_sweep.cuh"
 
 namespace pb {
@@ -186,6 +188,118 @@ __global__ void k_coverage(Geo4 g, int32_t* __restrict__ out) {
   }
 }
 
+
+// ---- rank-2 fast paths (2-D frames: configs[0..2], [4], the live path) ----
+// Extraction: a CTA takes a 8 x 32 tile of patch origins, stages the tensor /
+// mask window those patches cover into shared memory once (coalesced row
+// reads; 17 x 41 elements for 10x10 patches instead of 256 x 100 scattered
+// re-reads), then each thread builds its patch from shared memory: observed
+// count and f64 observed-only sum, then the plane-major (P, N) row writes
+// (each warp store a contiguous 128 B line of one plane).
+struct Geo2 {
+  int64_t m0, m1, gc0, gc1, n;
+  int b0, b1, s0, s1, p, w0, w1;
+};
+constexpr int kXR = 8, kXC = 32;   // origin tile of the 2-D extraction
+
+static Geo2 make_geo2(const Grid& g) {
+  Geo2 o;
+  o.m0 = g.tshape[0]; o.m1 = g.tshape[1];
+  o.gc0 = g.gcount[0]; o.gc1 = g.gcount[1];
+  o.n = g.n;
+  o.b0 = g.bshape[0]; o.b1 = g.bshape[1];
+  o.s0 = g.step[0]; o.s1 = g.step[1];
+  o.p = g.p;
+  o.w0 = (kXR - 1) * o.s0 + o.b0;
+  o.w1 = (kXC - 1) * o.s1 + o.b1;
+  return o;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kXR * kXC) k_extract2d(Geo2 g, const T* __restrict__ tensor,
+                                                         const uint8_t* __restrict__ mask, int mean_subtract,
+                                                         float* __restrict__ values, uint8_t* __restrict__ obs,
+                                                         float* __restrict__ means, int32_t* __restrict__ counts,
+                                                         int64_t i0, int64_t cnt_patches) {
+  extern __shared__ __align__(16) unsigned char xs[];
+  T* sv = (T*)xs;
+  uint8_t* so = (uint8_t*)(sv + (size_t)g.w0 * g.w1);
+  const int64_t ntx = (g.gc1 + kXC - 1) / kXC, nty = (g.gc0 + kXR - 1) / kXR;
+  const int ty = threadIdx.x / kXC, tx = threadIdx.x % kXC;
+  // tiles overlapping the patch range [i0, i0 + cnt) (rows of the origin grid)
+  const int64_t gy_lo = i0 / g.gc1, gy_hi = (i0 + cnt_patches - 1) / g.gc1;
+  const int64_t t_lo = (gy_lo / kXR) * ntx, t_hi = min(nty, gy_hi / kXR + 1) * ntx;
+  for (int64_t tile = t_lo + blockIdx.x; tile < t_hi; tile += gridDim.x) {
+    const int64_t gy0 = (tile / ntx) * kXR, gx0 = (tile % ntx) * kXC;
+    const int64_t y0 = gy0 * g.s0, x0 = gx0 * g.s1;
+    __syncthreads();   // the previous tile's window is consumed
+    for (int e = threadIdx.x; e < g.w0 * g.w1; e += blockDim.x) {
+      const int r = e / g.w1, c = e - r * g.w1;
+      const int64_t y = y0 + r, x = x0 + c;
+      const bool in = y < g.m0 && x < g.m1;
+      sv[e] = in ? tensor[y * g.m1 + x] : (T)0;
+      so[e] = in ? mask[y * g.m1 + x] : 0;
+    }
+    __syncthreads();
+    const int64_t gy = gy0 + ty, gx = gx0 + tx;
+    if (gy >= g.gc0 || gx >= g.gc1) continue;
+    const int64_t i = gy * g.gc1 + gx;
+    if (i < i0 || i >= i0 + cnt_patches) continue;
+    const int64_t li = i - i0;
+    const int wb = ty * g.s0 * g.w1 + tx * g.s1;
+    double sum = 0.0;
+    int cnt = 0;
+    for (int a = 0; a < g.b0; ++a) {
+      const int rb = wb + a * g.w1;
+      for (int b = 0; b < g.b1; ++b)
+        if (so[rb + b]) { sum += (double)sv[rb + b]; ++cnt; }
+    }
+    const double mean = (mean_subtract && cnt > 0) ? sum / (double)cnt : 0.0;
+    means[li] = (float)mean;
+    counts[li] = cnt;
+    int64_t q = li;
+    for (int a = 0; a < g.b0; ++a) {
+      const int rb = wb + a * g.w1;
+      for (int b = 0; b < g.b1; ++b, q += cnt_patches) {
+        const uint8_t o = so[rb + b] ? 1 : 0;
+        values[q] = o ? (float)((double)sv[rb + b] - mean) : 0.0f;
+        obs[q] = o;
+      }
+    }
+  }
+}
+
+// Overlap-add, rank 2: one thread per output element, covering patches in
+// ascending patch order (the reference's bincount order) with incremental
+// patch / offset indices.
+template <typename T>
+__global__ void __launch_bounds__(256) k_reconstitute2d(Geo2 g, const float* __restrict__ est, float est_scale,
+                                                        const float* __restrict__ means, const T* __restrict__ original,
+                                                        const uint8_t* __restrict__ mask, int dc, T* __restrict__ out,
+                                                        unsigned long long* __restrict__ uncovered) {
+  const int64_t m = g.m0 * g.m1;
+  for (int64_t xx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; xx < m; xx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t y = xx / g.m1, x = xx - y * g.m1;
+    int64_t lo0, hi0, lo1, hi1;
+    cover_range(y, g.b0, g.s0, g.gc0, lo0, hi0);
+    cover_range(x, g.b1, g.s1, g.gc1, lo1, hi1);
+    const int64_t cov = (hi0 >= lo0 && hi1 >= lo1) ? (hi0 - lo0 + 1) * (hi1 - lo1 + 1) : 0;
+    double acc = 0.0;
+    for (int64_t a0 = lo0; a0 <= hi0; ++a0) {
+      const int64_t ir = a0 * g.gc1;
+      const int64_t pr = (y - a0 * g.s0) * g.b1 + x;
+      for (int64_t a1 = lo1; a1 <= hi1; ++a1) {
+        const int64_t i = ir + a1, pe = pr - a1 * g.s1;
+        acc += (double)est[pe * g.n + i] * (double)est_scale + (double)means[i];
+      }
+    }
+    double v = cov > 0 ? acc / (double)cov : 0.0;
+    if (cov == 0 && uncovered) atomicAdd(uncovered, 1ull);
+    if (dc && mask[xx]) v = (double)original[xx];
+    out[xx] = (T)v;
+  }
+}
+
 static int grid_blocks(int64_t work, int threads) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -201,6 +315,22 @@ int launch_extract(const Grid& grid, const void* tensor, int f64, const uint8_t*
   const Geo4 g = make_geo4(grid);
   if (cnt < 0) cnt = g.n - i0;
   if (i0 < 0 || i0 + cnt > g.n) { set_error("patch range [%lld, %lld) outside the grid", (long long)i0, (long long)(i0 + cnt)); return PB_ESHAPE; }
+  if (grid.rank == 2) {   // tiled 2-D path (shared-memory window per 8 x 32 origins)
+    const Geo2 g2 = make_geo2(grid);
+    const size_t smem = (size_t)g2.w0 * g2.w1 * ((f64 ? 8 : 4) + 1);
+    if (smem <= 48 * 1024) {
+      const int64_t ntile = ceil_div(g2.gc0, kXR) * ceil_div(g2.gc1, kXC);
+      const int nb2 = (int)std::min<int64_t>(ntile, 148 * 16);
+      if (f64)
+        k_extract2d<double><<<nb2, kXR * kXC, smem, st>>>(g2, (const double*)tensor, mask, mean_subtract, values, obs,
+                                                          means, counts, i0, cnt);
+      else
+        k_extract2d<float><<<nb2, kXR * kXC, smem, st>>>(g2, (const float*)tensor, mask, mean_subtract, values, obs,
+                                                         means, counts, i0, cnt);
+      PB_LAUNCH_CHECK();
+      return PB_OK;
+    }
+  }
   const int th = 256;
   const int nb = grid_blocks(cnt, th);
   if (f64)
@@ -216,8 +346,20 @@ int launch_extract(const Grid& grid, const void* tensor, int f64, const uint8_t*
 int launch_reconstitute(const Grid& grid, const float* est, float est_scale, const float* means, const void* original,
                         const uint8_t* mask, int dc, int f64, void* out, unsigned long long* uncovered,
                         cudaStream_t st) {
-  const Geo4 g = make_geo4(grid);
   const int th = 256;
+  if (grid.rank == 2) {
+    const Geo2 g2 = make_geo2(grid);
+    const int nb2 = grid_blocks(g2.m0 * g2.m1, th);
+    if (f64)
+      k_reconstitute2d<double><<<nb2, th, 0, st>>>(g2, est, est_scale, means, (const double*)original, mask, dc,
+                                                   (double*)out, uncovered);
+    else
+      k_reconstitute2d<float><<<nb2, th, 0, st>>>(g2, est, est_scale, means, (const float*)original, mask, dc,
+                                                  (float*)out, uncovered);
+    PB_LAUNCH_CHECK();
+    return PB_OK;
+  }
+  const Geo4 g = make_geo4(grid);
   const int nb = grid_blocks(g.m, th);
   if (f64)
     k_reconstitute<double><<<nb, th, 0, st>>>(g, est, est_scale, means, (const double*)original, mask, dc,
