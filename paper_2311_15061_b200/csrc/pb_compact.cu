@@ -1100,6 +1100,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
   ell_cta_range(a, w_lo, w_hi, t_lo, t_hi);
   const int ntile = t_hi - t_lo;
   const uint32_t sbase = smem_u32(smraw);
+  uint64_t t_mark = a.prof ? gtimer() : 0;   // in-kernel phase profile (pb_dict_profile), thread 0
+  auto prof = [&](int slot) {
+    if (a.prof && threadIdx.x == 0) {
+      const uint64_t now = gtimer();
+      a.prof[blockIdx.x * kProfSlots + slot] += now - t_mark;
+      t_mark = now;
+    }
+  };
   if (a.split && a.blk_begin > 0) {  // split mode: the previous pass's shifts come from global memory
     for (int t = threadIdx.x; t < B * p; t += blockDim.x) dprev[t] = a.delta_g[t];
   }
@@ -1112,8 +1120,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
     const bool hc = bk < nblk, hp = bk > 0;
     mbar_expect_tx(&mbar[s], (hc ? kTile * B * 4u : 0u) + (hp ? kTile * B * 4u : 0u));
     if (hc) {
-      if (a.w_evict_first)
+      if (a.w_evict_first == 1)
         bulk_copy_g2s_hint(dst, a.wt + ((int64_t)tile * a.nblk8 + bk) * kTile * B, kTile * B * 4u, &mbar[s], pol_first);
+      else if (a.w_evict_first == 2)   // kept for its second use as the next pass's previous block
+        bulk_copy_g2s_hint(dst, a.wt + ((int64_t)tile * a.nblk8 + bk) * kTile * B, kTile * B * 4u, &mbar[s], pol_last);
       else
         bulk_copy_g2s(dst, a.wt + ((int64_t)tile * a.nblk8 + bk) * kTile * B, kTile * B * 4u, &mbar[s]);
     }
@@ -1142,6 +1152,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
     if (threadIdx.x == 0) next_wave = NW;   // waves 0..NW-1 go to warps 0..NW-1
     prefetched = false;
     __syncthreads();
+    prof(0);
     // ---- element phase: this warp's waves w_lo + wid, + NW, ... ----
     // Every warp visits every tile of the CTA in order: wait for the stage's
     // fill, its waves of the tile, count out (the last warp out refills the stage
@@ -1164,7 +1175,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
         return w_lo + (int64_t)__shfl_sync(0xffffffffu, w, 0);
       };
       int64_t wv = w_lo + wid;
-      bool have = wv < w_hi;
+      bool have = wv < w_hi && !PB_DBG(a, 8);   // (tuning builds: bit 8 skips the element phase)
       int wu = 0;              // tile (relative) of the next wave
       uint32_t ib[kEllPf];
       float rb[kEllPf];
@@ -1216,15 +1227,20 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
       fills0 += (ntile + 1) >> 1;
       fills1 += ntile >> 1;
     }
+    prof(2);
     if (!has_cur) break;
     __syncthreads();
+    prof(3);
     // pixel-major partials [pixel][CTA][NACC] (even + odd tile sums, fixed order)
     for (int t = threadIdx.x; t < p * L::NACC; t += blockDim.x) {
       const int pe = t / L::NACC, q = t - pe * L::NACC;
       a.partials[((size_t)pe * gridDim.x + blockIdx.x) * L::NACC + q] = acc0[t] + acc1[t];
     }
+    prof(5);
     if (PB_DBG(a, 16)) grid_sync(a.bar); else grid_sync_mono(a.bar + 2, bar_target);
+    prof(6);
     dict_owner_phase<NW>(a, smraw, &mbar[2], pphase, k0, nb, geps, epoch, dold, dprev);
+    prof(7);
     if (a.split) return;  // split mode: the caller allreduces `reduced` across ranks, then k_dict_update
     // the next pass's first tiles do not depend on the shifts: stage them now
     // (the owner scratch they overwrite is done) so they land during the barrier
@@ -1234,8 +1250,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
     }
     prefetched = true;
     if (PB_DBG(a, 16)) grid_sync(a.bar); else grid_sync_mono(a.bar + 2, bar_target);
+    prof(8);
     for (int t = threadIdx.x; t < B * p; t += blockDim.x) dprev[t] = __ldcg(a.delta_g + t);
     __syncthreads();
+    prof(9);
   }
 }
 

@@ -11,8 +11,8 @@ from paper_2311_15061_b200 import inputs  # noqa: E402
 from paper_2311_15061_b200 import patches as pp  # noqa: E402
 from tools.prof_epoch import CFGS  # noqa: E402
 
-NAMES = ["tile-top barrier", "W copy wait", "elements (warp 0)", "tile-end barrier", "boundary merge",
-         "pass-end partials", "grid sync 1", "owner update", "grid sync 2", "delta load", "fence", "owner reduce"]
+NAMES = ["pass start (acc, atoms)", "-", "elements (warp 0)", "pass-end CTA barrier", "-",
+         "partials write", "grid sync 1", "owner phase", "grid sync 2", "delta load", "-", "-"]
 for cid in [int(x) for x in sys.argv[1:]] or [3, 2]:
     c = CFGS[cid]
     img = inputs.synthetic_texture(c["shape"], seed=0) if len(c["shape"]) == 2 else \
