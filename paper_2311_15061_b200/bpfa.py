@@ -285,7 +285,7 @@ def _epoch_desc(state: GibbsState, pm: PatchMatrix, hp: Hyperparams, freeze: boo
     d.rng_mode = mode
     d.seed = state.seed & 0xFFFFFFFFFFFFFFFF
     d.n_obs = pm.n_obs
-    for j, v in enumerate(hp.as6()):
+    for j, v in enumerate(_hyper6(hp)):
         d.hyper[j] = float(v)
     d.values, d.observed = pm.values_pn.data_ptr(), pm.observed_pn.data_ptr()
     d.atoms, d.pi = state.dictionary.atoms.data_ptr(), state.dictionary.pi.data_ptr()
@@ -293,6 +293,12 @@ def _epoch_desc(state: GibbsState, pm: PatchMatrix, hp: Hyperparams, freeze: boo
     d.scalars = state.scalars.data_ptr()
     d.workspace = ws.data_ptr()
     return d, m
+
+
+def _hyper6(hp):
+    """(a, b, c, d, e, f) of a Hyperparams — this package's or the reference's
+    dataclass (bpfa.py:42-60), so reference callers can pass theirs."""
+    return (hp.concentration_a, hp.concentration_b, hp.weight_shape, hp.weight_rate, hp.noise_shape, hp.noise_rate)
 
 
 def _check_state(state, pm):
