@@ -949,8 +949,9 @@ __device__ __forceinline__ void ell_flush(float (&v)[GramLayout<kWB>::NP], int l
 // boundaries snapped to wave starts.
 __device__ __forceinline__ void ell_cta_range(const DictGramArgs& a, int64_t& w_lo, int64_t& w_hi, int& t_lo,
                                               int& t_hi) {
-  const double total_cost = (double)a.ell_base[a.ntiles] + kTileVisitCost * a.ntiles;
-  auto cost_at = [&](int t) { return (double)a.ell_base[t] + kTileVisitCost * t; };
+  const double tvc = a.tile_cost;
+  const double total_cost = (double)a.ell_base[a.ntiles] + tvc * a.ntiles;
+  auto cost_at = [&](int t) { return (double)a.ell_base[t] + tvc * t; };
   auto boundary = [&](int c) -> int64_t {
     if (c <= 0) return 0;
     if (c >= (int)gridDim.x) return a.wave_base[a.ntiles];
@@ -960,7 +961,7 @@ __device__ __forceinline__ void ell_cta_range(const DictGramArgs& a, int64_t& w_
       const int mid = (lo + hi + 1) >> 1;
       if (cost_at(mid) <= target) lo = mid; else hi = mid - 1;
     }
-    const double over = target - cost_at(lo) - kTileVisitCost;
+    const double over = target - cost_at(lo) - tvc;
     const int64_t w0 = a.wave_base[lo], w1 = a.wave_base[lo + 1];
     if (over <= 0.0 || w1 == w0) return w0;
     int64_t wl = w0, wh = w1 - 1;   // last wave starting at or before `over`
@@ -1679,6 +1680,7 @@ int launch_dict_gram(const DictGramArgs& a_in, cudaStream_t st) {
   // (re-read every pass) keep L2 (configs[1] 3.41 -> 2.52 ms)
   a.w_evict_first = PB_TUNE_INT("PB_DICT_W_EVICT", 1);
   a.dyn_waves = PB_TUNE_INT("PB_DICT_DYN", 1);
+  a.tile_cost = PB_TUNE_DBL("PB_DICT_TILE_COST", kTileVisitCost);
   {
     static bool l2_set = false;
     const int persist = PB_TUNE_INT("PB_L2_PERSIST_MB", 0);

@@ -84,6 +84,7 @@ struct DictGramArgs {
   int pstage_off;       // byte offset of the staged owner partials in shared memory (0: read from L2)
   int w_evict_first;    // the current block's W copy with an L2 evict_first policy too
   int dyn_waves;        // warps claim their waves from a CTA counter (else round-robin)
+  double tile_cost;     // work split: ELL positions equivalent to one tile visit
   int64_t n;
   int64_t ld;           // row pitch of usage/weights (K, ld), ld >= n
   int64_t nnz;          // observed elements (host copy of tile_base[ntiles])
