@@ -755,7 +755,7 @@ __device__ __forceinline__ void atom_block_update(const double* red, int p, int 
                          dprev, nullptr);
 }
 
-constexpr double kTileVisitCost = 3000.0;  // element-equivalents of one tile visit (work split)
+constexpr double kTileVisitCost = 500.0;   // ELL positions equivalent to one tile visit (work split; 3000: live +2 %)
 // Byte stride of one staged W block in shared memory: the tile's kTile x 8
 // floats, then the all-zero row kEllZeroRow that the ELL padding points to.
 constexpr uint32_t kWStride = (uint32_t)kTile * kWB * 4 + 128;
@@ -969,10 +969,16 @@ __device__ __forceinline__ void ell_cta_range(const DictGramArgs& a, int64_t& w_
       const int64_t mid = (wl + wh + 1) >> 1;
       if ((double)a.wave_off[mid] <= over) wl = mid; else wh = mid - 1;
     }
+    // the nearer of that wave's start and the next boundary (next wave or tile end)
+    if (a.split_nearest) {
+      const double nxt = wl + 1 < w1 ? (double)a.wave_off[wl + 1] : (double)(a.ell_base[lo + 1] - a.ell_base[lo]);
+      if (nxt - over < over - (double)a.wave_off[wl]) return wl + 1;
+    }
     return wl;
   };
-  w_lo = boundary(blockIdx.x);
-  w_hi = boundary(blockIdx.x + 1);
+  const int cr = PB_DBG(a, 32) ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x;   // (tuning: reversed ranges)
+  w_lo = boundary(cr);
+  w_hi = boundary(cr + 1);
   t_lo = 0;
   t_hi = 0;
   if (w_hi > w_lo) {
@@ -1681,6 +1687,7 @@ int launch_dict_gram(const DictGramArgs& a_in, cudaStream_t st) {
   a.w_evict_first = PB_TUNE_INT("PB_DICT_W_EVICT", 1);
   a.dyn_waves = PB_TUNE_INT("PB_DICT_DYN", 1);
   a.tile_cost = PB_TUNE_DBL("PB_DICT_TILE_COST", kTileVisitCost);
+  a.split_nearest = PB_TUNE_INT("PB_DICT_NEAREST", 0);
   {
     static bool l2_set = false;
     const int persist = PB_TUNE_INT("PB_L2_PERSIST_MB", 0);

@@ -85,6 +85,7 @@ struct DictGramArgs {
   int w_evict_first;    // the current block's W copy with an L2 evict_first policy too
   int dyn_waves;        // warps claim their waves from a CTA counter (else round-robin)
   double tile_cost;     // work split: ELL positions equivalent to one tile visit
+  int split_nearest;    // work split: CTA boundaries at the nearest wave start (else the preceding one)
   int64_t n;
   int64_t ld;           // row pitch of usage/weights (K, ld), ld >= n
   int64_t nnz;          // observed elements (host copy of tile_base[ntiles])
