@@ -1238,10 +1238,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
     if (!has_cur) break;
     __syncthreads();
     prof(3);
-    // pixel-major partials [pixel][CTA][NACC] (even + odd tile sums, fixed order)
-    for (int t = threadIdx.x; t < p * L::NACC; t += blockDim.x) {
-      const int pe = t / L::NACC, q = t - pe * L::NACC;
-      a.partials[((size_t)pe * gridDim.x + blockIdx.x) * L::NACC + q] = acc0[t] + acc1[t];
+    // pixel-major partials [pixel][CTA][NACC] (even + odd tile sums, fixed order), 16-byte chunks
+    static_assert(L::NACC % 4 == 0, "accumulator rows in 16-byte chunks");
+    for (int t = threadIdx.x; t < p * (L::NACC / 4); t += blockDim.x) {
+      const int pe = t / (L::NACC / 4), q4 = t - pe * (L::NACC / 4);
+      const float4 x = *(const float4*)(acc0 + pe * L::NACC + 4 * q4), y = *(const float4*)(acc1 + pe * L::NACC + 4 * q4);
+      *(float4*)(a.partials + ((size_t)pe * gridDim.x + blockIdx.x) * L::NACC + 4 * q4) =
+          make_float4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w);
     }
     prof(5);
     if (PB_DBG(a, 16)) grid_sync(a.bar); else grid_sync_mono(a.bar + 2, bar_target);
