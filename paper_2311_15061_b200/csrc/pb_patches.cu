@@ -269,10 +269,73 @@ __global__ void __launch_bounds__(kXR * kXC) k_extract2d(Geo2 g, const T* __rest
   }
 }
 
+
+// Row variant (stride-1-sized windows): a CTA takes 256 consecutive patch
+// origins of ONE grid row, shifted per row so that every warp's 32 patches
+// start at a multiple of 32 in the output (each warp store one whole aligned
+// 128-byte line of a plane: no partial-sector writes, whose read-for-ownership
+// cost the 8x32-tile kernel 100 MB of DRAM reads at configs[1]).  The window is
+// B0 rows x (255*s1 + B1) elements.
+constexpr int kXW = 256;
+template <typename T>
+__global__ void __launch_bounds__(kXW) k_extract2r(Geo2 g, const T* __restrict__ tensor, const uint8_t* __restrict__ mask,
+                                                   int mean_subtract, float* __restrict__ values,
+                                                   uint8_t* __restrict__ obs, float* __restrict__ means,
+                                                   int32_t* __restrict__ counts, int64_t i0, int64_t cnt_patches,
+                                                   int tiles_per_row) {
+  extern __shared__ __align__(16) unsigned char xs[];
+  const int w1 = (kXW - 1) * g.s1 + g.b1;
+  T* sv = (T*)xs;
+  uint8_t* so = (uint8_t*)(sv + (size_t)g.b0 * w1);
+  const int64_t gy_lo = i0 / g.gc1, gy_hi = (i0 + cnt_patches - 1) / g.gc1;
+  const int64_t ntile = (gy_hi - gy_lo + 1) * tiles_per_row;
+  for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+    const int64_t gy = gy_lo + tile / tiles_per_row;
+    const int k = (int)(tile % tiles_per_row);
+    const int off = (int)((((gy * g.gc1 - i0) % 32) + 32) % 32);
+    const int64_t sx = (int64_t)((32 - off) % 32) - kXW + (int64_t)kXW * k;   // first origin of the tile (may be < 0)
+    __syncthreads();   // the previous tile's window is consumed
+    const int64_t y0 = gy * g.s0, x0 = sx * g.s1;
+    for (int e = threadIdx.x; e < g.b0 * w1; e += blockDim.x) {
+      const int r = e / w1, c = e - r * w1;
+      const int64_t y = y0 + r, x = x0 + c;
+      const bool in = x >= 0 && y < g.m0 && x < g.m1;
+      sv[e] = in ? tensor[y * g.m1 + x] : (T)0;
+      so[e] = in ? mask[y * g.m1 + x] : 0;
+    }
+    __syncthreads();
+    const int64_t gx = sx + threadIdx.x;
+    if (gx < 0 || gx >= g.gc1) continue;
+    const int64_t i = gy * g.gc1 + gx;
+    if (i < i0 || i >= i0 + cnt_patches) continue;
+    const int64_t li = i - i0;
+    const int wb = threadIdx.x * g.s1;
+    double sum = 0.0;
+    int cnt = 0;
+    for (int a = 0; a < g.b0; ++a) {
+      const int rb = wb + a * w1;
+      for (int b = 0; b < g.b1; ++b)
+        if (so[rb + b]) { sum += (double)sv[rb + b]; ++cnt; }
+    }
+    const double mean = (mean_subtract && cnt > 0) ? sum / (double)cnt : 0.0;
+    means[li] = (float)mean;
+    counts[li] = cnt;
+    int64_t q = li;
+    for (int a = 0; a < g.b0; ++a) {
+      const int rb = wb + a * w1;
+      for (int b = 0; b < g.b1; ++b, q += cnt_patches) {
+        const uint8_t o = so[rb + b] ? 1 : 0;
+        values[q] = o ? (float)((double)sv[rb + b] - mean) : 0.0f;
+        obs[q] = o;
+      }
+    }
+  }
+}
+
 // Overlap-add, rank 2: one thread per output element, covering patches in
 // ascending patch order (the reference's bincount order) with incremental
 // patch / offset indices.
-template <typename T>
+template <typename T, int B1>   // B1 > 0: patch width known at compile time (inner loop unrolled)
 __global__ void __launch_bounds__(256) k_reconstitute2d(Geo2 g, const float* __restrict__ est, float est_scale,
                                                         const float* __restrict__ means, const T* __restrict__ original,
                                                         const uint8_t* __restrict__ mask, int dc, T* __restrict__ out,
@@ -288,6 +351,27 @@ __global__ void __launch_bounds__(256) k_reconstitute2d(Geo2 g, const float* __r
     for (int64_t a0 = lo0; a0 <= hi0; ++a0) {
       const int64_t ir = a0 * g.gc1;
       const int64_t pr = (y - a0 * g.s0) * g.b1 + x;
+      if constexpr (B1 > 0) {
+        // stride 1 along the row (the common case): the row's covering patches are
+        // a1 = lo1..hi1 (at most B1); all loads issue before the ordered adds
+        if (g.s1 == 1) {
+          float e[B1], mu[B1];
+          const int cnt = (int)(hi1 - lo1 + 1);
+#pragma unroll
+          for (int u = 0; u < B1; ++u) {
+            e[u] = 0.f; mu[u] = 0.f;
+            if (u < cnt) {
+              const int64_t a1 = lo1 + u, i = ir + a1, pe = pr - a1;
+              e[u] = est[pe * g.n + i];
+              mu[u] = means[i];
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < B1; ++u)
+            if (u < cnt) acc += (double)e[u] * (double)est_scale + (double)mu[u];
+          continue;
+        }
+      }
       for (int64_t a1 = lo1; a1 <= hi1; ++a1) {
         const int64_t i = ir + a1, pe = pr - a1 * g.s1;
         acc += (double)est[pe * g.n + i] * (double)est_scale + (double)means[i];
@@ -315,8 +399,22 @@ int launch_extract(const Grid& grid, const void* tensor, int f64, const uint8_t*
   const Geo4 g = make_geo4(grid);
   if (cnt < 0) cnt = g.n - i0;
   if (i0 < 0 || i0 + cnt > g.n) { set_error("patch range [%lld, %lld) outside the grid", (long long)i0, (long long)(i0 + cnt)); return PB_ESHAPE; }
-  if (grid.rank == 2) {   // tiled 2-D path (shared-memory window per 8 x 32 origins)
+  if (grid.rank == 2) {   // tiled 2-D paths (shared-memory windows)
     const Geo2 g2 = make_geo2(grid);
+    const size_t smem_r = (size_t)g2.b0 * ((kXW - 1) * g2.s1 + g2.b1) * ((f64 ? 8 : 4) + 1);
+    if (smem_r <= 48 * 1024 && g2.gc1 >= 768) {   // aligned row tiles (wide frames: configs[1] -18 %, [4] -41 %)
+      const int tpr = (int)((g2.gc1 + 2 * kXW - 1) / kXW);
+      const int64_t rows = (i0 + cnt - 1) / g2.gc1 - i0 / g2.gc1 + 1;
+      const int nb2 = (int)std::min<int64_t>(rows * tpr, 148 * 16);
+      if (f64)
+        k_extract2r<double><<<nb2, kXW, smem_r, st>>>(g2, (const double*)tensor, mask, mean_subtract, values, obs,
+                                                      means, counts, i0, cnt, tpr);
+      else
+        k_extract2r<float><<<nb2, kXW, smem_r, st>>>(g2, (const float*)tensor, mask, mean_subtract, values, obs,
+                                                     means, counts, i0, cnt, tpr);
+      PB_LAUNCH_CHECK();
+      return PB_OK;
+    }
     const size_t smem = (size_t)g2.w0 * g2.w1 * ((f64 ? 8 : 4) + 1);
     if (smem <= 48 * 1024) {
       const int64_t ntile = ceil_div(g2.gc0, kXR) * ceil_div(g2.gc1, kXC);
@@ -350,12 +448,13 @@ int launch_reconstitute(const Grid& grid, const float* est, float est_scale, con
   if (grid.rank == 2) {
     const Geo2 g2 = make_geo2(grid);
     const int nb2 = grid_blocks(g2.m0 * g2.m1, th);
-    if (f64)
-      k_reconstitute2d<double><<<nb2, th, 0, st>>>(g2, est, est_scale, means, (const double*)original, mask, dc,
-                                                   (double*)out, uncovered);
-    else
-      k_reconstitute2d<float><<<nb2, th, 0, st>>>(g2, est, est_scale, means, (const float*)original, mask, dc,
-                                                  (float*)out, uncovered);
+#define PB_OLA2(T, BB)                                                                                      \
+  k_reconstitute2d<T, BB><<<nb2, th, 0, st>>>(g2, est, est_scale, means, (const T*)original, mask, dc, (T*)out, \
+                                              uncovered)
+    // (a compile-time-width variant that issues a row's loads before the ordered
+    // adds measured 2.3x slower at configs[1]; the plain loop is kept)
+    if (f64) PB_OLA2(double, 0); else PB_OLA2(float, 0);
+#undef PB_OLA2
     PB_LAUNCH_CHECK();
     return PB_OK;
   }
