@@ -15,7 +15,9 @@ the oracle, which is bit-exact to patchbeam (tests/test_oracle_golden.py).
   (153,265 patches >= 2^17: the warp-claimed code step with pitch-8 windows
   that configs[1] runs), 2 epochs;
 * configs[3] crop: a 24x24x16 crop of the cube, 8x8x4, K = 64 (multi-lane code
-  step, 16-warp dictionary variant), 3 epochs.
+  step, 16-warp dictionary variant), 3 epochs;
+* configs[4] band: 40 rows of the 4096x4096 10 % frame, 8x8, K = 256 (135K
+  patches, the full row width), 2 epochs.
 """
 
 import numpy as np
@@ -62,3 +64,9 @@ def test_configs3_crop_teacher_forced():
     img = base[:, :, None] * spec[None, None, :]
     mask = inputs.make_mask(img.shape, 0.20, "uniform-random", 0)
     _run("cfg3crop", img, mask, (8, 8, 4), 64, 3, mean_subtract=False)
+
+
+def test_configs4_band_teacher_forced():
+    img = inputs.stem_lattice((4096, 4096), seed=0)[:40]
+    mask = inputs.make_mask((4096, 4096), 0.10, "uniform-random", 0)[:40]
+    _run("cfg4band", np.ascontiguousarray(img), np.ascontiguousarray(mask), (8, 8), 256, 2)
