@@ -76,7 +76,7 @@ static size_t ws_bytes(int64_t n, int p, int k, int64_t nnz, EpochWs* ws, char* 
   char* wt = take(wtb);
   char* pa = take(dict_gram_partials_bytes(p, kMaxDictBlocks));
   char* rd = take(dict_gram_reduced_bytes(p));
-  char* bar = take(16);
+  char* bar = take(16 + (size_t)p * 4);   // grid-barrier counters, then per-pixel ready flags
   char* bs = take((size_t)(ceil_div(n * 64, 256) + 8) * 2 * 8);  // upper bound of code-step blocks (two launches)
   char* mc = take((size_t)k * 4);
   char* dg = take((size_t)8 * p * 4);

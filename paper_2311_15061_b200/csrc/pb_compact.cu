@@ -1057,9 +1057,14 @@ __device__ __forceinline__ void dict_owner_phase(const DictGramArgs& a, unsigned
       pre[threadIdx.x] = atom_pre<B>(red64 + (size_t)i * L::NACC, threadIdx.x, pe, p, k0, geps, epoch, a.draws,
                                      a.key0, a.key1, dold);
     __syncthreads();
-    if (threadIdx.x == 0)
+    if (threadIdx.x == 0) {
       atom_pixel_update<B>(red64 + (size_t)i * L::NACC, pe, p, k0, nb, geps, epoch, a.draws, a.key0, a.key1, dold,
                            a.atoms, dprev, a.delta_g, pre);
+      if (a.pixel_flags) {   // publish the pixel's shifts: delta_g[.][pe] is ready for pass blk + 1
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.bar + 4 + pe), "r"((unsigned)(k0 / B + 1)) : "memory");
+      }
+    }
     __syncthreads();
   }
 }
@@ -1259,7 +1264,19 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
       if (ntile > 1) issue(1, blk + 1);
     }
     prefetched = true;
-    if (PB_DBG(a, 16)) grid_sync(a.bar); else grid_sync_mono(a.bar + 2, bar_target);
+    if (a.pixel_flags) {
+      // no second grid barrier: wait until every pixel's owner has published this
+      // block's shifts (owners finish reading the partials before they publish, so
+      // the next pass may overwrite them)
+      if (wid == 0)
+        for (int pe = lane; pe < p; pe += 32)
+          while (ld_acquire(a.bar + 4 + pe) < (unsigned)(blk + 1)) __nanosleep(32);
+      __syncthreads();
+    } else if (PB_DBG(a, 16)) {
+      grid_sync(a.bar);
+    } else {
+      grid_sync_mono(a.bar + 2, bar_target);
+    }
     prof(8);
     for (int t = threadIdx.x; t < B * p; t += blockDim.x) dprev[t] = __ldcg(a.delta_g + t);
     __syncthreads();
@@ -1668,7 +1685,7 @@ static int launch_dict_gram_b(DictGramArgs a, cudaStream_t st) {
     const int nostage = PB_TUNE_INT("PB_DICT_NO_PSTAGE", 0);   // 1: owners read the partials from L2 (A/B)
     a.pstage_off = (!nostage && off + (size_t)blocks * L::NACC * 4 <= wbytes) ? (int)off : 0;
   }
-  PB_CUDA_TRY(cudaMemsetAsync(a.bar, 0, 4 * sizeof(unsigned), st));
+  PB_CUDA_TRY(cudaMemsetAsync(a.bar, 0, (4 + (size_t)a.p) * sizeof(unsigned), st));
   void* args[] = {&a};
   PB_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(blocks), dim3(th), args, smem, st));
   return PB_OK;
@@ -1691,6 +1708,7 @@ int launch_dict_gram(const DictGramArgs& a_in, cudaStream_t st) {
   a.dyn_waves = PB_TUNE_INT("PB_DICT_DYN", 1);
   a.tile_cost = PB_TUNE_DBL("PB_DICT_TILE_COST", kTileVisitCost);
   a.split_nearest = PB_TUNE_INT("PB_DICT_NEAREST", 0);
+  a.pixel_flags = PB_TUNE_INT("PB_DICT_FLAGS", 1);
   {
     static bool l2_set = false;
     const int persist = PB_TUNE_INT("PB_L2_PERSIST_MB", 0);

@@ -71,7 +71,7 @@ struct DictGramArgs {
   // workspace
   float* partials;      // max_blocks * P * NACC
   double* reduced;      // P * NACC
-  unsigned* bar;        // 2
+  unsigned* bar;        // [4] grid-barrier counters, then [P] per-pixel shift-ready flags (zeroed per launch)
   unsigned long long* prof;  // optional [gridDim][kProfSlots] phase nanoseconds (profiling)
   int dbg;              // profiling-only: 4 skip the W/colptr bulk copies, 8 skip the element phase
   // split (multi-rank) mode: run the single pass blk_begin and stop after the
@@ -86,6 +86,7 @@ struct DictGramArgs {
   int dyn_waves;        // warps claim their waves from a CTA counter (else round-robin)
   double tile_cost;     // work split: ELL positions equivalent to one tile visit
   int split_nearest;    // work split: CTA boundaries at the nearest wave start (else the preceding one)
+  int pixel_flags;      // per-pixel ready flags instead of the second grid barrier of a pass
   int64_t n;
   int64_t ld;           // row pitch of usage/weights (K, ld), ld >= n
   int64_t nnz;          // observed elements (host copy of tile_base[ntiles])
