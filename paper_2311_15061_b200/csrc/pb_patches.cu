@@ -285,7 +285,9 @@ __global__ void __launch_bounds__(kXW) k_extract2r(Geo2 g, const T* __restrict__
                                                    int tiles_per_row) {
   extern __shared__ __align__(16) unsigned char xs[];
   const int w1 = (kXW - 1) * g.s1 + g.b1;
-  T* sv = (T*)xs;
+  double* csum = (double*)xs;                     // per window column: observed sum over the B0 rows
+  int* ccnt = (int*)(csum + w1);                  // ... and observed count
+  T* sv = (T*)(ccnt + ((w1 + 1) & ~1));
   uint8_t* so = (uint8_t*)(sv + (size_t)g.b0 * w1);
   const int64_t gy_lo = i0 / g.gc1, gy_hi = (i0 + cnt_patches - 1) / g.gc1;
   const int64_t ntile = (gy_hi - gy_lo + 1) * tiles_per_row;
@@ -304,6 +306,17 @@ __global__ void __launch_bounds__(kXW) k_extract2r(Geo2 g, const T* __restrict__
       so[e] = in ? mask[y * g.m1 + x] : 0;
     }
     __syncthreads();
+    // column sums of the window (shared by the B1 patches that cover a column):
+    // a patch's observed sum / count is then B1 column terms instead of B0*B1
+    for (int c = threadIdx.x; c < w1; c += blockDim.x) {
+      double cs = 0.0;
+      int cc = 0;
+      for (int a = 0; a < g.b0; ++a)
+        if (so[a * w1 + c]) { cs += (double)sv[a * w1 + c]; ++cc; }
+      csum[c] = cs;
+      ccnt[c] = cc;
+    }
+    __syncthreads();
     const int64_t gx = sx + threadIdx.x;
     if (gx < 0 || gx >= g.gc1) continue;
     const int64_t i = gy * g.gc1 + gx;
@@ -312,11 +325,7 @@ __global__ void __launch_bounds__(kXW) k_extract2r(Geo2 g, const T* __restrict__
     const int wb = threadIdx.x * g.s1;
     double sum = 0.0;
     int cnt = 0;
-    for (int a = 0; a < g.b0; ++a) {
-      const int rb = wb + a * w1;
-      for (int b = 0; b < g.b1; ++b)
-        if (so[rb + b]) { sum += (double)sv[rb + b]; ++cnt; }
-    }
+    for (int b = 0; b < g.b1; ++b) { sum += csum[wb + b]; cnt += ccnt[wb + b]; }
     const double mean = (mean_subtract && cnt > 0) ? sum / (double)cnt : 0.0;
     means[li] = (float)mean;
     counts[li] = cnt;
@@ -401,7 +410,8 @@ int launch_extract(const Grid& grid, const void* tensor, int f64, const uint8_t*
   if (i0 < 0 || i0 + cnt > g.n) { set_error("patch range [%lld, %lld) outside the grid", (long long)i0, (long long)(i0 + cnt)); return PB_ESHAPE; }
   if (grid.rank == 2) {   // tiled 2-D paths (shared-memory windows)
     const Geo2 g2 = make_geo2(grid);
-    const size_t smem_r = (size_t)g2.b0 * ((kXW - 1) * g2.s1 + g2.b1) * ((f64 ? 8 : 4) + 1);
+    const size_t w1r = (size_t)(kXW - 1) * g2.s1 + g2.b1;
+    const size_t smem_r = w1r * 8 + ((w1r + 1) & ~(size_t)1) * 4 + (size_t)g2.b0 * w1r * ((f64 ? 8 : 4) + 1);
     if (smem_r <= 48 * 1024 && g2.gc1 >= 768) {   // aligned row tiles (wide frames: configs[1] -18 %, [4] -41 %)
       const int tpr = (int)((g2.gc1 + 2 * kXW - 1) / kXW);
       const int64_t rows = (i0 + cnt - 1) / g2.gc1 - i0 / g2.gc1 + 1;
