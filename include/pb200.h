@@ -195,6 +195,9 @@ typedef struct pb_epoch_desc {
   int64_t n_global;
   pb_allreduce_fn allreduce;
   void* allreduce_ctx;
+  int32_t codes_zero;       /* caller asserts usage and weights are all zero on entry (fresh init,
+                               reset codes): the code step reads no old state — the buffers need
+                               not even be cleared, every entry of [0, n) is written */
 } pb_epoch_desc;
 
 size_t pb_epoch_workspace_bytes(int64_t n, int32_t p, int32_t k, int64_t nnz);

@@ -61,7 +61,7 @@ class EpochDesc(ctypes.Structure):
                 ("atoms", c_vp), ("pi", c_vp), ("usage", c_vp),
                 ("weights", c_vp), ("scalars", c_vp), ("atom_draws", c_vp), ("code_u", c_vp),
                 ("code_g", c_vp), ("workspace", c_vp), ("i_offset", c_i64), ("n_global", c_i64),
-                ("allreduce", ALLREDUCE_FN), ("allreduce_ctx", c_vp)]
+                ("allreduce", ALLREDUCE_FN), ("allreduce_ctx", c_vp), ("codes_zero", c_i32)]
 
 
 PB_DRAW_PRIOR, PB_DRAW_EPOCH, PB_DRAW_POSTERIOR = 0, 1, 2

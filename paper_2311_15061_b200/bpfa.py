@@ -274,6 +274,7 @@ def _epoch_desc(state: GibbsState, pm: PatchMatrix, hp: Hyperparams, freeze: boo
         d.resid_mode = _lib.PB_RESID_CARRY            # residual of this exact state is resident
     elif state._zero_key == state._codes_key():
         d.resid_mode = _lib.PB_RESID_FROM_VALUES      # Z*S == 0  =>  R = X
+        d.codes_zero = 1                              # Z = S = 0: the code step reads no old state
     else:
         d.resid_mode = _lib.PB_RESID_RECOMPUTE        # residual_full (bpfa.py:297)
     state._resid_key = key

@@ -169,6 +169,7 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
   philox_round_keys(k0, k1, c.rk);
   c.ld = d->ld > d->n ? d->ld : d->n;
   c.i_offset = d->i_offset;
+  c.codes_zero = d->codes_zero;
   const int64_t n_global = d->n_global > 0 ? d->n_global : d->n;
   phase_mark(kPhResid, st);
   int rc = PB_OK;
@@ -635,6 +636,13 @@ int pb_problem_create(const pb_problem_desc* desc, pb_problem** out) {
     }
   }
 #undef PB_A
+  // codes start (and their row padding [n, ld) stays) zero; frames rewrite [0, n)
+  if (cudaMemset(pr->usage, 0, (size_t)k * ld) != cudaSuccess ||
+      cudaMemset(pr->weights, 0, (size_t)k * ld * sizeof(float)) != cudaSuccess) {
+    set_error("code buffers: clear failed");
+    pb_problem_destroy(pr);
+    return PB_ECUDA;
+  }
   if (cudaStreamCreateWithFlags(&pr->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&pr->ev0) != cudaSuccess || cudaEventCreate(&pr->ev1) != cudaSuccess) {
     set_error("stream/event creation failed");
@@ -791,8 +799,8 @@ int pb_problem_submit_frame_ex(pb_problem* pr, const double* frame_host, const u
   if (!pr->have_state || !pr->desc.warm_start) {
     if ((rc = problem_cold_init(pr))) return rc;
   }
-  PB_CUDA_TRY(cudaMemsetAsync(pr->usage, 0, (size_t)pr->k * pr->ld, st));
-  PB_CUDA_TRY(cudaMemsetAsync(pr->weights, 0, (size_t)pr->k * pr->ld * sizeof(float), st));
+  // codes re-burn each frame (pipeline.py:232-233): the first sweep runs with
+  // codes_zero (no old state read, every entry rewritten), so no clearing pass
   pb_epoch_desc d{};
   d.n = n; d.ld = pr->ld; d.p = pr->p; d.k = pr->k;
   d.freeze_dict = pr->desc.freeze_dict;
@@ -807,6 +815,7 @@ int pb_problem_submit_frame_ex(pb_problem* pr, const double* frame_host, const u
   int tail = pr->desc.average_last < 1 ? 1 : (pr->desc.average_last > epochs ? epochs : pr->desc.average_last);
   for (int e = 0; e < epochs; ++e) {
     d.resid_mode = e == 0 ? PB_RESID_FROM_VALUES : PB_RESID_CARRY;  // codes were just reset
+    d.codes_zero = e == 0;
     if (pr->desc.replay) {
       if ((rc = replay_epoch(pr, d))) return rc;
     } else if ((rc = run_epoch(&d, pr->m_count, st))) {
@@ -910,6 +919,8 @@ static int problem_set_k(pb_problem* pr, int k) {
   int rc = PB_OK;
 #define PB_R(ptr, cnt) if ((rc = dalloc(&pr->ptr, (size_t)(cnt)))) return rc;
   PB_R(atoms, (int64_t)k * p) PB_R(pi, k) PB_R(usage, (int64_t)k * ld) PB_R(weights, (int64_t)k * ld) PB_R(m_count, k)
+  PB_CUDA_TRY(cudaMemset(pr->usage, 0, (size_t)k * ld));
+  PB_CUDA_TRY(cudaMemset(pr->weights, 0, (size_t)k * ld * sizeof(float)));
   if (compose_tc_supported((int)p) && !PB_TUNE_FLAG("PB_COMPOSE_TC_OFF")) PB_R(bpack, compose_tc_scratch_bytes((int)p, k) / 4)
   if (pr->desc.replay) {
     PB_R(d_atom, (int64_t)k * p) PB_R(d_u, (int64_t)k * n) PB_R(d_g, (int64_t)k * n)

@@ -272,9 +272,11 @@ __device__ __forceinline__ void code_atoms(const CompactArgs& a, const CodeConst
   // advances by 8 per pair (no per-slot address arithmetic beyond that)
   constexpr bool kPair = W <= 16;  // register budget: 2W values of D per pair
   int64_t zo = (int64_t)k0 * a.ld + c.ic;
-  uint8_t za = a.usage[zo], zb = 0;
-  float sa = a.weights[zo], sb = 0.0f;
-  if (k0 + 1 < a.k) { zb = a.usage[zo + a.ld]; sb = a.weights[zo + a.ld]; }
+  const bool ld_state = !a.codes_zero;   // all codes zero (fresh / warm-reset state): nothing to load
+  uint8_t za = 0, zb = 0;
+  float sa = 0.0f, sb = 0.0f;
+  if (ld_state) { za = a.usage[zo]; sa = a.weights[zo]; }
+  if (ld_state && k0 + 1 < a.k) { zb = a.usage[zo + a.ld]; sb = a.weights[zo + a.ld]; }
   for (int kg = k0; kg < k1; kg += 8) {
 #pragma unroll 1
     for (int q = 0; q < 8; q += 2) {
@@ -283,8 +285,8 @@ __device__ __forceinline__ void code_atoms(const CompactArgs& a, const CodeConst
       // prefetch the next pair's state
       uint8_t zna = 0, znb = 0;
       float sna = 0.0f, snb = 0.0f;
-      if (k + 2 < a.k) { zna = a.usage[zo + 2 * a.ld]; sna = a.weights[zo + 2 * a.ld]; }
-      if (k + 3 < a.k) { znb = a.usage[zo + 3 * a.ld]; snb = a.weights[zo + 3 * a.ld]; }
+      if (ld_state && k + 2 < a.k) { zna = a.usage[zo + 2 * a.ld]; sna = a.weights[zo + 2 * a.ld]; }
+      if (ld_state && k + 3 < a.k) { znb = a.usage[zo + 3 * a.ld]; snb = a.weights[zo + 3 * a.ld]; }
       float uu0 = 0.f, uu1 = 0.f, g0 = 0.f, g1 = 0.f;
       double ud0 = 0.0, ud1 = 0.0, gd0 = 0.0, gd1 = 0.0;
       if (MODE == kRngReplay) {

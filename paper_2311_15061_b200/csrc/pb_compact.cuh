@@ -48,6 +48,7 @@ struct CompactArgs {
   unsigned* blk_ctr;    // dynamic block counter of the launch (zeroed by the launcher)
   const float* dt_img;  // pre-packed transposed dictionary chunks (launch_pack_dt)
   int64_t dt_img_floats;
+  int codes_zero;       // usage / weights are all zero on entry: the code step loads no old state
 };
 
 struct DictGramArgs {
