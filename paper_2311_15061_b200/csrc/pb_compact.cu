@@ -1146,24 +1146,31 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
                          &mbar[s], pol_first);
   };
   bool prefetched = false;
+  // a pass's setup: zeroed accumulators, the block's current atoms, the zero W
+  // rows (the owner phase overwrote them), the wave counter.  For every pass but
+  // the first it runs while the previous pass's shifts are still being published.
+  auto setup = [&](int bk) {
+    const int nbk = bk < nblk ? min(B, a.k - bk * B) : 0;
+    for (int t = threadIdx.x; t < 2 * p * L::NACC; t += blockDim.x) acc0[t] = 0.0f;
+    for (int t = threadIdx.x; t < B * p; t += blockDim.x) {
+      const int j = t / p, pe = t - j * p;
+      dold[t] = j < nbk ? a.atoms[(int64_t)(bk * B + j) * p + pe] : 0.0f;
+    }
+    if (threadIdx.x < 16) {
+      const int blkno = threadIdx.x >> 2, part = threadIdx.x & 3;
+      *(float2*)(smraw + blkno * kWStride + kEllZeroRow + part * 8) = make_float2(0.f, 0.f);
+    }
+    if (threadIdx.x == 0) next_wave = NW;   // waves 0..NW-1 go to warps 0..NW-1
+  };
+  setup(a.split ? a.blk_begin : 0);
   for (int blk = a.split ? a.blk_begin : 0; blk <= (a.split ? a.blk_begin : nblk); ++blk) {
     const bool has_cur = blk < nblk, has_prev = blk > 0;
     const int k0 = blk * B;
     const int nb = has_cur ? min(B, a.k - k0) : 0;
-    for (int t = threadIdx.x; t < 2 * p * L::NACC; t += blockDim.x) acc0[t] = 0.0f;
-    for (int t = threadIdx.x; t < B * p; t += blockDim.x) {
-      const int j = t / p, pe = t - j * p;
-      dold[t] = j < nb ? a.atoms[(int64_t)(k0 + j) * p + pe] : 0.0f;
-    }
-    if (threadIdx.x < 16) {   // the zero rows behind the four blocks (the owner phase overwrote them)
-      const int blkno = threadIdx.x >> 2, part = threadIdx.x & 3;
-      *(float2*)(smraw + blkno * kWStride + kEllZeroRow + part * 8) = make_float2(0.f, 0.f);
-    }
     if (threadIdx.x == 0 && !prefetched) {
       if (ntile > 0) issue(0, blk);
       if (ntile > 1) issue(1, blk);
     }
-    if (threadIdx.x == 0) next_wave = NW;   // waves 0..NW-1 go to warps 0..NW-1
     prefetched = false;
     __syncthreads();
     prof(0);
@@ -1266,6 +1273,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
       if (ntile > 1) issue(1, blk + 1);
     }
     prefetched = true;
+    setup(blk + 1);
     if (a.pixel_flags) {
       // no second grid barrier: wait until every pixel's owner has published this
       // block's shifts (owners finish reading the partials before they publish, so
