@@ -485,10 +485,10 @@ def run_gpu_arm(args):
     replicas = replica_check(st, world) if world > 1 else None
 
     # --- roofline of the dominant kernel ------------------------------------
-    # the dictionary step runs k_dict_ell2 (two tile stages) whenever its shared memory fits (P <= 220),
+    # the dictionary step runs k_dict_ell2 (two tile stages) whenever its shared memory fits (P <= 256),
     # else the single-stage k_dict_gram
     names = ["k_resid_compact (residual / carry)",
-             ("k_dict_ell2" if p <= 220 else "k_dict_gram") + " (dictionary step)", "k_code_compact (code step)",
+             ("k_dict_ell2" if p <= 256 else "k_dict_gram") + " (dictionary step)", "k_code_compact (code step)",
              "k_finish_stats+k_draw_pi_gamma"]
     per = [phase[i] / max(1, nph.value) for i in range(4)]
     dom = int(np.argmax(per))

@@ -740,7 +740,7 @@ __device__ __forceinline__ void atom_pixel_update(const double* rv, int pe, int 
     const AtomPre pr = pre ? pre[j] : atom_pre<B>(rv, j, pe, p, k0, geps, epoch, draws, key0, key1, dold);
     const float dn = atom_chain_step<B>(rv, j, pr, dl, geps);
     if (atoms_out) atoms_out[(int64_t)(k0 + j) * p + pe] = dn;
-    const float dd = dold[j * p + pe] - dn;   // the next pass's shift
+    const float dd = (float)pr.d_o - dn;   // the next pass's shift (d_o: the old atom, read before the write)
     dsh[j * p + pe] = dd;
     if (delta_out) delta_out[j * p + pe] = dd;
     dl[j] = (double)dd;
@@ -912,6 +912,13 @@ __device__ __forceinline__ void ell_elements(const DictGramArgs& a, const EllWav
 // The R = 2^lg runs of each column (lanes [R*g, R*g + R)) combine their sums
 // (transpose reduction inside the group) and add the column's totals to the
 // accumulator; each column sits in exactly one wave per tile.
+// Accumulator rows of 44 floats (ACS = 44) drop the four redundant Gram entries
+// G_j,j+1 (even j) of the 48-value register layout; ACS = 48 keeps the layout.
+__host__ __device__ constexpr bool gram_redundant(int i) { return i == 9 || i == 15 || i == 25 || i == 39; }
+__host__ __device__ constexpr int gram_compact(int i) { return i - (i > 9) - (i > 15) - (i > 25) - (i > 39); }
+static_assert(GramLayout<8>::gidx(0, 1) == 9 && GramLayout<8>::gidx(2, 3) == 15 && GramLayout<8>::gidx(4, 5) == 25 &&
+              GramLayout<8>::gidx(6, 7) == 39, "redundant entries of the 8-atom Gram layout");
+template <int ACS>
 __device__ __forceinline__ void ell_flush(float (&v)[GramLayout<kWB>::NP], int lg, int col, int lane, float* acc) {
   using L = GramLayout<kWB>;
   auto flush = [&](auto s_c) {
@@ -930,10 +937,19 @@ __device__ __forceinline__ void ell_flush(float (&v)[GramLayout<kWB>::NP], int l
       for (int o = SG / 2; o >= 1; o >>= 1) { cnt >>= 1; if (lane & o) vb += cnt; }
     }
     if (col != 0xFFFF && (S < 32 || lane < 16)) {
-      float* dst = acc + col * L::NACC + vb;
+      if constexpr (ACS == L::NACC) {
+        float* dst = acc + col * L::NACC + vb;
 #pragma unroll
-      for (int q = 0; q < R; ++q)
-        if (vb + q < L::NACC) dst[q] += v[q];
+        for (int q = 0; q < R; ++q)
+          if (vb + q < L::NACC) dst[q] += v[q];
+      } else {
+        float* dst = acc + col * ACS;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int i = vb + q;
+          if (i < L::NACC && !gram_redundant(i)) dst[gram_compact(i)] += v[q];
+        }
+      }
     }
   };
   switch (lg) {
@@ -1081,7 +1097,7 @@ __device__ __forceinline__ void dict_owner_phase(const DictGramArgs& a, unsigned
 // so a column is never flushed by two warps at once), summed in fixed order at
 // the end of the pass.  The next wave's first elements are loaded before the
 // current wave's flush.
-template <int NW>
+template <int NW, int ACS>   // ACS: accumulator row (48, or 44 without the redundant Gram entries for large P)
 __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
   using L = GramLayout<kWB>;
   constexpr int B = kWB;
@@ -1089,10 +1105,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
   const int p = a.p;
   // [stage 0: cur | prev][stage 1: cur | prev] (each block + its zero row), aliased
   // by the owner scratch in the update phase; then acc[2][p*NACC], dold, dprev
-  float* acc0 = (float*)(smraw + a.wbytes);
-  float* acc1 = acc0 + (size_t)p * L::NACC;
-  float* dold = acc1 + (size_t)p * L::NACC;
-  float* dprev = dold + B * p;
+  constexpr bool kSmemOld = ACS == L::NACC;   // the block's old atoms staged (else read from global)
+  float* acc0 = (float*)(smraw + a.wbytes);             // [p][ACS] even tiles
+  float* acc1 = acc0 + (size_t)p * ACS;                  // [p][ACS] odd tiles
+  float* dprev = acc1 + (size_t)p * ACS;                 // B * p shifts of the previous block
+  float* dold = dprev + B * p;                           // B * p old atoms of the block (kSmemOld)
   __shared__ __align__(8) uint64_t mbar[3];   // [0..1] stage fills, [2] owner partials
   __shared__ int done[2];
   __shared__ unsigned next_wave;   // dynamic wave claiming inside the CTA
@@ -1150,11 +1167,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
   // rows (the owner phase overwrote them), the wave counter.  For every pass but
   // the first it runs while the previous pass's shifts are still being published.
   auto setup = [&](int bk) {
-    const int nbk = bk < nblk ? min(B, a.k - bk * B) : 0;
-    for (int t = threadIdx.x; t < 2 * p * L::NACC; t += blockDim.x) acc0[t] = 0.0f;
-    for (int t = threadIdx.x; t < B * p; t += blockDim.x) {
-      const int j = t / p, pe = t - j * p;
-      dold[t] = j < nbk ? a.atoms[(int64_t)(bk * B + j) * p + pe] : 0.0f;
+    for (int t = threadIdx.x; t < 2 * p * ACS; t += blockDim.x) acc0[t] = 0.0f;
+    if constexpr (kSmemOld) {
+      const int nbk = bk < nblk ? min(B, a.k - bk * B) : 0;
+      for (int t = threadIdx.x; t < B * p; t += blockDim.x) {
+        const int j = t / p, pe = t - j * p;
+        dold[t] = j < nbk ? a.atoms[(int64_t)(bk * B + j) * p + pe] : 0.0f;
+      }
     }
     if (threadIdx.x < 16) {
       const int blkno = threadIdx.x >> 2, part = threadIdx.x & 3;
@@ -1232,7 +1251,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
             h = ell_header(a, wv, a.ell_base[t_lo + wu], lane);
             ell_prefetch(a, h, ib, rb, pol_last);
           }
-          if (has_cur) ell_flush(v, lg_c, col_c, lane, acc);
+          if (has_cur) ell_flush<ACS>(v, lg_c, col_c, lane, acc);
         }
         // count out of tile u; the last warp out refills its stage with tile u + 2
         __syncwarp();
@@ -1252,18 +1271,28 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
     if (!has_cur) break;
     __syncthreads();
     prof(3);
-    // pixel-major partials [pixel][CTA][NACC] (even + odd tile sums, fixed order), 16-byte chunks
-    static_assert(L::NACC % 4 == 0, "accumulator rows in 16-byte chunks");
-    for (int t = threadIdx.x; t < p * (L::NACC / 4); t += blockDim.x) {
-      const int pe = t / (L::NACC / 4), q4 = t - pe * (L::NACC / 4);
-      const float4 x = *(const float4*)(acc0 + pe * L::NACC + 4 * q4), y = *(const float4*)(acc1 + pe * L::NACC + 4 * q4);
-      *(float4*)(a.partials + ((size_t)pe * gridDim.x + blockIdx.x) * L::NACC + 4 * q4) =
-          make_float4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w);
+    // pixel-major partials [pixel][CTA][NACC] (even + odd tile sums, fixed order)
+    if constexpr (ACS == L::NACC) {   // 16-byte chunks
+      static_assert(L::NACC % 4 == 0, "accumulator rows in 16-byte chunks");
+      for (int t = threadIdx.x; t < p * (L::NACC / 4); t += blockDim.x) {
+        const int pe = t / (L::NACC / 4), q4 = t - pe * (L::NACC / 4);
+        const float4 x = *(const float4*)(acc0 + pe * L::NACC + 4 * q4), y = *(const float4*)(acc1 + pe * L::NACC + 4 * q4);
+        *(float4*)(a.partials + ((size_t)pe * gridDim.x + blockIdx.x) * L::NACC + 4 * q4) =
+            make_float4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w);
+      }
+    } else {   // expanded to the 48-layout; the redundant Gram entries (never read by the draws) as 0
+      for (int t = threadIdx.x; t < p * L::NACC; t += blockDim.x) {
+        const int pe = t / L::NACC, q = t - pe * L::NACC;
+        const int c = pe * ACS + gram_compact(q);
+        a.partials[((size_t)pe * gridDim.x + blockIdx.x) * L::NACC + q] = gram_redundant(q) ? 0.0f : acc0[c] + acc1[c];
+      }
     }
     prof(5);
     if (PB_DBG(a, 16)) grid_sync(a.bar); else grid_sync_mono(a.bar + 2, bar_target);
     prof(6);
-    dict_owner_phase<NW>(a, smraw, &mbar[2], pphase, k0, nb, geps, epoch, dold, dprev);
+    // the block's old atoms: staged, or straight from global memory (atom_pre reads each before its write)
+    dict_owner_phase<NW>(a, smraw, &mbar[2], pphase, k0, nb, geps, epoch, kSmemOld ? dold : a.atoms + (size_t)k0 * p,
+                         dprev);
     prof(7);
     if (a.split) return;  // split mode: the caller allreduces `reduced` across ranks, then k_dict_update
     // the next pass's first tiles do not depend on the shifts: stage them now
@@ -1375,7 +1404,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) k_dict_gram(DictGramArgs a) 
         if (has_prev && has_cur) ell_elements<true, true>(a, h, wst, dl2, v, ib, rb, pol_last);
         else if (has_cur) ell_elements<false, true>(a, h, wst, dl2, v, ib, rb, pol_last);
         else ell_elements<true, false>(a, h, wst, dl2, v, ib, rb, pol_last);
-        if (has_cur) ell_flush(v, h.lg, h.col, lane, acc);
+        if (has_cur) ell_flush<L::NACC>(v, h.lg, h.col, lane, acc);
       }
     }
     if (!has_cur) break;
@@ -1667,18 +1696,18 @@ static size_t dict_gram_smem(int p, size_t* wbytes_out) {
   return wbytes + (size_t)p * L::NACC * 4 + (size_t)2 * kWB * p * 4;
 }
 
-static size_t dict_ell2_smem(int p, size_t* wbytes_out);
+static size_t dict_ell2_smem(int p, int acs, size_t* wbytes_out);
 
-template <int NW, bool TWO>
+template <int NW, int TWO>   // TWO: 0 the single-stage kernel, else the two-stage one with accumulator rows of TWO
 static int launch_dict_gram_b(DictGramArgs a, cudaStream_t st) {
   constexpr int B = kWB;
   const int th = NW * 32;
   if (a.ld % 4) { set_error("usage/weights row pitch must be a multiple of 4 (got %lld)", (long long)a.ld); return PB_EVALUE; }
   size_t wbytes = 0;
-  const size_t smem = TWO ? dict_ell2_smem(a.p, &wbytes) : dict_gram_smem<NW>(a.p, &wbytes);
+  const size_t smem = TWO ? dict_ell2_smem(a.p, TWO, &wbytes) : dict_gram_smem<NW>(a.p, &wbytes);
   a.wbytes = (int)wbytes;
   if (smem > 225 * 1024) { set_error("patch size %d too large for the dictionary step", a.p); return PB_EUNSUPPORTED; }
-  auto kern = TWO ? k_dict_ell2<NW> : k_dict_gram<NW>;
+  auto kern = TWO == 48 ? k_dict_ell2<NW, 48> : TWO == 44 ? k_dict_ell2<NW, 44> : k_dict_gram<NW>;
   PB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   PB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, th, smem));
@@ -1701,11 +1730,11 @@ static int launch_dict_gram_b(DictGramArgs a, cudaStream_t st) {
   return PB_OK;
 }
 
-static size_t dict_ell2_smem(int p, size_t* wbytes_out) {
+static size_t dict_ell2_smem(int p, int acs, size_t* wbytes_out) {
   using L = GramLayout<kWB>;
   const size_t wbytes = std::max((size_t)4 * kWStride, (size_t)p * L::NACC * 8);
   if (wbytes_out) *wbytes_out = wbytes;
-  return wbytes + (size_t)2 * p * L::NACC * 4 + (size_t)2 * kWB * p * 4;
+  return wbytes + (size_t)2 * p * acs * 4 + (size_t)kWB * p * 4 * (acs == L::NACC ? 2 : 1);
 }
 
 int launch_dict_gram(const DictGramArgs& a_in, cudaStream_t st) {
@@ -1728,10 +1757,11 @@ int launch_dict_gram(const DictGramArgs& a_in, cudaStream_t st) {
     }
   }
   const int variant = PB_TUNE_INT("PB_DICT_VARIANT", 0);
-  if (variant == 0 && dict_ell2_smem(a.p, nullptr) <= 225 * 1024)
-    return launch_dict_gram_b<16, true>(a, st);
-  if (variant != 1 && 2 * dict_gram_smem<8>(a.p, nullptr) <= 226 * 1024) return launch_dict_gram_b<8, false>(a, st);
-  return launch_dict_gram_b<16, false>(a, st);
+  if (variant == 0 && dict_ell2_smem(a.p, 48, nullptr) <= 225 * 1024) return launch_dict_gram_b<16, 48>(a, st);
+  // large patches (configs[3], P = 256): 44-float accumulator rows, old atoms read from global
+  if (variant == 0 && dict_ell2_smem(a.p, 44, nullptr) <= 225 * 1024) return launch_dict_gram_b<16, 44>(a, st);
+  if (variant != 1 && 2 * dict_gram_smem<8>(a.p, nullptr) <= 226 * 1024) return launch_dict_gram_b<8, 0>(a, st);
+  return launch_dict_gram_b<16, 0>(a, st);
 }
 
 int launch_dict_update(const DictGramArgs& a, int blk, cudaStream_t st) {
