@@ -213,19 +213,17 @@ __device__ __forceinline__ void box_muller_fast(uint32_t a, uint32_t b, float& n
   n1 = rr * s;
 }
 
-// One atom of the code step for this patch: moments u = |d|^2_obs, v = <d, r>_obs
-// (_kernels.code_moments), the z/s draw (_code_params, bpfa.py:169-178 and
-// 262-269), the residual shift (_kernels.shift_codes) and the state write.
-template <int CMAX, int W, int G, int MODE>
-__device__ __forceinline__ void code_one(const CompactArgs& a, const CodeConst& c, CodeThread& t, int k, int64_t zo,
-                                         const float (&d)[W], float (&r)[CMAX], uint8_t z_old8, float s_old, float uu,
-                                         float gn, double ud, double gd) {
-  float u = 0.0f, v = 0.0f;
-#pragma unroll
-  for (int j = 0; j < W; ++j) {
-    u = fmaf(d[j], d[j], u);
-    v = fmaf(d[j], r[j], v);
-  }
+// One atom's z/s draw from its moments u = |d|^2_obs, v = <d, r>_obs
+// (_kernels.code_moments; G lanes: partial sums) (_code_params, bpfa.py:169-178
+// and 262-269); dw = w_old - w_new is the residual shift (_kernels.shift_codes:
+// r += dw * d), applied by the caller before code_commit writes the state.
+struct CodeDraw {
+  float dw, s_new, w_new;
+  bool z;
+};
+template <int G, int MODE>
+__device__ __forceinline__ CodeDraw code_draw(const CodeConst& c, int k, float u, float v, uint8_t z_old8, float s_old,
+                                              float uu, float gn, double ud, double gd) {
   if (G > 1) {
     u = gsum<G>(u);
     v = gsum<G>(v);
@@ -246,21 +244,65 @@ __device__ __forceinline__ void code_one(const CompactArgs& a, const CodeConst& 
     s_new = z ? fmaf(c.geps * proj, ra * ra, gn * ra) : gn * c.inv_sqrt_gs;
   }
   const float w_new = z ? s_new : 0.0f;
-  const float dw = w_old - w_new;
-#pragma unroll
-  for (int j = 0; j < W; ++j) r[j] = fmaf(dw, d[j], r[j]);
+  return CodeDraw{w_old - w_new, s_new, w_new, z};
+}
+
+// The state write of one drawn atom (lane g == 0 of a patch) and the z count.
+template <int MODE>
+__device__ __forceinline__ void code_commit(const CompactArgs& a, const CodeConst& c, CodeThread& t, int k, int64_t zo,
+                                            const CodeDraw& x) {
   const bool own = c.live && c.g == 0;
   if (own) {
-    a.usage[zo] = z ? 1 : 0;
-    a.weights[zo] = s_new;
-    if (MODE == kRngReplay) t.sq_w += (double)s_new * (double)s_new;
-    else t.sq_w8 = fmaf(s_new, s_new, t.sq_w8);
-    c.wrow[(k & 7) ^ c.wx] = w_new;
+    a.usage[zo] = x.z ? 1 : 0;
+    a.weights[zo] = x.s_new;
+    if (MODE == kRngReplay) t.sq_w += (double)x.s_new * (double)x.s_new;
+    else t.sq_w8 = fmaf(x.s_new, x.s_new, t.sq_w8);
+    c.wrow[(k & 7) ^ c.wx] = x.w_new;
   }
   // the warp's z count of atom k goes to lane k & 7's register; flushed to the
   // CTA's shared counts once per 8-atom group (code_atoms)
-  const int nz = __popc(__ballot_sync(0xffffffffu, z && own));
+  const int nz = __popc(__ballot_sync(0xffffffffu, x.z && own));
   if (c.lane == (k & 7)) t.mc += nz;
+}
+
+// One atom over W slots of scalar column values d (multi-lane patches).
+template <int CMAX, int W, int G, int MODE>
+__device__ __forceinline__ void code_one(const CompactArgs& a, const CodeConst& c, CodeThread& t, int k, int64_t zo,
+                                         const float (&d)[W], float (&r)[CMAX], uint8_t z_old8, float s_old,
+                                         float uu, float gn, double ud, double gd) {
+  float u = 0.0f, v = 0.0f;
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    u = fmaf(d[j], d[j], u);
+    v = fmaf(d[j], r[j], v);
+  }
+  const CodeDraw x = code_draw<G, MODE>(c, k, u, v, z_old8, s_old, uu, gn, ud, gd);
+#pragma unroll
+  for (int j = 0; j < W; ++j) r[j] = fmaf(x.dw, d[j], r[j]);
+  code_commit<MODE>(a, c, t, k, zo, x);
+}
+
+// One atom over W slots given as slot pairs (one lane per patch, W > 16):
+// every multiply-add a packed FFMA2, u and v as even- and odd-slot partial sums.
+template <int CMAX, int W, int G, int MODE>
+__device__ __forceinline__ void code_one_sp(const CompactArgs& a, const CodeConst& c, CodeThread& t, int k,
+                                            int64_t zo, const float2 (&d)[W / 2], float (&r)[CMAX],
+                                            uint8_t z_old8, float s_old, float uu, float gn, double ud, double gd) {
+  float2 u2 = make_float2(0.0f, 0.0f), v2 = make_float2(0.0f, 0.0f);
+#pragma unroll
+  for (int j = 0; j < W / 2; ++j) {
+    u2 = __ffma2_rn(d[j], d[j], u2);
+    v2 = __ffma2_rn(d[j], make_float2(r[2 * j], r[2 * j + 1]), v2);
+  }
+  const CodeDraw x = code_draw<G, MODE>(c, k, u2.x + u2.y, v2.x + v2.y, z_old8, s_old, uu, gn, ud, gd);
+  const float2 dw2 = make_float2(x.dw, x.dw);
+#pragma unroll
+  for (int j = 0; j < W / 2; ++j) {
+    const float2 rj = __ffma2_rn(dw2, d[j], make_float2(r[2 * j], r[2 * j + 1]));
+    r[2 * j] = rj.x;
+    r[2 * j + 1] = rj.y;
+  }
+  code_commit<MODE>(a, c, t, k, zo, x);
 }
 
 // Atoms [k0, k1) (k0 a multiple of 8) against the staged DT whose column 0 is
@@ -270,7 +312,8 @@ __device__ __forceinline__ void code_atoms(const CompactArgs& a, const CodeConst
                                            const float* dt, float (&r)[CMAX], int (&addr)[CMAX]) {
   // addr[j]: byte offset of slot j's DT row + the current pair's column; it
   // advances by 8 per pair (no per-slot address arithmetic beyond that)
-  constexpr bool kPair = W <= 16;  // register budget: 2W values of D per pair
+  constexpr bool kPair = W <= 16;            // register budget: 2W values of D per pair
+  constexpr bool kSlotPair = !kPair && G == 1 && W <= 24;   // (W = 32: spills)
   int64_t zo = (int64_t)k0 * a.ld + c.ic;
   const bool ld_state = !a.codes_zero;   // all codes zero (fresh / warm-reset state): nothing to load
   uint8_t za = 0, zb = 0;
@@ -304,7 +347,7 @@ __device__ __forceinline__ void code_atoms(const CompactArgs& a, const CodeConst
         uu1 = u01_24(rnd.y);
       }
       const char* col = (const char*)dt;
-      if (kPair) {
+      if constexpr (kPair && G > 1) {
         float d0[W], d1[W];
 #pragma unroll
         for (int j = 0; j < W; ++j) {
@@ -314,6 +357,43 @@ __device__ __forceinline__ void code_atoms(const CompactArgs& a, const CodeConst
         }
         code_one<CMAX, W, G, MODE>(a, c, t, k, zo, d0, r, za, sa, uu0, g0, ud0, gd0);
         if (k + 1 < k1) code_one<CMAX, W, G, MODE>(a, c, t, k + 1, zo + a.ld, d1, r, zb, sb, uu1, g1, ud1, gd1);
+      } else if constexpr (kPair) {
+        // both atoms' columns per slot in one 8-byte load; |d_k|^2 and |d_k+1|^2 as one FFMA2
+        float2 dd[W];
+        float2 u01 = make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+          dd[j] = *(const float2*)(col + addr[j]);
+          u01 = __ffma2_rn(dd[j], dd[j], u01);
+        }
+        float v = 0.0f;
+#pragma unroll
+        for (int j = 0; j < W; ++j) v = fmaf(dd[j].x, r[j], v);
+        const CodeDraw x0 = code_draw<G, MODE>(c, k, u01.x, v, za, sa, uu0, g0, ud0, gd0);
+#pragma unroll
+        for (int j = 0; j < W; ++j) r[j] = fmaf(x0.dw, dd[j].x, r[j]);
+        code_commit<MODE>(a, c, t, k, zo, x0);
+        if (k + 1 < k1) {
+          v = 0.0f;
+#pragma unroll
+          for (int j = 0; j < W; ++j) v = fmaf(dd[j].y, r[j], v);
+          const CodeDraw x1 = code_draw<G, MODE>(c, k + 1, u01.y, v, zb, sb, uu1, g1, ud1, gd1);
+#pragma unroll
+          for (int j = 0; j < W; ++j) r[j] = fmaf(x1.dw, dd[j].y, r[j]);
+          code_commit<MODE>(a, c, t, k + 1, zo + a.ld, x1);
+        }
+      } else if constexpr (kSlotPair) {
+        float2 d0[W / 2];
+#pragma unroll
+        for (int j = 0; j < W / 2; ++j)
+          d0[j] = make_float2(*(const float*)(col + addr[2 * j]), *(const float*)(col + addr[2 * j + 1]));
+        code_one_sp<CMAX, W, G, MODE>(a, c, t, k, zo, d0, r, za, sa, uu0, g0, ud0, gd0);
+        if (k + 1 < k1) {
+#pragma unroll
+          for (int j = 0; j < W / 2; ++j)
+            d0[j] = make_float2(*(const float*)(col + 4 + addr[2 * j]), *(const float*)(col + 4 + addr[2 * j + 1]));
+          code_one_sp<CMAX, W, G, MODE>(a, c, t, k + 1, zo + a.ld, d0, r, zb, sb, uu1, g1, ud1, gd1);
+        }
       } else {
         float d0[W];
 #pragma unroll
