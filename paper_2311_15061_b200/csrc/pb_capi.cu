@@ -137,6 +137,7 @@ static void phase_mark(int ph, cudaStream_t st) {
 
 // Optional in-kernel phase profile of the dictionary step (globaltimer, CTA 0..n thread 0).
 static unsigned long long* g_dict_prof = nullptr;
+static unsigned long long* g_wave_prof = nullptr;   // tuning builds: per-wave profile of the last epoch
 
 static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
   phase_begin();
@@ -199,6 +200,14 @@ static int run_epoch(const pb_epoch_desc* d, int32_t* m_out, cudaStream_t st) {
     g.draws = d->rng_mode == PB_RNG_REPLAY ? d->atom_draws : nullptr;
     g.sc = sc; g.partials = ws.partials; g.reduced = ws.reduced; g.bar = ws.bar; g.max_blocks = kMaxDictBlocks;
     g.prof = g_dict_prof;
+#ifdef PB_TUNING
+    {   // per-wave durations of pass 3 (PB_DICT_WAVE_PROF=1): written to gpurun_out/wave_prof.bin by pb_dict_profile
+      static unsigned long long* wp = nullptr;
+      if (!wp && PB_TUNE_FLAG("PB_DICT_WAVE_PROF")) { cudaMalloc(&wp, (size_t)3 << 24 << 3); g_wave_prof = wp; }
+      if (wp) cudaMemsetAsync(wp, 0, (size_t)3 << 24 << 3, st);
+      g.wprof = wp;
+    }
+#endif
     g.dbg = PB_TUNE_INT("PB_DICT_DEBUG", 0);   // profiling bits exist in tuning builds only
     g.n = d->n; g.p = d->p; g.k = d->k; g.key0 = k0; g.key1 = k1;
     g.ld = c.ld;
@@ -471,9 +480,16 @@ int pb_dict_profile(int32_t enable, double* slots_ns_out) {
       if (PB_TUNE_FLAG("PB_DICT_PROF_CTAS")) {  // per-CTA element-phase and barrier-1 times (profiling aid)
         for (int b = 0; b < kMaxDictBlocks; ++b) {
           if (!h[b * kProfSlots + 2]) continue;
-          fprintf(stderr, "cta %d elems %.4f tile_end %.4f sync1 %.4f\n", b, h[b * kProfSlots + 2] / 1e6,
-                  h[b * kProfSlots + 3] / 1e6, h[b * kProfSlots + 6] / 1e6);
+          fprintf(stderr, "cta %d elems %.4f tile_end %.4f sync1 %.4f fillwait %.4f\n", b, h[b * kProfSlots + 2] / 1e6,
+                  h[b * kProfSlots + 3] / 1e6, h[b * kProfSlots + 6] / 1e6, h[b * kProfSlots + 10] / 1e6);
         }
+      }
+      if (g_wave_prof) {   // tuning builds: raw per-wave profile (3 x u64 per wave) of the last dictionary launch
+        std::vector<unsigned long long> w((size_t)3 << 24);
+        PB_CUDA_TRY(cudaMemcpy(w.data(), g_wave_prof, w.size() * 8, cudaMemcpyDeviceToHost));
+        size_t n = w.size();
+        while (n >= 3 && !w[n - 3]) n -= 3;
+        if (FILE* f = fopen("gpurun_out/wave_prof.bin", "wb")) { fwrite(w.data(), 8, n, f); fclose(f); }
       }
       if (PB_TUNE_FLAG("PB_DICT_PROF_DUMP")) {  // per-CTA spread of each slot (profiling aid)
         for (int i = 0; i < kProfSlots; ++i) {

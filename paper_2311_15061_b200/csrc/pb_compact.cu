@@ -842,6 +842,7 @@ constexpr double kTileVisitCost = 500.0;   // ELL positions equivalent to one ti
 // floats, then the all-zero row kEllZeroRow that the ELL padding points to.
 constexpr uint32_t kWStride = (uint32_t)kTile * kWB * 4 + 128;
 constexpr int kEllPf = 8;   // elements in flight per lane in the element phase (6: +1-3 %)
+constexpr int kEllTail = 8;   // granularity of the element loop's exit (see ell_elements; 1: dictionary step +6-40 %)
 
 // One ELL wave (pb_index.cu) as seen by a lane: its run's column, the wave's
 // run length, log2 of the lanes per column, and the lane's first position.
@@ -948,12 +949,19 @@ __device__ __forceinline__ void ell_elements(const DictGramArgs& a, const EllWav
     const int more = lw - j0 - kEllPf;   // positions left after this chunk
 #pragma unroll
     for (int d = 0; d < kEllPf; ++d) {
-      if (j0 + d >= lw) break;
+      // the wave's last chunk ends at the next multiple of kEllTail: positions past
+      // lw run on the zero W row with r = 0 (no effect on the sums) and store nothing
+      // (fewer exits from the unrolled chunk: no accumulator copies at the joins)
+      if (d % kEllTail == 0 && j0 + d >= lw) break;
+      const bool real = kEllTail == 1 || j0 + d < lw;
       const uint32_t il = ib[d];
       float r = rb[d];
       if (d < more) {
         ib[d] = __ldg(ep + (kEllPf + d) * 32);
         rb[d] = rp[(kEllPf + d) * 32];
+      } else if (kEllTail > 1) {
+        ib[d] = kEllZeroRow;
+        rb[d] = 0.0f;
       }
       const uint32_t wo[2] = {il, il ^ 16u};
       if constexpr (HP) {  // r += w_prev . delta  (packed pairs, two independent chains)
@@ -966,7 +974,7 @@ __device__ __forceinline__ void ell_elements(const DictGramArgs& a, const EllWav
         }
 #pragma unroll
         for (int q = 0; q < B / 4; ++q) r += sh[q].x + sh[q].y;
-        rp[d * 32] = r;
+        if (real) rp[d * 32] = r;
       }
       if constexpr (HC) {
         float wc[B];
@@ -1306,10 +1314,16 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
         ell_prefetch(a, h, ib, rb, pol_last);
       }
       for (int u = 0; u < ntile; ++u) {
+        const uint64_t t_fw = (a.prof && threadIdx.x == 0) ? gtimer() : 0;
         mbar_wait(&mbar[u & 1], fill_parity(u));
+        if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * kProfSlots + 10] += gtimer() - t_fw;   // fill waits
         const uint32_t wcur_s = ell_stage_addr(sbase + (uint32_t)(u & 1) * 2 * kWStride);
         float* acc = (u & 1) ? acc1 : acc0;
         while (have && wu == u) {
+#ifdef PB_TUNING
+          const uint64_t t_w0 = (a.wprof && blk == 3 && lane == 0) ? gtimer() : 0;
+          const int64_t wv_self = wv;
+#endif
           float2 dl2[B / 2];
           const bool live = h.col != 0xFFFF;
 #pragma unroll
@@ -1332,6 +1346,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_dict_ell2(DictGramArgs a) {
             ell_prefetch(a, h, ib, rb, pol_last);
           }
           if (has_cur) ell_flush<ACS>(v, lg_c, col_c, lane, acc);
+#ifdef PB_TUNING
+          if (a.wprof && blk == 3 && lane == 0 && wv_self < ((int64_t)1 << 24)) {   // per-wave profile
+            unsigned smid;
+            asm("mov.u32 %0, %%smid;" : "=r"(smid));
+            a.wprof[3 * wv_self] = gtimer() - t_w0;
+            a.wprof[3 * wv_self + 1] = smid;
+            a.wprof[3 * wv_self + 2] = wid;
+          }
+#endif
         }
         // count out of tile u; the last warp out refills its stage with tile u + 2
         __syncwarp();

@@ -74,6 +74,7 @@ struct DictGramArgs {
   double* reduced;      // P * NACC
   unsigned* bar;        // [4] grid-barrier counters, then [P] per-pixel shift-ready flags (zeroed per launch)
   unsigned long long* prof;  // optional [gridDim][kProfSlots] phase nanoseconds (profiling)
+  unsigned long long* wprof;  // optional per-wave [ns, smid, warp] of pass 3 (tuning builds, profiling)
   int dbg;              // profiling-only: 4 skip the W/colptr bulk copies, 8 skip the element phase
   // split (multi-rank) mode: run the single pass blk_begin and stop after the
   // per-GPU reduction; the previous pass's shifts come from delta_g [B][P]
