@@ -841,7 +841,7 @@ constexpr double kTileVisitCost = 500.0;   // ELL positions equivalent to one ti
 // Byte stride of one staged W block in shared memory: the tile's kTile x 8
 // floats, then the all-zero row kEllZeroRow that the ELL padding points to.
 constexpr uint32_t kWStride = (uint32_t)kTile * kWB * 4 + 128;
-constexpr int kEllPf = 8;   // elements in flight per lane in the element phase (6: +1-3 %)
+constexpr int kEllPf = 5;   // elements per chunk / in flight per lane in the element phase (measured 2..8: 4-5 best; 8: +6 %)
 constexpr int kEllTail = 8;   // granularity of the element loop's exit (see ell_elements; 1: dictionary step +6-40 %)
 
 // One ELL wave (pb_index.cu) as seen by a lane: its run's column, the wave's
