@@ -438,15 +438,17 @@ __device__ __forceinline__ void stage_dt_chunk(float* dt, const CompactArgs& a, 
   for (int t = threadIdx.x; t < n4; t += blockDim.x) dst[t] = __ldg(src + t);
 }
 
-// Stage atoms [k0, k0+kn) transposed into DT straight from D (pitch kp, P+1
-// rows, zero row P and zero pad columns): the multi-lane (G > 1) variants, whose
-// register allocation the vector-copy path perturbs into spills.
-__device__ __forceinline__ void stage_atoms_t(float* dt, const float* __restrict__ atoms, int k0, int kn, int p,
-                                              int kp) {
-  for (int t = threadIdx.x; t < (p + 1) * kp; t += blockDim.x) {
-    const int kk = t / (p + 1), pe = t - kk * (p + 1);
-    dt[pe * kp + kk] = (pe < p && kk < kn) ? atoms[(int64_t)(k0 + kk) * p + pe] : 0.0f;
-  }
+// The same chunk through cp.async (global -> shared without registers): the
+// multi-lane (G > 1) variants, whose register allocation the vector-copy path
+// perturbs into spills, and which restage every chunk per block of patches when
+// D does not fit (the cube: K = 512, P = 256).  Caller synchronizes as above.
+__device__ __forceinline__ void stage_dt_chunk_async(float* dt, const CompactArgs& a, int ci) {
+  const float4* __restrict__ src = (const float4*)(a.dt_img + (int64_t)ci * a.dt_img_floats);
+  const uint32_t dst = smem_u32(dt);
+  const int n4 = (int)(a.dt_img_floats >> 2);
+  for (int t = threadIdx.x; t < n4; t += blockDim.x)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * t), "l"(src + t) : "memory");
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 template <int CMAX, int W, int G, int MODE>
@@ -459,7 +461,7 @@ __device__ __forceinline__ void code_patch_range(const CompactArgs& a, const Cod
       const int kn = min(a.kc, a.k - k0);
       __syncthreads();
       if constexpr (G == 1) stage_dt_chunk(dt, a, k0 / a.kc);
-      else stage_atoms_t(dt, a.atoms, k0, kn, a.p, kp);
+      else stage_dt_chunk_async(dt, a, k0 / a.kc);
       __syncthreads();
       code_atoms<CMAX, W, G, MODE>(a, c, t, k0, k0 + kn, dt, r, addr);
 #pragma unroll
@@ -477,7 +479,7 @@ __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
   extern __shared__ __align__(16) float sm[];
   const int kp = a.kc + 2;                     // DT row pitch (kc % 8 == 0  =>  kp/2 odd)
   float* dt = sm;                              // (P+1) * kp
-  float* logit = dt + (G == 1 ? a.dt_img_floats : (int64_t)(a.p + 1) * kp);  // K (after the DT chunk)
+  float* logit = dt + a.dt_img_floats;         // K (after the DT chunk)
   int* mcnt = (int*)(logit + a.k);             // K
   float* wwin = (float*)(mcnt + a.k);          // (blockDim / G) * (WS ? 8 : 9)
   __shared__ double red[32];
@@ -500,7 +502,7 @@ __global__ void __launch_bounds__(256, 2) k_code_compact(CompactArgs a) {
   }
   if (a.kc >= a.k) {
     if constexpr (G == 1) stage_dt_chunk(dt, a, 0);
-    else stage_atoms_t(dt, a.atoms, 0, a.k, a.p, kp);
+    else stage_dt_chunk_async(dt, a, 0);
   }
   __syncthreads();
   const int row_bytes = kp * 4;
