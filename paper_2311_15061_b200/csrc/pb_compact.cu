@@ -1119,6 +1119,18 @@ __device__ __forceinline__ void dict_owner_phase(const DictGramArgs& a, unsigned
   double* part64 = red64 + (size_t)((p + gridDim.x - 1) / gridDim.x) * L::NACC;  // [NPART][NACC] scratch
   AtomPre* pre = (AtomPre*)(part64 + NPART * L::NACC);                          // [B]
   float* pstage = (float*)(smraw + a.pstage_off);
+#ifdef PB_TUNING
+  uint64_t t_op = (a.prof && threadIdx.x == 0) ? gtimer() : 0;   // owner sub-phases (slots 1, 4, 11)
+  auto oprof = [&](int slot) {
+    if (a.prof && threadIdx.x == 0) {
+      const uint64_t now = gtimer();
+      a.prof[blockIdx.x * kProfSlots + slot] += now - t_op;
+      t_op = now;
+    }
+  };
+#else
+  auto oprof = [](int) {};
+#endif
   for (int i = 0; i < npl; ++i) {
     const int pe = blockIdx.x + i * gridDim.x;
     const float* pix = a.partials + (size_t)pe * gridDim.x * L::NACC;
@@ -1132,6 +1144,7 @@ __device__ __forceinline__ void dict_owner_phase(const DictGramArgs& a, unsigned
       mbar_wait(pbar, pphase);
       pphase ^= 1u;
     }
+    oprof(1);
     if (threadIdx.x < NPART * L::NACC) {
       const int q = threadIdx.x % L::NACC, part = threadIdx.x / L::NACC;
       const float* src = (a.pstage_off ? (const float*)pstage : pix) + q;
@@ -1160,6 +1173,7 @@ __device__ __forceinline__ void dict_owner_phase(const DictGramArgs& a, unsigned
       if (a.split) a.reduced[(size_t)pe * L::NACC + threadIdx.x] = sum;
     }
     __syncthreads();
+    oprof(4);
     if (a.split) continue;
     if ((int)threadIdx.x < nb)   // the parallel part of the B draws
       pre[threadIdx.x] = atom_pre<B>(red64 + (size_t)i * L::NACC, threadIdx.x, pe, p, k0, geps, epoch, a.draws,
@@ -1174,6 +1188,7 @@ __device__ __forceinline__ void dict_owner_phase(const DictGramArgs& a, unsigned
       }
     }
     __syncthreads();
+    oprof(11);
   }
 }
 

@@ -11,8 +11,9 @@ from paper_2311_15061_b200 import inputs  # noqa: E402
 from paper_2311_15061_b200 import patches as pp  # noqa: E402
 from tools.prof_epoch import CFGS  # noqa: E402
 
-NAMES = ["pass start (acc, atoms)", "-", "elements (warp 0)", "pass-end CTA barrier", "-",
-         "partials write", "grid sync 1", "owner phase", "grid sync 2", "delta load", "-", "-"]
+NAMES = ["pass start (acc, atoms)", "owner: partials copy wait", "elements (warp 0)", "pass-end CTA barrier",
+         "owner: f64 reduce", "partials write", "grid sync 1", "owner phase", "grid sync 2", "delta load",
+         "tile fill waits", "owner: draws + publish"]
 for cid in [int(x) for x in sys.argv[1:]] or [3, 2]:
     c = CFGS[cid]
     img = inputs.synthetic_texture(c["shape"], seed=0) if len(c["shape"]) == 2 else \
