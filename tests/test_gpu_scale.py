@@ -17,7 +17,11 @@ the oracle, which is bit-exact to patchbeam (tests/test_oracle_golden.py).
 * configs[3] crop: a 24x24x16 crop of the cube, 8x8x4, K = 64 (multi-lane code
   step, 16-warp dictionary variant), 3 epochs;
 * configs[4] band: 40 rows of the 4096x4096 10 % frame, 8x8, K = 256 (135K
-  patches, the full row width), 2 epochs.
+  patches, the full row width), 2 epochs;
+* cube with a dictionary larger than shared memory: 8x8x4 patches (P = 256),
+  K = 160 > the ~100 atoms a code-step chunk holds, ~64 observed per patch (the
+  2- and 4-lane variants restaging every chunk per block of patches, as
+  configs[3] with K = 512 does), 2 epochs.
 """
 
 import numpy as np
@@ -70,3 +74,11 @@ def test_configs4_band_teacher_forced():
     img = inputs.stem_lattice((4096, 4096), seed=0)[:40]
     mask = inputs.make_mask((4096, 4096), 0.10, "uniform-random", 0)[:40]
     _run("cfg4band", np.ascontiguousarray(img), np.ascontiguousarray(mask), (8, 8), 256, 2)
+
+
+def test_cube_chunked_dictionary_teacher_forced():
+    rng = np.random.default_rng(7)
+    base = inputs.stem_lattice((20, 22), seed=1)
+    img = base[:, :, None] * (0.6 + 0.4 * rng.random(12))[None, None, :]
+    mask = inputs.make_mask(img.shape, 0.25, "uniform-random", 1)
+    _run("cubechunk", img, mask, (8, 8, 4), 160, 2, mean_subtract=False)
