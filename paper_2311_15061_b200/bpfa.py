@@ -11,7 +11,8 @@ sampler state is device-resident:
   atom-major (K,N) device storage, so in-place edits such as the pipeline's
   warm-start ``state.usage[:] = False`` work unchanged (pipeline.py:232-233);
 * ``weight_precision``, ``noise_precision`` and ``epoch`` live in a 40-byte
-  device scalar block (``pb_scalars``) and are synced on attribute access.
+  device scalar block (``pb_scalars``); the first read after a sweep copies the
+  block to the host once, later reads use that copy until the next sweep.
 
 RNG modes (``rng=``):
   ``"numpy"``  — the reference's own keyed Philox4x64 streams, drawn on the
@@ -108,6 +109,7 @@ class GibbsState:
         self.scalars = scalars          # 40-byte pb_scalars block (uint8 tensor)
         self.seed = int(seed)
         self._workspace = None
+        self._sc_cache = None           # host copy of the scalar block (see _sc)
         self._resid_key = None          # residual in the workspace belongs to this key
         # codes known to be all zero at these tensor versions (fresh init / reset_codes)
         self._zero_key = self._codes_key() if codes_zero else None
@@ -146,7 +148,15 @@ class GibbsState:
 
     # -- device scalars ---------------------------------------------------
     def _sc(self) -> _lib.Scalars:
-        return _lib.Scalars.from_buffer_copy(self.scalars.cpu().numpy().tobytes())
+        """Host copy of the device scalar block.  One device->host read per change:
+        the copy is kept until a sweep is launched on this state (_epoch_desc drops
+        it) or the tensor is written through torch (version counter)."""
+        key = (id(self.scalars), self.scalars._version)
+        c = getattr(self, "_sc_cache", None)
+        if c is None or c[0] != key:
+            c = (key, bytes(self.scalars.cpu().numpy().tobytes()))
+            self._sc_cache = c
+        return _lib.Scalars.from_buffer_copy(c[1])
 
     def _set_sc(self, **kw):
         s = self._sc()
@@ -292,6 +302,7 @@ def _epoch_desc(state: GibbsState, pm: PatchMatrix, hp: Hyperparams, freeze: boo
     d.atoms, d.pi = state.dictionary.atoms.data_ptr(), state.dictionary.pi.data_ptr()
     d.usage, d.weights = state.usage_kn.data_ptr(), state.weights_kn.data_ptr()
     d.scalars = state.scalars.data_ptr()
+    state._sc_cache = None   # the sweep rewrites the scalar block on the device
     d.workspace = ws.data_ptr()
     return d, m
 
