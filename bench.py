@@ -24,10 +24,13 @@ updates/s (higher is better).
              patchbeam itself): replay mode (same draws) and Philox mode (mean
              over 3 seeds) for configs[0] in full, configs[2] live, a configs[1] crop;
 * roofline   the dominant kernel (by measured phase time) against MEASURED_PEAKS.json;
-* cpu_baseline  the oracle port (numpy + OpenMP C restatement of the reference
-             kernels, f64) on bounded bands of the same frame, host cores.
+* cpu_baseline  the reference's own CPU path — the unmodified patchbeam installed in
+             baseline/_ref (its Numba kernels through bpfa.gibbs_epoch, all host
+             threads) when present, else the oracle port (numpy + OpenMP C
+             restatement, f64; measured 12 % slower than patchbeam on the box,
+             profiles/r02/cpu_ref_vs_port.json) — on bounded bands of the same frame.
 
---impl reference runs that CPU port alone on the same metric and config (rank 0
+--impl reference runs that CPU path alone on the same metric and config (rank 0
 only): each step is one full Gibbs epoch over one 64-row band of the frame,
 consecutive steps walking the bands.
 
@@ -136,6 +139,84 @@ def cpu_epoch_sample(cfg, seconds_budget=20.0, steps=None, warmup=0):
                        f"epochs walking its {nbands} bands")
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_available():
+    return os.path.isdir(os.path.join(REF_DIR, "patchbeam"))
+
+
+def ref_epoch_sample(cfg, seconds_budget=20.0, steps=None, warmup=1):
+    """The UNMODIFIED reference (patchbeam from baseline/_ref, its own Numba kernels
+    and public API, all host threads) on the same CROP_ROWS-row bands as
+    cpu_epoch_sample.  The first warm-up epoch includes Numba's compilation."""
+    import tempfile
+
+    cache = os.path.join(ROOT, "baseline", "_numba_cache")   # git-ignored; compiled once per box
+    try:
+        os.makedirs(cache, exist_ok=True)
+    except OSError:
+        cache = tempfile.mkdtemp(prefix="numba_")
+    os.environ.setdefault("NUMBA_CACHE_DIR", cache)
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import numba
+    from patchbeam import bpfa as rb
+    from patchbeam.patches import PatchSpec as RSpec
+    from patchbeam.patches import extract_patches as rextract
+
+    img, mask = workload_inputs(cfg)
+    nbands = cfg["shape"][0] // CROP_ROWS
+    hp = rb.Hyperparams(num_atoms=cfg["k"])
+
+    def band(t):
+        b = t % nbands
+        sl = slice(b * CROP_ROWS, (b + 1) * CROP_ROWS)
+        pm = rextract(np.ascontiguousarray(img[sl]), np.ascontiguousarray(mask[sl]), RSpec(cfg["patch"]),
+                      mean_subtract=True)
+        return pm, rb.init_state(pm, hp, cfg["seed"], init_mode="prior")
+
+    for _ in range(max(1, warmup)):
+        pm, st = band(0)
+        rb.gibbs_epoch(st, pm, hp)
+    times, upd = [], 0
+    t_all = time.perf_counter()
+    t = 0
+    while True:
+        pm, st = band(t)
+        t0 = time.perf_counter()
+        rb.gibbs_epoch(st, pm, hp)
+        times.append(time.perf_counter() - t0)
+        upd += pm.values.shape[0] * cfg["k"]
+        t += 1
+        if steps is not None:
+            if len(times) >= steps:
+                break
+        elif time.perf_counter() - t_all >= seconds_budget:
+            break
+    return dict(updates=upd, times=times, cores=numba.get_num_threads(), kind="reference",
+                sample=f"{len(times)} full Gibbs epoch(s) (K={cfg['k']}, f64) of the unmodified reference "
+                       f"(patchbeam from baseline/_ref, Numba kernels, bpfa.gibbs_epoch), each over one "
+                       f"{CROP_ROWS}-row band of the frame (N={pm.values.shape[0]}), consecutive epochs walking "
+                       f"its {nbands} bands")
+
+
+def cpu_reference_sample(cfg, **kw):
+    """The reference's own CPU path when it is installed (baseline/_ref), else the
+    oracle port of it (kind "port")."""
+    if reference_available():
+        try:
+            return ref_epoch_sample(cfg, **kw)
+        except Exception as e:  # noqa: BLE001 - fall back to the port, saying why
+            r = cpu_epoch_sample(cfg, **kw)
+            r["kind"] = "port"
+            r["sample"] += f" (reference unavailable: {type(e).__name__}: {e})"
+            return r
+    r = cpu_epoch_sample(cfg, **kw)
+    r["kind"] = "port"
+    return r
+
+
 def headline_config(world, n_units, extra=None):
     cfg = workload(world)
     c = {"workload": cfg["what"], "global_batch": n_units, "seq_len": 1,
@@ -149,7 +230,7 @@ def run_reference_arm(args):
     if int(os.environ.get("RANK", "0")) != 0:
         return
     cfg = workload(world)
-    r = cpu_epoch_sample(cfg, steps=args.steps, warmup=args.warmup)
+    r = cpu_reference_sample(cfg, steps=args.steps, warmup=args.warmup)
     total = sum(r["times"])
     v = r["updates"] / total
     n_units = grid_n(cfg["shape"], cfg["patch"])
@@ -159,7 +240,7 @@ def run_reference_arm(args):
         "ms_per_step": 1e3 * total / len(r["times"]), "higher_is_better": True,
         "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": headline_config(world, n_units),
-        "cpu_baseline": {"value": v, "unit": "updates/s", "cores": r["cores"], "kind": "port",
+        "cpu_baseline": {"value": v, "unit": "updates/s", "cores": r["cores"], "kind": r["kind"],
                          "sample": r["sample"]},
         "e2e": {"value": v, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -601,9 +682,9 @@ def run_gpu_arm(args):
     if world == 1 and not args.no_configs:
         line["configs"] = all_configs(args)
     if rank == 0 and world == 1 and not args.no_cpu:
-        r = cpu_epoch_sample(cfg, seconds_budget=args.cpu_seconds)
+        r = cpu_reference_sample(cfg, seconds_budget=args.cpu_seconds)
         line["cpu_baseline"] = {"value": r["updates"] / sum(r["times"]), "unit": "updates/s",
-                                "cores": r["cores"], "kind": "port", "sample": r["sample"]}
+                                "cores": r["cores"], "kind": r["kind"], "sample": r["sample"]}
         full = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "cpu_fullframe.json")), reverse=True)
         if full:
             line["cpu_baseline"]["full_frame"] = json.load(open(full[0]))
