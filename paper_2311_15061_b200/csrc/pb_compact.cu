@@ -844,7 +844,7 @@ constexpr double kTileVisitCost = 500.0;   // ELL positions equivalent to one ti
 // floats, then the all-zero row kEllZeroRow that the ELL padding points to.
 constexpr uint32_t kWStride = (uint32_t)kTile * kWB * 4 + 128;
 constexpr int kEllPf = 5;   // elements per chunk / in flight per lane in the element phase (measured 2..8: 4-5 best; 8: +6 %)
-constexpr int kEllTail = 8;   // granularity of the element loop's exit (see ell_elements; 1: dictionary step +6-40 %)
+constexpr int kEllTail = kEllPf;   // granularity of the element loop's exit: whole chunks (see ell_elements; 1: +6-40 %)
 
 // One ELL wave (pb_index.cu) as seen by a lane: its run's column, the wave's
 // run length, log2 of the lanes per column, and the lane's first position.
@@ -951,7 +951,7 @@ __device__ __forceinline__ void ell_elements(const DictGramArgs& a, const EllWav
     const int more = lw - j0 - kEllPf;   // positions left after this chunk
 #pragma unroll
     for (int d = 0; d < kEllPf; ++d) {
-      // the wave's last chunk ends at the next multiple of kEllTail: positions past
+      // the wave's last chunk runs to a multiple of kEllTail positions: positions past
       // lw run on the zero W row with r = 0 (no effect on the sums) and store nothing
       // (fewer exits from the unrolled chunk: no accumulator copies at the joins)
       if (d % kEllTail == 0 && j0 + d >= lw) break;
