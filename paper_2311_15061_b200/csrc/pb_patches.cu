@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(kXR * kXC) k_extract2d(Geo2 g, const T* __rest
 // cost the 8x32-tile kernel 100 MB of DRAM reads at configs[1]).  The window is
 // B0 rows x (255*s1 + B1) elements.
 constexpr int kXW = 256;
-template <typename T>
+template <typename T, int CB0, int CB1>   // CB0, CB1 > 0: patch shape known at compile time (unrolled plane loop)
 __global__ void __launch_bounds__(kXW) k_extract2r(Geo2 g, const T* __restrict__ tensor, const uint8_t* __restrict__ mask,
                                                    int mean_subtract, float* __restrict__ values,
                                                    uint8_t* __restrict__ obs, float* __restrict__ means,
@@ -329,13 +329,31 @@ __global__ void __launch_bounds__(kXW) k_extract2r(Geo2 g, const T* __restrict__
     const double mean = (mean_subtract && cnt > 0) ? sum / (double)cnt : 0.0;
     means[li] = (float)mean;
     counts[li] = cnt;
-    int64_t q = li;
-    for (int a = 0; a < g.b0; ++a) {
-      const int rb = wb + a * w1;
-      for (int b = 0; b < g.b1; ++b, q += cnt_patches) {
-        const uint8_t o = so[rb + b] ? 1 : 0;
-        values[q] = o ? (float)((double)sv[rb + b] - mean) : 0.0f;
-        obs[q] = o;
+    if constexpr (CB0 > 0 && CB1 > 0) {
+      // unrolled: shared loads at immediate offsets, one pointer bump per plane
+      float* vp = values + li;
+      uint8_t* op = obs + li;
+      const T* svb = sv + wb;
+      const uint8_t* sob = so + wb;
+#pragma unroll
+      for (int a = 0; a < CB0; ++a)
+#pragma unroll
+        for (int b = 0; b < CB1; ++b) {
+          const uint8_t o = sob[a * w1 + b] ? 1 : 0;
+          *vp = o ? (float)((double)svb[a * w1 + b] - mean) : 0.0f;
+          *op = o;
+          vp += cnt_patches;
+          op += cnt_patches;
+        }
+    } else {
+      int64_t q = li;
+      for (int a = 0; a < g.b0; ++a) {
+        const int rb = wb + a * w1;
+        for (int b = 0; b < g.b1; ++b, q += cnt_patches) {
+          const uint8_t o = so[rb + b] ? 1 : 0;
+          values[q] = o ? (float)((double)sv[rb + b] - mean) : 0.0f;
+          obs[q] = o;
+        }
       }
     }
   }
@@ -393,6 +411,96 @@ __global__ void __launch_bounds__(256) k_reconstitute2d(Geo2 g, const float* __r
   }
 }
 
+// Overlap-add, rank 2, stride 1 along the row, patch width B1 in {8, 10}: a
+// CTA takes kOW consecutive output elements of ONE frame row y.  Every (patch
+// row a0, patch column c) pair that covers the row is one contiguous run of
+// the plane (y - a0*s0)*B1 + c over the patches a0*gc1 + [x0-B1+1, x0+kOW),
+// so per covering patch row the CTA stages B1 runs plus the means run into
+// shared memory with cp.async (coalesced, no register staging; the next patch
+// row's stage is in flight while this one is summed — double buffered), and
+// each thread adds its pixel's covering patches in the reference's ascending
+// patch order.  Run entries of patches that do not exist (a1 < 0 or >= gc1,
+// the frame's left / right margins) are zero, so the pixel loop is uniform and
+// unrolled: a missing patch adds +0.0, which leaves the f64 sum unchanged
+// (bit-identical to k_reconstitute2d, tests/test_gpu_patches.py).
+// Measured (configs[1], tools/patch_timing.py): gather form 0.187 ms -> all
+// rows staged at once 0.16 -> double-buffered rows, kOW 128: 0.140 -> kOW 256:
+// 0.121 ms; a three-stage ring measured 0.138.
+constexpr int kOW = 256;
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+
+template <typename T, int B1>
+__global__ void __launch_bounds__(kOW) k_ola2s(Geo2 g, const float* __restrict__ est, float est_scale,
+                                               const float* __restrict__ means, const T* __restrict__ original,
+                                               const uint8_t* __restrict__ mask, int dc, T* __restrict__ out,
+                                               unsigned long long* __restrict__ uncovered) {
+  constexpr int L = kOW + B1 - 1;                 // patch columns a staged run spans
+  constexpr int LP = L + 1;                       // run pitch
+  constexpr int SZ = (B1 + 1) * LP;               // one stage: B1 runs + the means run
+  constexpr int NS = 2;                           // double-buffered patch-row stages
+  __shared__ __align__(16) float os[NS][SZ];
+  const int64_t segs = (g.m1 + kOW - 1) / kOW;
+  const int64_t ntile = g.m0 * segs;
+  const double scale = (double)est_scale;
+  for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+    const int64_t y = tile / segs, x0 = (tile - y * segs) * kOW;
+    int64_t lo0, hi0;
+    cover_range(y, g.b0, g.s0, g.gc0, lo0, hi0);
+    const int na = hi0 >= lo0 ? (int)(hi0 - lo0 + 1) : 0;
+    const int64_t base = x0 - B1 + 1;             // patch column of run element 0
+    // stage patch row a0 = lo0 + j into buffer j % NS (one cp.async group)
+    auto issue = [&](int j) {
+      const int64_t a0 = lo0 + j;
+      const float* src = est + (y - a0 * g.s0) * B1 * g.n + a0 * g.gc1 + base;
+      const float* msrc = means + a0 * g.gc1 + base;
+      float* dst = os[j % NS];
+      for (int t = threadIdx.x; t < L; t += kOW) {
+        const int64_t a1 = base + t;
+        if (a1 < 0 || a1 >= g.gc1) {            // no such patch: a zero term
+#pragma unroll
+          for (int c = 0; c <= B1; ++c) dst[c * LP + t] = 0.f;
+          continue;
+        }
+        const float* sp = src + t;
+#pragma unroll
+        for (int c = 0; c < B1; ++c, sp += g.n) cp_async4(dst + c * LP + t, sp);
+        cp_async4(dst + B1 * LP + t, msrc + t);
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    __syncthreads();                              // the previous tile's stages are consumed
+    if (na > 0) issue(0);
+    const int64_t x = x0 + threadIdx.x;
+    double acc = 0.0;
+    for (int j = 0; j < na; ++j) {
+      if (j + 1 < na) {
+        issue(j + 1);                             // its buffer was released by the barrier below
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      }
+      __syncthreads();
+      // patch a1 = x - B1 + 1 + u: run column threadIdx.x + u, plane column B1 - 1 - u
+      const float* run = os[j % NS] + threadIdx.x;
+#pragma unroll
+      for (int u = 0; u < B1; ++u) acc += (double)run[(B1 - 1 - u) * LP + u] * scale + (double)run[B1 * LP + u];
+      __syncthreads();
+    }
+    if (x >= g.m1) continue;
+    int64_t lo1, hi1;
+    cover_range(x, B1, 1, g.gc1, lo1, hi1);
+    const int64_t cov = (na > 0 && hi1 >= lo1) ? (int64_t)na * (hi1 - lo1 + 1) : 0;
+    const int64_t xx = y * g.m1 + x;
+    double v = cov > 0 ? acc / (double)cov : 0.0;
+    if (cov == 0 && uncovered) atomicAdd(uncovered, 1ull);
+    if (dc && mask[xx]) v = (double)original[xx];
+    out[xx] = (T)v;
+  }
+}
+
 static int grid_blocks(int64_t work, int threads) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -416,12 +524,16 @@ int launch_extract(const Grid& grid, const void* tensor, int f64, const uint8_t*
       const int tpr = (int)((g2.gc1 + 2 * kXW - 1) / kXW);
       const int64_t rows = (i0 + cnt - 1) / g2.gc1 - i0 / g2.gc1 + 1;
       const int nb2 = (int)std::min<int64_t>(rows * tpr, 148 * 16);
-      if (f64)
-        k_extract2r<double><<<nb2, kXW, smem_r, st>>>(g2, (const double*)tensor, mask, mean_subtract, values, obs,
-                                                      means, counts, i0, cnt, tpr);
-      else
-        k_extract2r<float><<<nb2, kXW, smem_r, st>>>(g2, (const float*)tensor, mask, mean_subtract, values, obs,
-                                                     means, counts, i0, cnt, tpr);
+#define PB_X2R(T, B0, B1)                                                                                   \
+  k_extract2r<T, B0, B1><<<nb2, kXW, smem_r, st>>>(g2, (const T*)tensor, mask, mean_subtract, values, obs, means, \
+                                                   counts, i0, cnt, tpr)
+#define PB_X2R_SHAPES(T)                                                              \
+  if (g2.b0 == 10 && g2.b1 == 10) PB_X2R(T, 10, 10);                                  \
+  else if (g2.b0 == 8 && g2.b1 == 8) PB_X2R(T, 8, 8);                                 \
+  else PB_X2R(T, 0, 0)
+      if (f64) { PB_X2R_SHAPES(double); } else { PB_X2R_SHAPES(float); }
+#undef PB_X2R_SHAPES
+#undef PB_X2R
       PB_LAUNCH_CHECK();
       return PB_OK;
     }
@@ -457,6 +569,23 @@ int launch_reconstitute(const Grid& grid, const float* est, float est_scale, con
   const int th = 256;
   if (grid.rank == 2) {
     const Geo2 g2 = make_geo2(grid);
+    if (g2.s1 == 1 && (g2.b1 == 8 || g2.b1 == 10)) {   // staged runs (configs[0..2], [4])
+      const void* fn = f64 ? (g2.b1 == 8 ? (const void*)k_ola2s<double, 8> : (const void*)k_ola2s<double, 10>)
+                           : (g2.b1 == 8 ? (const void*)k_ola2s<float, 8> : (const void*)k_ola2s<float, 10>);
+      int dev = 0, sms = 148, per_sm = 1;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kOW, 0);
+      const int64_t ntile = g2.m0 * ((g2.m1 + kOW - 1) / kOW);
+      const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ntile, (int64_t)sms * std::max(per_sm, 1)));
+#define PB_OLA2S(T, BB)                                                                                        \
+  k_ola2s<T, BB><<<nb, kOW, 0, st>>>(g2, est, est_scale, means, (const T*)original, mask, dc, (T*)out, uncovered)
+      if (f64) { if (g2.b1 == 8) PB_OLA2S(double, 8); else PB_OLA2S(double, 10); }
+      else { if (g2.b1 == 8) PB_OLA2S(float, 8); else PB_OLA2S(float, 10); }
+#undef PB_OLA2S
+      PB_LAUNCH_CHECK();
+      return PB_OK;
+    }
     const int nb2 = grid_blocks(g2.m0 * g2.m1, th);
 #define PB_OLA2(T, BB)                                                                                      \
   k_reconstitute2d<T, BB><<<nb2, th, 0, st>>>(g2, est, est_scale, means, (const T*)original, mask, dc, (T*)out, \

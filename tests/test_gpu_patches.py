@@ -254,3 +254,36 @@ def test_observed_element_index_exact(cuda_device, shape, patch, ratio, kind):
             spread += quarter_cost(blk)
             ascending += quarter_cost(asc)
     assert spread <= ascending, (spread, ascending)
+
+
+@pytest.mark.parametrize("shape,patch,stride,f32", [((70, 1100), (10, 10), (1, 1), False),   # wide: row tiles
+                                                    ((300, 800), (8, 8), (1, 1), True),
+                                                    ((45, 333), (6, 5), (1, 1), False),     # runtime shape
+                                                    ((64, 64), (10, 10), (3, 1), False),    # row stride > 1
+                                                    ((64, 90), (7, 7), (2, 3), True),       # fallback OLA
+                                                    ((9, 300), (10, 10), (1, 1), False)])   # < one patch row of
+def test_rank2_fast_paths_bit_identical_to_generic(cuda_device, shape, patch, stride, f32):   # output rows
+    """The rank-2 kernels (shared-memory windows for extraction, staged runs for
+    overlap-add) against the generic N-D kernels on the same frame viewed as
+    (1, H, W): identical values, flags, means and reconstructions, bit for bit
+    (same per-element arithmetic and the same ascending patch order)."""
+    rng = np.random.default_rng(11)
+    if shape[0] < patch[0]:
+        patch = (shape[0], patch[1])
+    t = rng.random(shape)
+    mask = rng.random(shape) < 0.2
+    dt = torch.float32 if f32 else torch.float64
+    tt = torch.as_tensor(t, dtype=dt, device="cuda")
+    mm = torch.as_tensor(mask, device="cuda")
+    pm2 = pp.extract_patches(tt, mm, pp.PatchSpec(patch, stride), True)
+    pm3 = pp.extract_patches(tt[None], mm[None], pp.PatchSpec((1,) + patch, (1,) + stride), True)
+    assert torch.equal(pm2.values_pn, pm3.values_pn)
+    assert torch.equal(pm2.observed_pn, pm3.observed_pn)
+    assert torch.equal(pm2.means_dev, pm3.means_dev) and torch.equal(pm2.counts, pm3.counts)
+    est = torch.randn(pm2.values_pn.shape, device="cuda")
+    for dc in (False, True):
+        kw = dict(dc_original=tt, dc_mask=mm) if dc else {}
+        kw3 = dict(dc_original=tt[None], dc_mask=mm[None]) if dc else {}
+        r2 = pp.reconstitute(pm2, est.T, out="device", dtype=dt, **kw)
+        r3 = pp.reconstitute(pm3, est.T, out="device", dtype=dt, **kw3)
+        assert torch.equal(r2, r3[0]), (shape, patch, stride, dc)
