@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(kXR * kXC) k_extract2d(Geo2 g, const T* __rest
 // B0 rows x (255*s1 + B1) elements.
 constexpr int kXW = 256;
 template <typename T, int CB0, int CB1>   // CB0, CB1 > 0: patch shape known at compile time (unrolled plane loop)
-__global__ void __launch_bounds__(kXW) k_extract2r(Geo2 g, const T* __restrict__ tensor, const uint8_t* __restrict__ mask,
+__global__ void __launch_bounds__(kXW, CB0 == 8 ? 3 : (CB0 == 10 ? 2 : 1)) k_extract2r(Geo2 g, const T* __restrict__ tensor, const uint8_t* __restrict__ mask,
                                                    int mean_subtract, float* __restrict__ values,
                                                    uint8_t* __restrict__ obs, float* __restrict__ means,
                                                    int32_t* __restrict__ counts, int64_t i0, int64_t cnt_patches,
@@ -298,12 +298,34 @@ __global__ void __launch_bounds__(kXW) k_extract2r(Geo2 g, const T* __restrict__
     const int64_t sx = (int64_t)((32 - off) % 32) - kXW + (int64_t)kXW * k;   // first origin of the tile (may be < 0)
     __syncthreads();   // the previous tile's window is consumed
     const int64_t y0 = gy * g.s0, x0 = sx * g.s1;
-    for (int e = threadIdx.x; e < g.b0 * w1; e += blockDim.x) {
-      const int r = e / w1, c = e - r * w1;
-      const int64_t y = y0 + r, x = x0 + c;
-      const bool in = x >= 0 && y < g.m0 && x < g.m1;
-      sv[e] = in ? tensor[y * g.m1 + x] : (T)0;
-      so[e] = in ? mask[y * g.m1 + x] : 0;
+    if constexpr (CB0 > 0) {
+      // window rows unrolled: a thread's CB0 loads of column c are all in flight
+      // before the first shared store (one load latency per tile, not CB0)
+      for (int c = threadIdx.x; c < w1; c += blockDim.x) {
+        const int64_t x = x0 + c;
+        T v[CB0];
+        uint8_t mk[CB0];
+#pragma unroll
+        for (int r = 0; r < CB0; ++r) {
+          const int64_t y = y0 + r;
+          const bool in = x >= 0 && y < g.m0 && x < g.m1;
+          v[r] = in ? tensor[y * g.m1 + x] : (T)0;
+          mk[r] = in ? mask[y * g.m1 + x] : 0;
+        }
+#pragma unroll
+        for (int r = 0; r < CB0; ++r) {
+          sv[r * w1 + c] = v[r];
+          so[r * w1 + c] = mk[r];
+        }
+      }
+    } else {
+      for (int e = threadIdx.x; e < g.b0 * w1; e += blockDim.x) {
+        const int r = e / w1, c = e - r * w1;
+        const int64_t y = y0 + r, x = x0 + c;
+        const bool in = x >= 0 && y < g.m0 && x < g.m1;
+        sv[e] = in ? tensor[y * g.m1 + x] : (T)0;
+        so[e] = in ? mask[y * g.m1 + x] : 0;
+      }
     }
     __syncthreads();
     // column sums of the window (shared by the B1 patches that cover a column):
