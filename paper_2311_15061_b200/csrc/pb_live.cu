@@ -8,14 +8,13 @@
 //                    of the masked input (server.py:46-53: round(clip(x,0,1)·255),
 //                    rank-3 tensors show slice 0) — one pass over the frame.
 //  adaptive mask     sampling.py:184-207 on device: the exploit set is the top
-//                    round(f·budget) residuals, ties by lowest flat index (a
-//                    stable descending radix sort of (residual, index) pairs —
-//                    the reference's argsort(-r, kind="stable")); the explore
-//                    set is drawn uniformly without replacement from the rest
-//                    by sorting Philox keys (device stream, keyed by seed and
-//                    frame index; not numpy's Generator.choice stream).
-#include <cub/cub.cuh>
-
+//                    round(f·budget) residuals, ties by lowest flat index (the
+//                    first n of the reference's argsort(-r, kind="stable")); the
+//                    explore set is drawn uniformly without replacement from the
+//                    rest as the n smallest Philox keys (device stream, keyed by
+//                    seed and frame index; not numpy's Generator.choice stream).
+//                    Both are a radix SELECT of the n largest 64-bit keys
+//                    (pb_select.cu), not a sort of all m (key, index) pairs.
 #include "pb_live.cuh"
 
 namespace pb {
@@ -75,27 +74,28 @@ __global__ void k_adaptive_check(const double* __restrict__ r, int64_t m, unsign
   }
 }
 
-__global__ void k_iota(int64_t* __restrict__ idx, int64_t m) {
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < m; x += (int64_t)gridDim.x * blockDim.x)
-    idx[x] = x;
+// Exploit keys: the residual's bit pattern (monotone for non-negative
+// doubles; -0.0 and +0.0 tie as 0).
+__global__ void k_resid_keys(const double* __restrict__ r, int64_t m, uint64_t* __restrict__ keys) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < m; x += (int64_t)gridDim.x * blockDim.x) {
+    const double v = r[x];
+    keys[x] = v > 0.0 ? (uint64_t)__double_as_longlong(v) : 0ull;
+  }
 }
 
-__global__ void k_mark(const int64_t* __restrict__ idx, int64_t cnt, uint8_t* __restrict__ mask) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < cnt; t += (int64_t)gridDim.x * blockDim.x)
-    mask[idx[t]] = 1;
-}
-
-// 64-bit uniform sort key per element; taken elements sort last.
+// Explore keys: a 63-bit uniform u per free element, stored as ~u so that the
+// n LARGEST stored keys are the n smallest u (ties by index, as a stable
+// ascending sort); taken elements store 0 and are never chosen.
 __global__ void k_explore_keys(const uint8_t* __restrict__ taken, int64_t m, uint32_t k0, uint32_t k1,
                                uint64_t frame_index, uint64_t* __restrict__ keys) {
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < m; x += (int64_t)gridDim.x * blockDim.x) {
     if (taken[x]) {
-      keys[x] = ~0ull;
+      keys[x] = 0ull;
     } else {
       const u32x4 rr = philox4x32_10(u32x4{(uint32_t)x, (uint32_t)(x >> 32), (uint32_t)frame_index,
                                            ((uint32_t)(frame_index >> 32) & 0xFFFFFFu) | (kDomMask << 24)},
                                      k0, k1);
-      keys[x] = ((uint64_t)(rr.x >> 1) << 32) | rr.y;  // < 2^63: always below a taken element
+      keys[x] = ~(((uint64_t)(rr.x >> 1) << 32) | rr.y);  // u < 2^63: ~u >= 2^63 > a taken element's 0
     }
   }
 }
@@ -110,54 +110,39 @@ int adaptive_mask(const double* resid, int64_t m, int64_t budget, int64_t n_expl
                   uint64_t frame_index, uint8_t* mask, int* status, cudaStream_t st) {
   *status = 0;
   if (m <= 0) return PB_OK;
-  // scratch: flags, (keys, idx) in/out pairs
-  unsigned* flags = nullptr;
-  double *kd_in = nullptr, *kd_out = nullptr;
-  uint64_t *ku_in = nullptr, *ku_out = nullptr;
-  int64_t *iv_in = nullptr, *iv_out = nullptr;
-  void* temp = nullptr;
-  size_t tb_d = 0, tb_u = 0;
-  cub::DeviceRadixSort::SortPairsDescending(nullptr, tb_d, kd_in, kd_out, iv_in, iv_out, m, 0, 64, st);
-  cub::DeviceRadixSort::SortPairs(nullptr, tb_u, ku_in, ku_out, iv_in, iv_out, m, 0, 64, st);
-  const size_t tb = tb_d > tb_u ? tb_d : tb_u;
+  // scratch: flags, keys, selection scratch
+  char* buf = nullptr;
+  const size_t keys_off = 256, sel_off = keys_off + ((size_t)m * 8 + 255) / 256 * 256;
+  if (cudaMallocAsync((void**)&buf, sel_off + select_scratch_bytes(m), st) != cudaSuccess) {
+    set_error("adaptive mask: scratch allocation failed");
+    return PB_ECUDA;
+  }
+  unsigned* flags = (unsigned*)buf;
+  uint64_t* keys = (uint64_t*)(buf + keys_off);
+  void* sel = buf + sel_off;
   int rc = PB_OK;
-#define PB_M(ptr, bytes)                                                                   \
-  if (cudaMallocAsync((void**)&ptr, (bytes), st) != cudaSuccess) {                          \
-    set_error("adaptive mask: scratch allocation failed");                                  \
-    rc = PB_ECUDA;                                                                           \
-  }
-  PB_M(flags, 8) if (!rc) PB_M(ku_in, (size_t)m * 8) if (!rc) PB_M(ku_out, (size_t)m * 8)
-  if (!rc) PB_M(iv_in, (size_t)m * 8) if (!rc) PB_M(iv_out, (size_t)m * 8) if (!rc) PB_M(temp, tb ? tb : 16)
-#undef PB_M
+  unsigned hflags[2] = {0, 0};
+  cudaMemsetAsync(flags, 0, 8, st);
+  k_adaptive_check<<<grid_for(m), 256, 0, st>>>(resid, m, flags);
+  cudaMemcpyAsync(hflags, flags, 8, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) { set_error("adaptive mask: check failed"); rc = PB_ECUDA; }
+  else if (hflags[1]) { set_error("residual map must be non-negative and finite"); rc = PB_EVALUE; }
   if (!rc) {
-    kd_out = (double*)ku_out;  // reuse: the double keys are only an output of the first sort
-    unsigned hflags[2] = {0, 0};
-    cudaMemsetAsync(flags, 0, 8, st);
-    k_adaptive_check<<<grid_for(m), 256, 0, st>>>(resid, m, flags);
-    cudaMemcpyAsync(hflags, flags, 8, cudaMemcpyDeviceToHost, st);
-    if (cudaStreamSynchronize(st) != cudaSuccess) { set_error("adaptive mask: check failed"); rc = PB_ECUDA; }
-    else if (hflags[1]) { set_error("residual map must be non-negative and finite"); rc = PB_EVALUE; }
-    if (!rc) {
-      cudaMemsetAsync(mask, 0, (size_t)m, st);
-      k_iota<<<grid_for(m), 256, 0, st>>>(iv_in, m);
-      if (!hflags[0]) n_exploit = 0;  // all-zero residual: uniform sampling (status 1)
-      *status = hflags[0] ? 0 : 1;
-      if (n_exploit > 0) {
-        cub::DeviceRadixSort::SortPairsDescending(temp, tb_d, resid, kd_out, iv_in, iv_out, m, 0, 64, st);
-        k_mark<<<grid_for(n_exploit), 256, 0, st>>>(iv_out, n_exploit, mask);
-      }
-      const int64_t n_explore = budget - n_exploit;
-      if (n_explore > 0) {
-        k_explore_keys<<<grid_for(m), 256, 0, st>>>(mask, m, k0, k1, frame_index, ku_in);
-        cub::DeviceRadixSort::SortPairs(temp, tb_u, ku_in, ku_out, iv_in, iv_out, m, 0, 64, st);
-        k_mark<<<grid_for(n_explore), 256, 0, st>>>(iv_out, n_explore, mask);
-      }
-      if (cudaGetLastError() != cudaSuccess) { set_error("adaptive mask: kernel launch failed"); rc = PB_ECUDA; }
+    cudaMemsetAsync(mask, 0, (size_t)m, st);
+    if (!hflags[0]) n_exploit = 0;  // all-zero residual: uniform sampling (status 1)
+    *status = hflags[0] ? 0 : 1;
+    if (n_exploit > 0) {
+      k_resid_keys<<<grid_for(m), 256, 0, st>>>(resid, m, keys);
+      rc = select_top(keys, m, n_exploit, sel, mask, nullptr, st);
     }
+    const int64_t n_explore = budget - n_exploit;
+    if (!rc && n_explore > 0) {
+      k_explore_keys<<<grid_for(m), 256, 0, st>>>(mask, m, k0, k1, frame_index, keys);
+      rc = select_top(keys, m, n_explore, sel, mask, nullptr, st);
+    }
+    if (!rc && cudaGetLastError() != cudaSuccess) { set_error("adaptive mask: kernel launch failed"); rc = PB_ECUDA; }
   }
-  void* bufs[] = {flags, ku_in, ku_out, iv_in, iv_out, temp};
-  for (void* b : bufs)
-    if (b) cudaFreeAsync(b, st);
+  cudaFreeAsync(buf, st);
   return rc;
 }
 
@@ -247,13 +232,27 @@ int launch_atlas(const float* atoms, const double* pi, int k, int rank, const in
 namespace pb {
 
 // ---- data-mode dictionary seeding (bpfa.py:126-134) ------------------------
-// order = argsort(-counts, kind="stable"): a stable ascending radix sort of
-// (P - count, patch) pairs; atom j <- patch order[j], unit-normalized (norm in
+// order = argsort(-counts, kind="stable")[:K]: the K largest counts (ties by
+// patch index) by radix select (pb_select.cu), then ONE CTA ranks those K by
+// (count desc, index asc); atom j <- patch order[j], unit-normalized (norm in
 // f64), zero-norm candidates keep their prior atom; atoms past min(K, N) too.
-__global__ void k_seed_keys(const int32_t* counts, int64_t n, int p, uint32_t* keys, int32_t* idx) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    keys[i] = (uint32_t)(p - counts[i]);
-    idx[i] = (int32_t)i;
+__global__ void k_seed_keys(const int32_t* counts, int64_t n, uint64_t* keys) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    keys[i] = (uint64_t)(uint32_t)counts[i];
+}
+
+__global__ void __launch_bounds__(1024) k_seed_order(const int32_t* __restrict__ sel, int take,
+                                                     const int32_t* __restrict__ counts, int32_t* __restrict__ order) {
+  for (int a = threadIdx.x; a < take; a += blockDim.x) {
+    const int32_t ia = sel[a];
+    const int32_t ca = counts[ia];
+    int rank = 0;
+    for (int b = 0; b < take; ++b) {
+      const int32_t ib = sel[b];
+      const int32_t cb = counts[ib];
+      rank += (cb > ca || (cb == ca && ib < ia)) ? 1 : 0;
+    }
+    order[rank] = ia;
   }
 }
 
@@ -277,30 +276,25 @@ __global__ void __launch_bounds__(128) k_data_atoms(const float* values_pn, int6
 
 int launch_data_atoms(const float* values_pn, const int32_t* counts, int64_t n, int p, int k, float* atoms,
                       cudaStream_t st) {
+  (void)p;
   if (n < 1 || k < 1) return PB_OK;
   if (n >= ((int64_t)1 << 31)) { set_error("data-mode seeding supports < 2^31 patches"); return PB_EUNSUPPORTED; }
   const int take = (int)(k < n ? k : n);
-  int bits = 1;
-  while ((1 << bits) <= p) ++bits;
-  uint32_t *kin = nullptr, *kout = nullptr;
-  int32_t *iin = nullptr, *iout = nullptr;
-  void* tmp = nullptr;
-  size_t tmp_bytes = 0;
-  PB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kin, kout, iin, iout, (int)n, 0, bits, st));
+  const size_t al = 256;
+  const size_t keys_b = ((size_t)n * 8 + al - 1) / al * al, list_b = ((size_t)take * 4 + al - 1) / al * al;
   char* buf = nullptr;
-  const size_t al = 256, nb = ((size_t)n * 4 + al - 1) / al * al;
-  PB_CUDA_TRY(cudaMallocAsync((void**)&buf, 4 * nb + tmp_bytes, st));
-  kin = (uint32_t*)buf; kout = (uint32_t*)(buf + nb); iin = (int32_t*)(buf + 2 * nb); iout = (int32_t*)(buf + 3 * nb);
-  tmp = buf + 4 * nb;
+  PB_CUDA_TRY(cudaMallocAsync((void**)&buf, keys_b + 2 * list_b + select_scratch_bytes(n), st));
+  uint64_t* keys = (uint64_t*)buf;
+  int32_t* sel = (int32_t*)(buf + keys_b);
+  int32_t* order = (int32_t*)(buf + keys_b + list_b);
+  void* scratch = buf + keys_b + 2 * list_b;
   int64_t g = (n + 255) / 256;
   if (g > 148 * 8) g = 148 * 8;
-  k_seed_keys<<<(unsigned)g, 256, 0, st>>>(counts, n, p, kin, iin);
-  int rc = PB_OK;
-  if (cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, iin, iout, (int)n, 0, bits, st) != cudaSuccess) {
-    set_error("data-mode seeding sort failed");
-    rc = PB_ECUDA;
-  } else {
-    k_data_atoms<<<take, 128, 0, st>>>(values_pn, n, p, iout, atoms);
+  k_seed_keys<<<(unsigned)g, 256, 0, st>>>(counts, n, keys);
+  int rc = select_top(keys, n, take, scratch, nullptr, sel, st);
+  if (!rc) {
+    k_seed_order<<<1, 1024, 0, st>>>(sel, take, counts, order);
+    k_data_atoms<<<take, 128, 0, st>>>(values_pn, n, p, order, atoms);
     if (cudaGetLastError() != cudaSuccess) { set_error("k_data_atoms launch failed"); rc = PB_ECUDA; }
   }
   cudaFreeAsync(buf, st);

@@ -28,6 +28,14 @@ int launch_data_atoms(const float* values_pn, const int32_t* counts, int64_t n, 
 int adaptive_mask(const double* resid, int64_t m, int64_t budget, int64_t n_exploit, uint32_t k0, uint32_t k1,
                   uint64_t frame_index, uint8_t* mask, int* status, cudaStream_t st);
 
+// pb_select.cu: the n largest of keys[0, m), ties by lowest index (1 <= n <= m):
+// mark[x] = 1 for each selected x (if mark; other entries untouched) and/or the
+// selected indices appended to list (if list; unordered).  scratch: device
+// memory of select_scratch_bytes(m).
+size_t select_scratch_bytes(int64_t m);
+int select_top(const uint64_t* keys, int64_t m, int64_t n, void* scratch, uint8_t* mark, int32_t* list,
+               cudaStream_t st);
+
 // server.py:84-120: atlas geometry and render (canvas f64 and/or uint8, device)
 int atlas_geometry(int k, int rank, const int32_t* shape, int& b0, int& b1, int& inner, int& grid, int64_t& h,
                    int64_t& w);

@@ -162,3 +162,23 @@ def test_atlas_on_device_matches_reference(golden, cuda_device):
         lp.submit_frame(inputs.synthetic_frames((24, 24), 1, seed=0)[0], np.ones((24, 24), bool))
         atoms, pi, _ = lp.dictionary()
         assert np.array_equal(lp.render_atlas(), osm.quantize_panel(osm.render_dictionary_atlas(atoms, pi, (6, 6))))
+
+
+@pytest.mark.parametrize("shape,levels,ratio", [((1, 1), 3, 1.0), ((33, 47), 4, 0.3), ((512, 512), 7, 0.25),
+                                                ((1000, 1100), 1000, 0.1), ((640, 480), 2, 0.5)])
+def test_adaptive_exploit_select_ties_exact(cuda_device, shape, levels, ratio):
+    """Pure exploit on residuals with heavy ties (few distinct levels, zeros,
+    -0.0): the device radix select (pb_select.cu) takes exactly the first
+    n_exploit of the reference's argsort(-r, kind="stable") — every key above
+    the threshold and the lowest-index ties at it."""
+    rng = np.random.default_rng(levels)
+    res = rng.integers(0, levels, size=shape).astype(np.float64) * 0.37
+    res[rng.random(shape) < 0.05] = -0.0
+    if res.max() == 0:
+        res.flat[0] = 1.0
+    mask, all_zero = adaptive_mask(res, ratio, 1.0, 0, 0)
+    budget, n_exploit = osm.adaptive_split(ratio, 1.0, res.size)
+    want = np.zeros(res.size, bool)
+    want[np.argsort(-res.ravel(), kind="stable")[:n_exploit]] = True
+    assert not all_zero and n_exploit == budget
+    assert np.array_equal(mask.ravel(), want)
