@@ -447,7 +447,8 @@ __global__ void __launch_bounds__(256) k_reconstitute2d(Geo2 g, const float* __r
 // (bit-identical to k_reconstitute2d, tests/test_gpu_patches.py).
 // Measured (configs[1], tools/patch_timing.py): gather form 0.187 ms -> all
 // rows staged at once 0.16 -> double-buffered rows, kOW 128: 0.140 -> kOW 256:
-// 0.121 ms; a three-stage ring measured 0.138.
+// 0.121 ms; a three-stage ring measured 0.138, and 16-byte cp.async chunks (runs
+// staged at their global 16-byte alignment, a per-run shift in the sum) 0.163.
 constexpr int kOW = 256;
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
