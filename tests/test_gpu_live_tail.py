@@ -165,7 +165,8 @@ def test_atlas_on_device_matches_reference(golden, cuda_device):
 
 
 @pytest.mark.parametrize("shape,levels,ratio", [((1, 1), 3, 1.0), ((33, 47), 4, 0.3), ((512, 512), 7, 0.25),
-                                                ((1000, 1100), 1000, 0.1), ((640, 480), 2, 0.5)])
+                                                ((1000, 1100), 1000, 0.1), ((640, 480), 2, 0.5),
+                                                ((257, 129), 5, 1.0), ((3000, 3000), 50, 0.0005)])
 def test_adaptive_exploit_select_ties_exact(cuda_device, shape, levels, ratio):
     """Pure exploit on residuals with heavy ties (few distinct levels, zeros,
     -0.0): the device radix select (pb_select.cu) takes exactly the first
