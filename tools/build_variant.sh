@@ -12,7 +12,7 @@ cp $C/*.cu $C/*.cuh $T/
 for e in "$@"; do sed -i "$e" $T/pb_compact.cu; done
 mkdir -p $O/variants
 objs=""
-for f in pb_patches pb_sweep pb_index pb_compact pb_live pb_compose_tc pb_nccl pb_entry pb_capi; do
+for f in pb_patches pb_sweep pb_index pb_compact pb_live pb_select pb_compose_tc pb_nccl pb_entry pb_capi; do
   nvcc -DPB_TUNING -O3 -std=c++17 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC -Xptxas -v \
     --expt-relaxed-constexpr -I$R/include -I$C -c $T/$f.cu -o $T/$f.o 2> $T/$f.ptxas.log &
   objs="$objs $T/$f.o"
