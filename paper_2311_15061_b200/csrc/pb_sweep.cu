@@ -147,8 +147,13 @@ __device__ double log_gamma_draw(DevRng& rng, double shape) {
 __global__ void k_draw_pi_gamma(double* pi, const int32_t* m_count, SweepScalars* sc, int k_len, int64_t n,
                                 int64_t n_obs, double ca, double cb, double ws, double wr, double ns, double nr,
                                 uint32_t key0, uint32_t key1) {
+  // warps 0..nw-2 draw pi (one atom per thread), the last warp's lane 0 the two
+  // gamma draws concurrently (the same streams as drawing them after pi)
   const int epoch = sc->epoch + 1;
-  for (int k = threadIdx.x; k < k_len; k += blockDim.x) {
+  __syncthreads();   // every thread has read the epoch before it is advanced below
+  const int npi = blockDim.x - 32;
+  if (threadIdx.x < npi) {
+  for (int k = threadIdx.x; k < k_len; k += npi) {
     const double m = (double)m_count[k];
     const double sa = fmax(ca / k_len + m, 1e-12);
     const double sb = fmax(cb * (k_len - 1) / k_len + (double)n - m, 1e-12);
@@ -157,7 +162,7 @@ __global__ void k_draw_pi_gamma(double* pi, const int32_t* m_count, SweepScalars
     const double mx = fmax(la, lb);
     pi[k] = exp(la - mx) / (exp(la - mx) + exp(lb - mx));
   }
-  if (threadIdx.x == 0) {
+  } else if (threadIdx.x == npi) {
     DevRng r{0u, 0u, (uint32_t)epoch, kDomGamma << 24, key0, key1, {}, 4};
     const double sh_s = ws + 0.5 * (double)n * k_len;
     const double gs = exp(log_gamma_draw(r, sh_s)) / (wr + 0.5 * sc->sq_w);
@@ -405,7 +410,7 @@ int launch_finish_stats(const double* block_sums, int nblocks, SweepScalars* sc,
 
 int launch_draw_pi_gamma(double* pi, const int32_t* m_count, SweepScalars* sc, int k_len, int64_t n, int64_t n_obs,
                          const double* hyper6, uint32_t key0, uint32_t key1, cudaStream_t st) {
-  k_draw_pi_gamma<<<1, 256, 0, st>>>(pi, m_count, sc, k_len, n, n_obs, hyper6[0], hyper6[1], hyper6[2], hyper6[3],
+  k_draw_pi_gamma<<<1, 256 + 32, 0, st>>>(pi, m_count, sc, k_len, n, n_obs, hyper6[0], hyper6[1], hyper6[2], hyper6[3],
                                      hyper6[4], hyper6[5], key0, key1);
   PB_LAUNCH_CHECK();
   return PB_OK;
