@@ -780,9 +780,26 @@ int pb_problem_submit_frame_ex(pb_problem* pr, const double* frame_host, const u
   // the observed-element index follows the mask (a device-generated mask is
   // already resident but still needs its index)
   const bool new_mask = mask_changed || !pr->index_valid;
-  int rc = launch_extract(pr->grid, pr->frame, 1, pr->mask, pr->desc.mean_subtract, pr->values, pr->obs, pr->means,
-                          pr->counts, st);
-  if (rc) return rc;
+  // Cached mask, 2-D frame: the observed values go from the frame straight into
+  // the index's compact order (k_refresh_frame2d) — unless a cold data-mode
+  // seeding will read the dense values, or the frame is wide enough that the
+  // extraction would take the row-tile kernel (another summation order of the
+  // means).  Otherwise: the dense extraction, then the index build / refresh.
+  const bool cold = !pr->have_state || !pr->desc.warm_start;
+  const bool fused = !new_mask && pr->grid.rank == 2 && pr->grid.gcount[1] < 768 &&
+                     !(cold && pr->desc.init_mode == PB_INIT_DATA && pr->desc.freeze_dict);
+  int rc = PB_OK;
+  if (fused) {
+    PatchIndex ix;
+    index_view(&pr->index, ix);
+    rc = launch_refresh_frame2d(ix, pr->frame, pr->grid.tshape[1], pr->grid.gcount[1], pr->grid.bshape[1],
+                                pr->grid.step[0], pr->grid.step[1], pr->desc.mean_subtract, pr->counts, pr->means, st);
+    if (rc) return rc;
+  } else {
+    rc = launch_extract(pr->grid, pr->frame, 1, pr->mask, pr->desc.mean_subtract, pr->values, pr->obs, pr->means,
+                        pr->counts, st);
+    if (rc) return rc;
+  }
   if (new_mask) {
     if ((rc = launch_sum_counts(pr->counts, n, pr->nobs_dev, st))) return rc;
     unsigned long long nobs = 0;
@@ -800,7 +817,7 @@ int pb_problem_submit_frame_ex(pb_problem* pr, const double* frame_host, const u
     pr->index.n = n; pr->index.p = pr->p; pr->index.nnz = pr->n_obs;
     if ((rc = pb_build_index(&pr->index, pr->obs, pr->values, pr->counts, st))) return rc;
     pr->index_valid = true;
-  } else {
+  } else if (!fused) {
     if ((rc = pb_index_refresh_values(&pr->index, pr->values, pr->counts, st))) return rc;
   }
   {  // epoch workspace for this mask's observed count and the current K

@@ -1,3 +1,4 @@
+#include <algorithm>
 // pb200 — observed-element index of a patch matrix (built once per mask).
 //
 // The sweep never touches unobserved elements: every conditional of the
@@ -174,6 +175,52 @@ __global__ void k_scatter_x(const float* __restrict__ values, const int32_t* __r
     const int c = counts[i];
     for (int j = 0; j < c; ++j) x_csc[csr_pos[r + j]] = values[(int64_t)csr_p[r + j] * n + i];
   }
+}
+
+// Live frame under a cached mask, rank 2: the observed values straight from
+// the frame into the compact order (csr_p: the patch's observed offsets in
+// ascending order; csr_pos: their compact positions), with the observed-only
+// mean — no dense (P, N) values / flags written and re-read.  The mean sums in
+// ascending offset order, as k_extract2d / k_extract do (bit-identical to
+// extraction + k_scatter_x when the extraction would take one of those).
+__global__ void k_refresh_frame2d(const double* __restrict__ frame, int64_t m1, int64_t gc1, int b1, int s0, int s1,
+                                  int mean_subtract, const int32_t* __restrict__ counts,
+                                  const int64_t* __restrict__ rowptr, const uint16_t* __restrict__ csr_p,
+                                  const uint32_t* __restrict__ csr_pos, int64_t n, float* __restrict__ x_csc,
+                                  float* __restrict__ means) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t gy = i / gc1, gx = i - gy * gc1;
+    const double* f = frame + gy * s0 * m1 + gx * s1;
+    const int64_t r = rowptr[i];
+    const int c = counts[i];
+    double mean = 0.0;
+    if (mean_subtract && c > 0) {
+      double sum = 0.0;
+      for (int j = 0; j < c; ++j) {
+        const int pe = csr_p[r + j];
+        const int a = pe / b1;
+        sum += f[a * m1 + (pe - a * b1)];
+      }
+      mean = sum / (double)c;
+    }
+    means[i] = (float)mean;
+    for (int j = 0; j < c; ++j) {
+      const int pe = csr_p[r + j];
+      const int a = pe / b1;
+      x_csc[csr_pos[r + j]] = (float)(f[a * m1 + (pe - a * b1)] - mean);
+    }
+  }
+}
+
+int launch_refresh_frame2d(const PatchIndex& ix, const double* frame, int64_t m1, int64_t gc1, int b1, int s0, int s1,
+                           int mean_subtract, const int32_t* counts, float* means, cudaStream_t st) {
+  int64_t nb = ceil_div(ix.n, 256);
+  if (nb > 148 * 16) nb = 148 * 16;
+  k_refresh_frame2d<<<(unsigned)std::max<int64_t>(nb, 1), 256, 0, st>>>(frame, m1, gc1, b1, s0, s1, mean_subtract,
+                                                                      counts, ix.rowptr, ix.csr_p, ix.csr_pos, ix.n,
+                                                                      ix.x_csc, means);
+  PB_LAUNCH_CHECK();
+  return PB_OK;
 }
 
 int index_bytes(int64_t n, int p, int64_t nnz_upper, size_t* out) {

@@ -66,6 +66,10 @@ void carve_index(PatchIndex& ix, char* base, int64_t n, int p, int64_t nnz);
 int launch_build_index(PatchIndex& ix, const uint8_t* obs, const float* values, const int32_t* counts,
                        cudaStream_t st);
 int launch_scatter_x(const PatchIndex& ix, const float* values, const int32_t* counts, cudaStream_t st);
+// Cached-mask live frame, rank 2: observed values (and means) from the frame
+// straight into the index's compact order (no dense extraction).
+int launch_refresh_frame2d(const PatchIndex& ix, const double* frame, int64_t m1, int64_t gc1, int b1, int s0, int s1,
+                           int mean_subtract, const int32_t* counts, float* means, cudaStream_t st);
 int launch_count_hist(const PatchIndex& ix, const int32_t* counts, cudaStream_t st);
 int launch_outliers(const PatchIndex& ix, const int32_t* counts, int split, cudaStream_t st);
 
