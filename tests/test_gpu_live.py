@@ -178,3 +178,24 @@ def test_native_frozen_data_init_matches_oracle(cuda_device):
         assert np.abs(atoms - want_atoms).max() <= 1e-6, rng   # data-seeded and frozen
         if rng == "numpy":
             assert np.abs(rec - orec).max() <= 1e-3
+
+
+def test_cached_mask_frame_refresh_bit_identical_to_extraction(cuda_device):
+    """A cached mask sends a 2-D frame's observed values straight from the frame
+    into the compact index order (k_refresh_frame2d) instead of the dense
+    extraction + value refresh: the same bits.  Problem A keeps one mask (fused
+    refresh from its second frame on); problem B re-draws the same mask before
+    every frame (pure-explore adaptive mask at a fixed frame index), which
+    invalidates its index, so B always extracts densely."""
+    from paper_2311_15061_b200.live import LiveProblem
+
+    frames = inputs.synthetic_frames((72, 80), 4, seed=2)
+    hp = gb.Hyperparams(num_atoms=16)
+    with LiveProblem((72, 80), pp.PatchSpec((8, 8)), hp, seed=4, epochs_per_frame=2) as a, \
+            LiveProblem((72, 80), pp.PatchSpec((8, 8)), hp, seed=4, epochs_per_frame=2) as b:
+        mask = b.adaptive_mask(0.3, 0.0, seed=1, frame_index=0)
+        for f in frames:
+            assert np.array_equal(b.adaptive_mask(0.3, 0.0, seed=1, frame_index=0), mask)
+            ra = a.submit_frame(f, mask).reconstruction
+            rb = b.submit_frame(f, mask).reconstruction
+            assert np.array_equal(ra, rb)
