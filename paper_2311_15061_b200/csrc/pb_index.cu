@@ -183,11 +183,13 @@ __global__ void k_scatter_x(const float* __restrict__ values, const int32_t* __r
 // mean — no dense (P, N) values / flags written and re-read.  The mean sums in
 // ascending offset order, as k_extract2d / k_extract do (bit-identical to
 // extraction + k_scatter_x when the extraction would take one of those).
-__global__ void k_refresh_frame2d(const double* __restrict__ frame, int64_t m1, int64_t gc1, int b1, int s0, int s1,
+template <int CB1>   // CB1 > 0: patch width known at compile time (offset split by a constant)
+__global__ void k_refresh_frame2d(const double* __restrict__ frame, int64_t m1, int64_t gc1, int b1_rt, int s0, int s1,
                                   int mean_subtract, const int32_t* __restrict__ counts,
                                   const int64_t* __restrict__ rowptr, const uint16_t* __restrict__ csr_p,
                                   const uint32_t* __restrict__ csr_pos, int64_t n, float* __restrict__ x_csc,
                                   float* __restrict__ means) {
+  const int b1 = CB1 > 0 ? CB1 : b1_rt;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t gy = i / gc1, gx = i - gy * gc1;
     const double* f = frame + gy * s0 * m1 + gx * s1;
@@ -216,9 +218,14 @@ int launch_refresh_frame2d(const PatchIndex& ix, const double* frame, int64_t m1
                            int mean_subtract, const int32_t* counts, float* means, cudaStream_t st) {
   int64_t nb = ceil_div(ix.n, 256);
   if (nb > 148 * 16) nb = 148 * 16;
-  k_refresh_frame2d<<<(unsigned)std::max<int64_t>(nb, 1), 256, 0, st>>>(frame, m1, gc1, b1, s0, s1, mean_subtract,
-                                                                      counts, ix.rowptr, ix.csr_p, ix.csr_pos, ix.n,
-                                                                      ix.x_csc, means);
+#define PB_RF(CB)                                                                                               \
+  k_refresh_frame2d<CB><<<(unsigned)std::max<int64_t>(nb, 1), 256, 0, st>>>(frame, m1, gc1, b1, s0, s1, mean_subtract, \
+                                                                          counts, ix.rowptr, ix.csr_p, ix.csr_pos,      \
+                                                                          ix.n, ix.x_csc, means)
+  if (b1 == 8) PB_RF(8);
+  else if (b1 == 10) PB_RF(10);
+  else PB_RF(0);
+#undef PB_RF
   PB_LAUNCH_CHECK();
   return PB_OK;
 }
